@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""femforge-b200 benchmark: assembled elements/sec (+ HBM GB/s) of the numeric
+FE assembly -- K0 zero-fill + K2 element kernel with CSR/RHS scatter into a
+prebuilt pattern (the reference's criterion-9 protocol, acceptance.cpp:292-327)
+-- on the BASELINE.json north-star workload: 3D P2 Poisson on the Kuhn 128^3
+cube (12,582,912 tets, 16,974,593 DOFs, 484,609,025 nnz).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config ns|c1|c2|c3|c4]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (row-block weak scaling)
+  python bench.py --impl reference ...                (reference CPU arm)
+
+One JSON line on rank 0. Multi-GPU: contiguous DOF row blocks, halo elements
+duplicated, no collective on the data path; the NCCL process
+group only provides the barrier and the max-over-ranks of the timings.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "ns": dict(dim=3, degree=2, n=128, form="poisson", quad=4,
+               workload="3D P2 Poisson tets, Kuhn 128^3 cube (north star, BASELINE.json)"),
+    "c1": dict(dim=2, degree=1, n=512, form="poisson", quad=3,
+               workload="2D P1 Poisson triangles, unit square 512x512 (BASELINE.json config 1)"),
+    "c2": dict(dim=3, degree=1, n=128, form="poisson", quad=4,
+               workload="3D P1 Poisson tets, Kuhn 128^3 cube (BASELINE.json config 2)"),
+    "c3": dict(dim=3, degree=2, n=96, form="poisson", quad=4,
+               workload="3D P2 Poisson tets, Kuhn 96^3 cube, stiffness + load (BASELINE.json config 3)"),
+    "c4": dict(dim=3, degree=2, n=96, form="varcoef", quad=14,
+               workload="3D P2 var-coef mass+stiffness+convection, Kuhn 96^3, 14-point rule (config 4)"),
+}
+METRIC = "assembled elements/sec (3D P2 Poisson tets)"
+UNIT = "elements/s"
+
+
+def make_mesh(ff, cfg):
+    if cfg["dim"] == 2:
+        coords, vconn = ff.unit_square_mesh(cfg["n"])
+        dconn, n_dofs = (vconn, coords.shape[0]) if cfg["degree"] == 1 else ff.p2_dofs(2, vconn, coords.shape[0])
+    else:
+        coords, vconn = ff.kuhn_mesh(cfg["n"])
+        dconn, n_dofs = (vconn, coords.shape[0]) if cfg["degree"] == 1 else ff.kuhn_p2_dofs(cfg["n"], vconn)
+    return coords, vconn, dconn, n_dofs
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(cfg, n_elems, n_vertices, n_rows, nnz):
+    """SURVEY.md §8d compulsory-traffic model: connectivity + coordinates +
+    CSR values written and col_idx read + row_ptr + RHS."""
+    k = {(2, 1): 3, (2, 2): 6, (3, 1): 4, (3, 2): 10}[(cfg["dim"], cfg["degree"])]
+    w_rp = 8 if nnz >= 2 ** 31 else 4
+    return n_elems * k * 4 + n_vertices * cfg["dim"] * 8 + nnz * 12 + (n_rows + 1) * w_rp + n_rows * 8
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: report why
+            self.nv, self.err = None, str(e)
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        names = {}
+        if self.nv:
+            nv = self.nv
+            for attr, name in [("nvmlClocksEventReasonHwSlowdown", "hw_slowdown"),
+                               ("nvmlClocksEventReasonHwThermalSlowdown", "hw_thermal_slowdown"),
+                               ("nvmlClocksEventReasonSwThermalSlowdown", "sw_thermal_slowdown"),
+                               ("nvmlClocksEventReasonSwPowerCap", "sw_power_cap"),
+                               ("nvmlClocksEventReasonHwPowerBrakeSlowdown", "hw_power_brake_slowdown")]:
+                if hasattr(nv, attr):
+                    names[getattr(nv, attr)] = name
+        while not self._stop.is_set():
+            if self.nv:
+                try:
+                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    for bit, name in names.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# reference CPU arm
+
+def cpu_reference_sample(cfg, target_s=2.0):
+    """Reference CPU assembly on the box's host cores (bounded sample).
+
+    oracle/_ref: the unmodified reference library (symbolic CAS + IR VM +
+    binary-search scatter + OpenMP/atomics, all host threads) driving a 3D
+    instantiation restated from fem.cpp:122-158 (2D configs run the reference
+    pipeline unchanged). Falls back to the C restatement (oracle/femoracle.c)
+    when the reference build is absent. Returns a callable step() and a
+    description."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    workers = os.cpu_count() or 1
+    n_s = 24 if cfg["dim"] == 3 else 256   # sample mesh of the same element type
+    if cfg["dim"] == 2:
+        coords, vconn = po.unit_square_mesh(n_s)
+        dconn, nd = vconn, coords.shape[0]
+    else:
+        coords, vconn = po.kuhn_mesh(n_s)
+        dconn, nd = (vconn, coords.shape[0]) if cfg["degree"] == 1 else po.p2_dofs_kuhn(n_s, vconn)
+    E = vconn.shape[0]
+    if po.ref_available() and not (cfg["dim"] == 2 and cfg["degree"] == 2):
+        h = po.RefHarness(cfg["dim"], cfg["degree"], coords, vconn, dconn, nd, cfg["form"], cfg["quad"])
+        kind = "reference"
+
+        def run(limit):
+            h.assemble(workers=workers, elem_limit=limit)
+    else:
+        rp, ci = po.build_pattern(dconn, nd)
+        kind = "port"
+
+        def run(limit):
+            po.assemble(cfg["form"], cfg["dim"], cfg["degree"], cfg["quad"], coords, vconn[:limit], dconn[:limit],
+                        rp, ci, workers=workers)
+    probe = min(E, 4 * workers * 64)
+    t0 = time.perf_counter()
+    run(probe)
+    rate = probe / max(time.perf_counter() - t0, 1e-6)
+    limit = int(min(E, max(probe, rate * target_s)))
+    desc = (f"{'reference lib (oracle/_ref)' if kind == 'reference' else 'C restatement (oracle/femoracle.c)'}: "
+            f"first {limit} of {E} elements of the same element type/form on a "
+            f"{'Kuhn ' + str(n_s) + '^3' if cfg['dim'] == 3 else str(n_s) + '^2'} mesh, "
+            f"{workers} OpenMP threads, pattern prebuilt (acceptance.cpp:295-296)")
+
+    def step():
+        t = time.perf_counter()
+        run(limit)
+        return limit, time.perf_counter() - t
+
+    return step, kind, workers, desc
+
+
+def run_reference_arm(args, cfg, rank, world):
+    if rank != 0:
+        return
+    step, kind, workers, desc = cpu_reference_sample(cfg, target_s=args.ref_step_s)
+    for _ in range(args.warmup):
+        step()
+    elems, secs = 0, 0.0
+    for _ in range(args.steps):
+        e, s = step()
+        elems += e
+        secs += s
+    value = elems / secs
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic structured mesh)",
+            "config": {"workload": cfg["workload"], "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="ns", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0, help="override mesh resolution")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-step-s", type=float, default=2.0)
+    ap.add_argument("--block", type=int, default=256)
+    ap.add_argument("--strategy", default="auto")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1802_03433_b200 import femforge as ff
+
+    coords, vconn, dconn, n_dofs = make_mesh(ff, cfg)
+    E = vconn.shape[0]
+    rb, re = ff.partition_rows(n_dofs, world, rank)
+    if world > 1:
+        ids = ff.select_elements(dconn, rb, re)   # owned + halo elements
+        vconn_l, dconn_l = np.ascontiguousarray(vconn[ids]), np.ascontiguousarray(dconn[ids])
+    else:
+        vconn_l, dconn_l = vconn, dconn
+    ctx = ff.Context(local)
+    bil, lin = ff.named_form(cfg["form"], cfg["dim"])
+    t = time.perf_counter()
+    form = ff.Form(ctx, cfg["dim"], cfg["degree"], bil, lin, quad_rule=cfg["quad"], strategy=args.strategy,
+                   block_size=args.block)
+    compile_ms = 1e3 * (time.perf_counter() - t)
+    mesh = ff.Mesh(ctx, cfg["dim"], coords, vconn_l, None if cfg["degree"] == 1 else dconn_l, n_dofs)
+    t = time.perf_counter()
+    pat = ff.Pattern(ctx, mesh, rb, re)
+    pattern_ms = 1e3 * (time.perf_counter() - t)
+    t = time.perf_counter()
+    pat.prepare(mesh)
+    plan_ms = 1e3 * (time.perf_counter() - t)
+    values = torch.empty(pat.nnz, dtype=torch.float64, device="cuda")
+    rhs = torch.empty(pat.n_rows, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    l2_bytes = 126 * 2 ** 20
+    need_flush = values.numel() * 8 < 2 * l2_bytes
+    flush = torch.empty(2 * l2_bytes // 4, dtype=torch.int32, device="cuda") if need_flush else None
+
+    def step():
+        ff.assemble_device(form, mesh, pat, values.data_ptr(), rhs.data_ptr(), sp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.check()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(i)
+            ev[i][0].record(stream)
+            ff.assemble_device_ex(form, mesh, pat, values.data_ptr(), rhs.data_ptr(), sp, ff.FF_ZERO_ONLY)
+            ev[i][1].record(stream)
+            ff.assemble_device_ex(form, mesh, pat, values.data_ptr(), rhs.data_ptr(), sp, ff.FF_SKIP_ZERO)
+            ev[i][2].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.check()  # device-side errors (degenerate element / missing column) fail the run
+    step_ms = float(np.mean([a.elapsed_time(c) for a, b, c in ev]))
+    k0_ms = float(np.mean([a.elapsed_time(b) for a, b, c in ev]))
+    k2_ms = float(np.mean([b.elapsed_time(c) for a, b, c in ev]))
+    times = torch.tensor([step_ms, k0_ms, k2_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    step_ms, k0_ms, k2_ms = times.tolist()
+
+    # end to end through the public API: pinned host inputs -> H2D, pattern
+    # re-validation, K0 + K2, D2H of values and rhs, every step
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+        hc, hv = pin(coords), pin(vconn_l)
+        hd = pin(dconn_l) if cfg["degree"] > 1 else None
+        hval = torch.empty(pat.nnz, dtype=torch.float64).pin_memory().numpy()
+        hrhs = torch.empty(pat.n_rows, dtype=torch.float64).pin_memory().numpy()
+        ff.assemble(form, mesh, pat, hc, hv, hd, hval, hrhs)  # warm
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            ff.assemble(form, mesh, pat, hc, hv, hd, hval, hrhs)
+        e2e_s = torch.tensor([(time.perf_counter() - t) / args.e2e_steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        h2d = hc.nbytes + hv.nbytes + (hd.nbytes if hd is not None else 0)
+        e2e = {"value": E / float(e2e_s), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(hval.nbytes + hrhs.nbytes), "ms_per_step": 1e3 * float(e2e_s)}
+
+    nnz_tot = torch.tensor([pat.nnz], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(nnz_tot)
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    peak, peak_src = measured_peaks()
+    B = algorithmic_bytes(cfg, vconn_l.shape[0], coords.shape[0], pat.n_rows, pat.nnz)
+    achieved = B / (k2_ms * 1e-3) / 1e9
+    info = form.info
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{cfg['n']}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            stepf, kind, workers, desc = cpu_reference_sample(cfg)
+            e, s = stepf()
+            cpu = {"value": e / s, "unit": UNIT, "cores": workers, "kind": kind, "sample": desc}
+        except Exception as ex:  # never let the baseline hide the GPU number
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
+    value = E / (step_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic structured mesh)",
+        "config": {"workload": cfg["workload"], "n": cfg["n"], "elements": int(E), "dofs": int(n_dofs),
+                   "nnz": int(nnz_tot.item()), "form": cfg["form"], "quad_rule": cfg["quad"],
+                   "parallelism": f"row-blocks x{world} (halo elements duplicated, no collective)",
+                   "l2": "flushed (256 MiB write) between steps" if need_flush else
+                         f"inputs > L2 (CSR values {values.numel() * 8 / 1e9:.2f} GB)",
+                   "step": "K0 zero-fill + K2 element kernel/atomic scatter, inputs resident in HBM",
+                   "k0_ms": k0_ms, "k2_ms": k2_ms, "pattern_build_ms": pattern_ms, "slot_plan_ms": plan_ms,
+                   "nvrtc_compile_ms": compile_ms, "strategy": info["strategy"], "registers": info["registers"],
+                   "flops_per_element": info["flops_per_element"],
+                   "hbm_gbs_step": B / (step_ms * 1e-3) / 1e9},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "ff_assemble_atomic (K2)",
+                     "bytes_per_launch": int(B), "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps,  # K0 + K2 per step (the L2 flush is a torch fill)
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

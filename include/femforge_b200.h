@@ -1,0 +1,171 @@
+/* femforge_b200.h -- the drop-in C ABI of the femforge-b200 assembly engine.
+ *
+ * The hot path of the reference (femforge, arXiv:1802.03433, mounted at
+ * /root/reference/proj) sits behind these C++ entry points, which this ABI
+ * replaces:
+ *
+ *   device::flatten_mesh     include/femforge/device/device.hpp:63   -> ff_mesh_create
+ *   device::build_sparsity   include/femforge/device/device.hpp:74   -> ff_pattern_build
+ *   codegen::compile_form /  include/femforge/codegen/kernel.hpp:65  -> ff_form_create
+ *   codegen::emit_source     include/femforge/codegen/kernel.hpp:76  -> ff_form_source / ff_compile
+ *   device::assemble_sparse  include/femforge/device/device.hpp:143-153 -> ff_assemble (host
+ *                            buffers) / ff_assemble_device (device-resident, async)
+ *   device::FormEvaluator    include/femforge/device/device.hpp:97-102 -> ff_form (the
+ *                            compiled element kernel is the evaluator plug-in)
+ *
+ * Conventions: C linkage, plain pointers and sizes, no exceptions across the
+ * ABI. Every function returns an ff_status (0 = FF_OK); on failure the
+ * thread-local ff_last_error() carries the reference's message (e.g.
+ * "degenerate element 7 (|det J| <= 1e-14)", "column 5 not present in
+ * sparsity row 0 (inconsistent sparsity pattern)"). Caller-owned host arrays
+ * go in, caller-allocated outputs come back; library-owned device memory
+ * lives behind handles. Handles are immutable after creation except the
+ * per-context stream; use one context per device and per host thread.
+ *
+ * Output layout: CSR with int64 row_ptr (n_rows+1), int32 col_idx (nnz,
+ * sorted ascending within each row, diagonal always present -- device.cpp:70),
+ * fp64 values (nnz) and fp64 rhs (n_rows). A row block [row_begin, row_end)
+ * selects the rows a device owns (multi-GPU row partitioning).
+ */
+#ifndef FEMFORGE_B200_H
+#define FEMFORGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ff_status {
+  FF_OK = 0,
+  FF_E_ARG = -1,        /* invalid argument / launch limit (DeviceError in device.cpp:90-97) */
+  FF_E_DEGENERATE = -2, /* |det J| <= 1e-14; lowest element index in the message / stats */
+  FF_E_PATTERN = -3,    /* column not present in sparsity row (device.cpp:285-288) */
+  FF_E_NVRTC = -4,      /* runtime compilation failed (log in ff_last_error) */
+  FF_E_CUDA = -5,       /* CUDA runtime error */
+  FF_E_FORM = -6,       /* weak-form error (FormError / CodegenError) */
+  FF_E_MESH = -7,       /* mesh validation error (MeshError) */
+  FF_E_SYMBOLIC = -8,   /* parse / symbolic error (ParseError with offset) */
+  FF_E_NOMEM = -9       /* device or host allocation failed */
+} ff_status;
+
+typedef struct ff_ctx ff_ctx;
+typedef struct ff_form ff_form;
+typedef struct ff_mesh ff_mesh;
+typedef struct ff_pattern ff_pattern;
+
+/* element body strategies (codegen::Strategy) */
+enum { FF_STRATEGY_AUTO = 0, FF_STRATEGY_TENSOR = 1, FF_STRATEGY_POINTWISE = 2 };
+
+typedef struct ff_form_desc {
+  int dim;               /* 2 or 3 */
+  int degree;            /* Lagrange degree 1 or 2 */
+  int quad_rule;         /* 0 = default (2D: reference 3-point rule; 3D: 4-point degree 2) */
+  int strategy;          /* FF_STRATEGY_* */
+  int block_size;        /* threads per CTA of the element kernel; 0 = 256 */
+  const char* bilinear;  /* integrand over u, u_x, u_y[, u_z], v, v_x, v_y[, v_z], x, y[, z] */
+  const char* linear;    /* integrand over v, x, y[, z] */
+} ff_form_desc;
+
+typedef struct ff_form_info {
+  int dim, degree, n_local, n_quad, strategy;
+  int n_invariants;      /* reference-tensor strategy: merged geometric invariants */
+  int n_unique_entries;  /* distinct local entries computed per element */
+  int64_t flops_per_element;
+  int registers;         /* per thread, from the loaded cubin (0 if not loaded) */
+  int shared_bytes;      /* static shared memory per CTA */
+  double compile_ms;     /* symbolic + emit + NVRTC */
+} ff_form_info;
+
+typedef struct ff_stats {
+  int64_t bad_element;   /* lowest degenerate element, or -1 */
+  int64_t bad_row;       /* lowest row with a missing column, or -1 */
+  double ms;             /* wall time of the call (host-synchronous entry points) */
+} ff_stats;
+
+/* ---- library / context ------------------------------------------------- */
+const char* ff_version(void);
+const char* ff_last_error(void);
+int ff_device_count(int* count);
+int ff_init(int device, ff_ctx** out);
+int ff_ctx_destroy(ff_ctx* ctx);
+int ff_ctx_synchronize(ff_ctx* ctx);
+void* ff_ctx_stream(ff_ctx* ctx); /* cudaStream_t of the context */
+
+/* ---- forms: weak form text -> symbolic -> CUDA source -> NVRTC (sm_100a) - */
+/* ctx may be NULL: compile-only (no device needed; ff_assemble* then fail). */
+int ff_form_create(ff_ctx* ctx, const ff_form_desc* desc, ff_form** out);
+/* Raw template route: compile caller-provided CUDA source that defines
+ * extern "C" __global__ ff_assemble_atomic with the template's signature. */
+int ff_compile(ff_ctx* ctx, const char* cuda_src, int dim, int degree, int block_size, ff_form** out,
+               char* log, size_t log_cap);
+int ff_form_source(const ff_form* form, char* buf, size_t cap, size_t* len);
+int ff_form_cubin(const ff_form* form, void* buf, size_t cap, size_t* len);
+int ff_form_info_get(const ff_form* form, ff_form_info* out);
+int ff_form_destroy(ff_form* form);
+
+/* ---- meshes: host arrays copied to the device --------------------------- */
+/* coords [n_vertices][dim] fp64; vconn [n_elems][dim+1] vertex ids;
+ * dconn [n_elems][dofs_per_elem] DOF ids (NULL for P1: dconn = vconn). */
+int ff_mesh_create(ff_ctx* ctx, int dim, const double* coords, int64_t n_vertices, const int32_t* vconn,
+                   int64_t n_elems, const int32_t* dconn, int32_t dofs_per_elem, int64_t n_dofs,
+                   ff_mesh** out);
+/* Re-upload coordinates/connectivity into an existing mesh (same sizes). */
+int ff_mesh_update(ff_mesh* mesh, const double* coords, const int32_t* vconn, const int32_t* dconn);
+int ff_mesh_destroy(ff_mesh* mesh);
+
+/* ---- sparsity (K1: sort + unique over element DOF pairs) ----------------- */
+int ff_pattern_build(ff_ctx* ctx, const ff_mesh* mesh, int64_t row_begin, int64_t row_end, ff_pattern** out);
+int ff_pattern_info(const ff_pattern* p, int64_t* n_rows, int64_t* nnz, int32_t* max_row_len);
+int ff_pattern_export(const ff_pattern* p, int64_t* row_ptr, int32_t* col_idx);
+/* ELL view for API parity with SparsityPattern (device.hpp:67-72): row_len
+ * [n_rows], row_cols [n_rows][max_nz] padded with -1. */
+int ff_pattern_export_ell(const ff_pattern* p, int32_t max_nz, int32_t* row_len, int32_t* row_cols);
+int ff_pattern_device(const ff_pattern* p, const int64_t** row_ptr, const int32_t** col_idx);
+int ff_pattern_destroy(ff_pattern* p);
+/* Element slot plan of (pattern, mesh): per element and local (a,b) the
+ * position of column dof[b] inside row dof[a]. Built on first assembly;
+ * exposed for tests. Returns FF_E_PATTERN on a missing column. */
+int ff_pattern_prepare(ff_pattern* p, const ff_mesh* mesh);
+
+/* ---- numeric assembly (K0 zero-fill + K2 element kernel with scatter) ---- */
+/* Device-resident, asynchronous on `stream` (NULL: the context stream).
+ * d_values [nnz], d_rhs [n_rows] are caller-owned device buffers. Errors
+ * detected on the device are reported by ff_check(). */
+int ff_assemble_device(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double* d_values, double* d_rhs,
+                       void* stream);
+/* Same with flags: FF_SKIP_ZERO (values/rhs already zero: K2 only) or
+ * FF_ZERO_ONLY (K0 only); lets callers time the two kernels separately. */
+enum { FF_SKIP_ZERO = 1, FF_ZERO_ONLY = 2 };
+int ff_assemble_device_ex(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double* d_values, double* d_rhs,
+                          void* stream, unsigned flags);
+/* Synchronises the context stream and reports device-side errors of the
+ * last ff_assemble_device (degenerate element / missing column). */
+int ff_check(ff_ctx* ctx, ff_stats* stats);
+/* End-to-end with host buffers (the reference call shape): uploads the
+ * mesh's coordinates and connectivity, assembles, downloads values and rhs,
+ * synchronously. Host buffers may be pageable or pinned. */
+int ff_assemble(ff_form* form, ff_mesh* mesh, ff_pattern* p, const double* coords, const int32_t* vconn,
+                const int32_t* dconn, double* values_out, double* rhs_out, ff_stats* stats);
+
+/* ---- host helpers (CPU only; no device needed) --------------------------- */
+/* meshgen.cpp:13-33 unit square; SURVEY.md Appendix C Kuhn cube + P2 lattice. */
+int ff_unit_square_mesh(int n, double* coords, int32_t* conn);
+int ff_kuhn_mesh(int n, double* coords, int32_t* conn);
+int ff_kuhn_p2_dofs(int n, const int32_t* vconn, int64_t n_elems, int32_t* dconn);
+/* Generic P2 numbering (vertices first, then edges by (min,max)); returns
+ * n_dofs through *n_dofs. */
+int ff_p2_dofs(int dim, const int32_t* vconn, int64_t n_elems, int64_t n_vertices, int32_t* dconn,
+               int64_t* n_dofs);
+/* Contiguous row block of part `part` of `n_parts` (balanced by DOF count). */
+int ff_partition_rows(int64_t n_dofs, int n_parts, int part, int64_t* row_begin, int64_t* row_end);
+/* Elements with at least one DOF in [row_begin,row_end) (owned + halo), in
+ * ascending order; ids may be NULL to count only. */
+int ff_select_elements(const int32_t* dconn, int64_t n_elems, int32_t dofs_per_elem, int64_t row_begin,
+                       int64_t row_end, int64_t* ids, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEMFORGE_B200_H */

@@ -1,0 +1,598 @@
+// The C ABI (include/femforge_b200.h): handles, error translation, and the
+// host orchestration of K0 (zero-fill), K1 (pattern), the slot plan and K2
+// (the NVRTC element kernel with its scatter).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../kernels/kernels.hpp"
+#include "femforge/codegen.hpp"
+#include "femforge/fem.hpp"
+#include "femforge/meshgen.hpp"
+#include "femforge/symbolic.hpp"
+#include "femforge_b200.h"
+#include "../runtime/runtime.hpp"
+
+using namespace femforge;
+using ffb::Error;
+
+namespace {
+
+thread_local std::string g_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FF_OK;
+  } catch (const Error& e) {
+    g_error = e.what();
+    return e.code;
+  } catch (const symbolic::SymbolicError& e) {
+    g_error = e.what();
+    return FF_E_SYMBOLIC;
+  } catch (const fem::MeshError& e) {
+    g_error = e.what();
+    return FF_E_MESH;
+  } catch (const fem::FormError& e) {
+    g_error = e.what();
+    return FF_E_FORM;
+  } catch (const codegen::CodegenError& e) {
+    g_error = e.what();
+    return FF_E_FORM;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return FF_E_NOMEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return FF_E_ARG;
+  }
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(FF_E_ARG, msg);
+}
+
+void check_alloc(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) throw Error(FF_E_NOMEM, std::string(what) + ": out of device memory");
+  ffb::cuda_check(e, what);
+}
+
+template <typename T>
+T* device_alloc(std::size_t n, const char* what) {
+  T* p = nullptr;
+  check_alloc(cudaMalloc(&p, std::max<std::size_t>(n, 1) * sizeof(T)), what);
+  return p;
+}
+
+void bind(const ff_ctx* ctx) {
+  if (ctx) ffb::cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+}
+
+void load_module(ff_form* f, int w) {
+  if (f->kernel[w] || !f->ctx) return;
+  bind(f->ctx);
+  ffb::cuda_check(cudaLibraryLoadData(&f->lib[w], f->module[w].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+                  "cudaLibraryLoadData");
+  ffb::cuda_check(cudaLibraryGetKernel(&f->kernel[w], f->lib[w], "ff_assemble_atomic"), "cudaLibraryGetKernel");
+}
+
+// Renders + compiles the template for slot width w (1 or 2).
+void build_variant(ff_form* f, int w) {
+  if (!f->module[w].cubin.empty()) return;
+  if (f->raw) throw Error(FF_E_ARG, "raw-source forms are compiled for one slot width only");
+  codegen::LaunchParams p = f->params;
+  p.slot_bytes = w;
+  const auto t0 = std::chrono::steady_clock::now();
+  f->source[w] = codegen::emit_source(f->inst, p, &f->plan);
+  f->module[w] = ffb::nvrtc_compile(f->source[w], "femforge_element.cu");
+  f->compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  load_module(f, w);
+}
+
+void ensure_plan(ff_pattern* p, const ff_mesh* m) {
+  if (p->plan_mesh == m && p->plan_generation == m->generation && p->slots) return;
+  require(m->k == p->k, "mesh and sparsity pattern have different DOFs per element");
+  ff_ctx* ctx = p->ctx;
+  bind(ctx);
+  const int w = p->max_row_len <= 256 ? 1 : 2;
+  require(p->max_row_len <= 65536, "rows longer than 65536 entries are not supported");
+  if (p->slots && (p->ne != m->ne || p->slot_bytes != w)) {
+    cudaFree(p->slots);
+    p->slots = nullptr;
+  }
+  if (!p->slots) p->slots = device_alloc<unsigned char>(static_cast<std::size_t>(m->ne) * m->k * m->k * w, "slot plan");
+  p->ne = m->ne;
+  p->slot_bytes = w;
+  ffb::cuda_check(cudaMemsetAsync(ctx->d_status, 0xff, 2 * sizeof(unsigned long long), ctx->stream), "memset");
+  ffb::cuda_check(ffb::kernels::build_slots(m->dconn, m->ne, m->k, p->rb, p->re, p->row_ptr, p->col_idx, w, p->slots,
+                                            ctx->d_status + 1, ctx->sm_count, ctx->stream),
+                  "slot plan kernel");
+  unsigned long long bad = 0;
+  ffb::cuda_check(cudaMemcpyAsync(&bad, ctx->d_status + 1, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream), "copy");
+  ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "slot plan");
+  p->plan_mesh = m;
+  p->plan_generation = m->generation;
+  if (bad != ~0ull) {
+    p->plan_mesh = nullptr;
+    throw Error(FF_E_PATTERN, "column not present in sparsity row " + std::to_string(bad) +
+                                  " (inconsistent sparsity pattern)");
+  }
+}
+
+void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
+                     unsigned flags = 0) {
+  require(f->ctx && f->ctx == m->ctx && m->ctx == p->ctx, "form, mesh and pattern must share one context");
+  require(f->dim == m->dim, "form and mesh dimensions differ");
+  require(f->n_local == m->k, "form and mesh have different DOFs per element");
+  ensure_plan(p, m);
+  const int w = p->slot_bytes;
+  build_variant(f, w);
+  ff_ctx* ctx = f->ctx;
+  const int64_t n_rows = p->re - p->rb;
+  if (!(flags & FF_SKIP_ZERO))
+    ffb::cuda_check(ffb::kernels::zero_fill(d_values, p->nnz, d_rhs, n_rows, ctx->d_status, ctx->sm_count, s), "K0");
+  if (m->ne == 0 || (flags & FF_ZERO_ONLY)) return;
+  const double* coords = m->coords;
+  const int32_t* vconn = m->vconn;
+  const int32_t* dconn = m->dconn;
+  const void* slots = p->slots;
+  long long ne = m->ne, rb = p->rb, re = p->re;
+  const int64_t* row_ptr = p->row_ptr;
+  unsigned long long* status = ctx->d_status;
+  void* args[] = {&coords, &vconn, &dconn, &slots, &ne, &row_ptr, &d_values, &d_rhs, &rb, &re, &status};
+  const unsigned grid = static_cast<unsigned>((m->ne + f->block - 1) / f->block);
+  ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel[w]), dim3(grid), dim3(f->block), args, 0, s),
+                  "K2 launch");
+}
+
+void report_status(ff_ctx* ctx, ff_stats* stats) {
+  ffb::cuda_check(cudaMemcpyAsync(ctx->h_status, ctx->d_status, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  ctx->stream),
+                  "status copy");
+  ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "assembly");
+  const unsigned long long be = ctx->h_status[0], br = ctx->h_status[1];
+  if (stats) {
+    stats->bad_element = be == ~0ull ? -1 : static_cast<int64_t>(be);
+    stats->bad_row = br == ~0ull ? -1 : static_cast<int64_t>(br);
+  }
+  if (be != ~0ull) throw Error(FF_E_DEGENERATE, "degenerate element " + std::to_string(be) + " (|det J| <= 1e-14)");
+  if (br != ~0ull)
+    throw Error(FF_E_PATTERN, "column not present in sparsity row " + std::to_string(br) + " (inconsistent sparsity pattern)");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ff_version(void) { return "femforge-b200 0.1 (sm_100a, NVRTC)"; }
+const char* ff_last_error(void) { return g_error.c_str(); }
+
+int ff_device_count(int* count) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    *count = n;
+  });
+}
+
+int ff_init(int device, ff_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, "ff_init: out is NULL");
+    auto c = std::make_unique<ff_ctx>();
+    c->device = device;
+    ffb::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    ffb::cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attribute");
+    ffb::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->d_status = device_alloc<unsigned long long>(2, "status");
+    ffb::cuda_check(cudaMallocHost(&c->h_status, 2 * sizeof(unsigned long long)), "cudaMallocHost");
+    ffb::cuda_check(cudaMemset(c->d_status, 0xff, 2 * sizeof(unsigned long long)), "memset");
+    *out = c.release();
+  });
+}
+
+int ff_ctx_destroy(ff_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    bind(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->d_status);
+    cudaFreeHost(ctx->h_status);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int ff_ctx_synchronize(ff_ctx* ctx) {
+  return guarded([&] {
+    require(ctx, "null context");
+    bind(ctx);
+    ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "synchronize");
+  });
+}
+
+void* ff_ctx_stream(ff_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int ff_form_create(ff_ctx* ctx, const ff_form_desc* d, ff_form** out) {
+  return guarded([&] {
+    require(d && out, "ff_form_create: null argument");
+    require(d->dim == 2 || d->dim == 3, "form dimension must be 2 or 3");
+    require(d->degree == 1 || d->degree == 2, "only Lagrange degree 1 and 2 are supported");
+    require(d->bilinear && d->linear, "bilinear and linear integrands are required");
+    auto f = std::make_unique<ff_form>();
+    f->ctx = ctx;
+    f->dim = d->dim;
+    f->degree = d->degree;
+    f->block = d->block_size > 0 ? d->block_size : 256;
+    fem::WeakForm wf;
+    wf.bilinear = symbolic::parse(d->bilinear);
+    wf.linear = symbolic::parse(d->linear);
+    wf.space.dim = d->dim;
+    wf.space.degree = d->degree;
+    const auto t0 = std::chrono::steady_clock::now();
+    f->inst = fem::instantiate(wf);
+    f->n_local = f->inst.n_local;
+    f->params.block_size = f->block;
+    f->params.quad_rule = d->quad_rule;
+    f->params.strategy = static_cast<codegen::Strategy>(d->strategy);
+    f->params.n_local = f->n_local;
+    f->compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    build_variant(f.get(), 1);
+    *out = f.release();
+  });
+}
+
+int ff_compile(ff_ctx* ctx, const char* src, int dim, int degree, int block_size, ff_form** out, char* log,
+               size_t log_cap) {
+  return guarded([&] {
+    require(src && out, "ff_compile: null argument");
+    auto f = std::make_unique<ff_form>();
+    f->ctx = ctx;
+    f->raw = true;
+    f->dim = dim;
+    f->degree = degree;
+    f->n_local = fem::local_dofs(dim, degree);
+    f->block = block_size > 0 ? block_size : 256;
+    f->source[1] = src;
+    try {
+      f->module[1] = ffb::nvrtc_compile(f->source[1], "femforge_user.cu");
+    } catch (const Error& e) {
+      if (log && log_cap) {
+        std::strncpy(log, e.what(), log_cap - 1);
+        log[log_cap - 1] = '\0';
+      }
+      throw;
+    }
+    if (log && log_cap) {
+      std::strncpy(log, f->module[1].log.c_str(), log_cap - 1);
+      log[log_cap - 1] = '\0';
+    }
+    f->compile_ms = f->module[1].ms;
+    load_module(f.get(), 1);
+    *out = f.release();
+  });
+}
+
+int ff_form_source(const ff_form* f, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    require(f, "null form");
+    const std::string& s = f->source[1];
+    if (len) *len = s.size();
+    if (buf && cap) {
+      const std::size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+
+int ff_form_cubin(const ff_form* f, void* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    require(f, "null form");
+    const std::string& s = f->module[1].cubin;
+    if (len) *len = s.size();
+    if (buf) std::memcpy(buf, s.data(), std::min(cap, s.size()));
+  });
+}
+
+int ff_form_info_get(const ff_form* f, ff_form_info* o) {
+  return guarded([&] {
+    require(f && o, "null argument");
+    o->dim = f->dim;
+    o->degree = f->degree;
+    o->n_local = f->n_local;
+    o->n_quad = f->plan.n_quad;
+    o->strategy = static_cast<int>(f->plan.strategy);
+    o->n_invariants = f->plan.n_invariants;
+    o->n_unique_entries = f->plan.n_unique_entries;
+    o->flops_per_element = f->plan.flops;
+    o->registers = f->module[1].registers;
+    o->shared_bytes = f->module[1].shared_bytes;
+    o->compile_ms = f->compile_ms;
+  });
+}
+
+int ff_form_destroy(ff_form* f) {
+  return guarded([&] {
+    if (!f) return;
+    for (auto& lib : f->lib)
+      if (lib) cudaLibraryUnload(lib);
+    delete f;
+  });
+}
+
+int ff_mesh_create(ff_ctx* ctx, int dim, const double* coords, int64_t nv, const int32_t* vconn, int64_t ne,
+                   const int32_t* dconn, int32_t k, int64_t n_dofs, ff_mesh** out) {
+  return guarded([&] {
+    require(ctx && out && coords && vconn, "ff_mesh_create: null argument");
+    require(dim == 2 || dim == 3, "mesh dimension must be 2 or 3");
+    require(nv >= 0 && ne >= 0 && n_dofs >= 0, "negative size");
+    require(n_dofs < (int64_t(1) << 31), "more than 2^31 DOFs per device are not supported");
+    require(k == dim + 1 || dconn, "dconn is required when dofs_per_elem != dim+1");
+    bind(ctx);
+    auto m = std::make_unique<ff_mesh>();
+    m->ctx = ctx;
+    m->dim = dim;
+    m->k = k;
+    m->nv = nv;
+    m->ne = ne;
+    m->n_dofs = n_dofs;
+    m->coords = device_alloc<double>(nv * dim, "coords");
+    m->vconn = device_alloc<int32_t>(ne * (dim + 1), "vconn");
+    m->dconn = dconn ? device_alloc<int32_t>(ne * k, "dconn") : m->vconn;
+    ffb::cuda_check(cudaMemcpyAsync(m->coords, coords, nv * dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ffb::cuda_check(cudaMemcpyAsync(m->vconn, vconn, ne * (dim + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (dconn)
+      ffb::cuda_check(cudaMemcpyAsync(m->dconn, dconn, ne * k * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "mesh upload");
+    *out = m.release();
+  });
+}
+
+int ff_mesh_update(ff_mesh* m, const double* coords, const int32_t* vconn, const int32_t* dconn) {
+  return guarded([&] {
+    require(m, "null mesh");
+    ff_ctx* ctx = m->ctx;
+    bind(ctx);
+    if (coords)
+      ffb::cuda_check(cudaMemcpyAsync(m->coords, coords, m->nv * m->dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (vconn)
+      ffb::cuda_check(cudaMemcpyAsync(m->vconn, vconn, m->ne * (m->dim + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (dconn && m->dconn != m->vconn)
+      ffb::cuda_check(cudaMemcpyAsync(m->dconn, dconn, m->ne * m->k * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (vconn || dconn) ++m->generation;  // slot plans are re-derived (and re-validated)
+  });
+}
+
+int ff_mesh_destroy(ff_mesh* m) {
+  return guarded([&] {
+    if (!m) return;
+    bind(m->ctx);
+    cudaFree(m->coords);
+    if (m->dconn != m->vconn) cudaFree(m->dconn);
+    cudaFree(m->vconn);
+    delete m;
+  });
+}
+
+int ff_pattern_build(ff_ctx* ctx, const ff_mesh* m, int64_t rb, int64_t re, ff_pattern** out) {
+  return guarded([&] {
+    require(ctx && m && out, "ff_pattern_build: null argument");
+    require(0 <= rb && rb <= re && re <= m->n_dofs, "row block outside [0, n_dofs]");
+    require(re - rb < (int64_t(1) << 31), "row block too large");
+    bind(ctx);
+    auto p = std::make_unique<ff_pattern>();
+    p->ctx = ctx;
+    p->rb = rb;
+    p->re = re;
+    p->k = m->k;
+    int mx = 0;
+    ffb::cuda_check(ffb::kernels::build_pattern(m->dconn, m->ne, m->k, rb, re, ctx->sm_count, ctx->stream, &p->row_ptr,
+                                                &p->col_idx, &p->nnz, &mx),
+                    "K1 pattern build");
+    p->max_row_len = mx;
+    *out = p.release();
+  });
+}
+
+int ff_pattern_info(const ff_pattern* p, int64_t* n_rows, int64_t* nnz, int32_t* max_row_len) {
+  return guarded([&] {
+    require(p, "null pattern");
+    if (n_rows) *n_rows = p->re - p->rb;
+    if (nnz) *nnz = p->nnz;
+    if (max_row_len) *max_row_len = p->max_row_len;
+  });
+}
+
+int ff_pattern_export(const ff_pattern* p, int64_t* row_ptr, int32_t* col_idx) {
+  return guarded([&] {
+    require(p, "null pattern");
+    bind(p->ctx);
+    if (row_ptr)
+      ffb::cuda_check(cudaMemcpy(row_ptr, p->row_ptr, (p->re - p->rb + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+    if (col_idx) ffb::cuda_check(cudaMemcpy(col_idx, p->col_idx, p->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int ff_pattern_export_ell(const ff_pattern* p, int32_t max_nz, int32_t* row_len, int32_t* row_cols) {
+  return guarded([&] {
+    require(p && row_len && row_cols, "null argument");
+    require(max_nz >= p->max_row_len, "max_nz smaller than the longest row");
+    const int64_t n = p->re - p->rb;
+    std::vector<int64_t> rp(n + 1);
+    std::vector<int32_t> ci(p->nnz);
+    bind(p->ctx);
+    ffb::cuda_check(cudaMemcpy(rp.data(), p->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+    ffb::cuda_check(cudaMemcpy(ci.data(), p->col_idx, p->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t i = 0; i < n; ++i) {
+      row_len[i] = static_cast<int32_t>(rp[i + 1] - rp[i]);
+      for (int32_t c = 0; c < max_nz; ++c)
+        row_cols[i * max_nz + c] = c < row_len[i] ? ci[rp[i] + c] : -1;
+    }
+  });
+}
+
+int ff_pattern_device(const ff_pattern* p, const int64_t** row_ptr, const int32_t** col_idx) {
+  return guarded([&] {
+    require(p, "null pattern");
+    if (row_ptr) *row_ptr = p->row_ptr;
+    if (col_idx) *col_idx = p->col_idx;
+  });
+}
+
+int ff_pattern_destroy(ff_pattern* p) {
+  return guarded([&] {
+    if (!p) return;
+    bind(p->ctx);
+    cudaFree(p->row_ptr);
+    cudaFree(p->col_idx);
+    cudaFree(p->slots);
+    cudaFree(p->e2e_values);
+    cudaFree(p->e2e_rhs);
+    delete p;
+  });
+}
+
+int ff_pattern_prepare(ff_pattern* p, const ff_mesh* m) {
+  return guarded([&] {
+    require(p && m, "null argument");
+    ensure_plan(p, m);
+  });
+}
+
+int ff_assemble_device(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, void* stream) {
+  return guarded([&] {
+    require(f && m && p && d_values && d_rhs, "ff_assemble_device: null argument");
+    bind(f->ctx);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : f->ctx->stream;
+    launch_assembly(f, m, p, d_values, d_rhs, s);
+  });
+}
+
+int ff_assemble_device_ex(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, void* stream,
+                          unsigned flags) {
+  return guarded([&] {
+    require(f && m && p && d_values && d_rhs, "ff_assemble_device_ex: null argument");
+    require(flags <= 2, "unknown flags");
+    bind(f->ctx);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : f->ctx->stream;
+    launch_assembly(f, m, p, d_values, d_rhs, s, flags);
+  });
+}
+
+int ff_check(ff_ctx* ctx, ff_stats* stats) {
+  return guarded([&] {
+    require(ctx, "null context");
+    bind(ctx);
+    ffb::cuda_check(cudaDeviceSynchronize(), "device");
+    report_status(ctx, stats);
+  });
+}
+
+int ff_assemble(ff_form* f, ff_mesh* m, ff_pattern* p, const double* coords, const int32_t* vconn, const int32_t* dconn,
+                double* values_out, double* rhs_out, ff_stats* stats) {
+  return guarded([&] {
+    require(f && m && p && values_out && rhs_out, "ff_assemble: null argument");
+    const auto t0 = std::chrono::steady_clock::now();
+    ff_ctx* ctx = f->ctx;
+    require(ctx, "form was compiled without a context");
+    bind(ctx);
+    // inputs: the flattened mesh (device.cpp:48-64 analogue), host -> device
+    if (coords)
+      ffb::cuda_check(cudaMemcpyAsync(m->coords, coords, m->nv * m->dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (vconn)
+      ffb::cuda_check(cudaMemcpyAsync(m->vconn, vconn, m->ne * (m->dim + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (dconn && m->dconn != m->vconn)
+      ffb::cuda_check(cudaMemcpyAsync(m->dconn, dconn, m->ne * m->k * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    if (vconn || dconn) ++m->generation;  // re-derive + re-validate the slot plan, as the
+                                          // reference re-searches every column (device.cpp:274-288)
+    const int64_t n_rows = p->re - p->rb;
+    if (!p->e2e_values) p->e2e_values = device_alloc<double>(p->nnz, "values");
+    if (!p->e2e_rhs) p->e2e_rhs = device_alloc<double>(n_rows, "rhs");
+    launch_assembly(f, m, p, p->e2e_values, p->e2e_rhs, ctx->stream);
+    report_status(ctx, stats);
+    ffb::cuda_check(cudaMemcpyAsync(values_out, p->e2e_values, p->nnz * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ffb::cuda_check(cudaMemcpyAsync(rhs_out, p->e2e_rhs, n_rows * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "D2H");
+    if (stats) stats->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// ---- host helpers ---------------------------------------------------------
+
+int ff_unit_square_mesh(int n, double* coords, int32_t* conn) {
+  return guarded([&] {
+    const fem::Mesh m = meshgen::unit_square_mesh(n);
+    const auto c = m.coords_flat();
+    const auto e = m.conn_flat();
+    std::memcpy(coords, c.data(), c.size() * sizeof(double));
+    std::memcpy(conn, e.data(), e.size() * sizeof(int32_t));
+  });
+}
+
+int ff_kuhn_mesh(int n, double* coords, int32_t* conn) {
+  return guarded([&] {
+    const fem::Mesh m = meshgen::kuhn_cube_mesh(n);
+    const auto c = m.coords_flat();
+    const auto e = m.conn_flat();
+    std::memcpy(coords, c.data(), c.size() * sizeof(double));
+    std::memcpy(conn, e.data(), e.size() * sizeof(int32_t));
+  });
+}
+
+int ff_kuhn_p2_dofs(int n, const int32_t* vconn, int64_t ne, int32_t* dconn) {
+  return guarded([&] {
+    fem::Mesh m;
+    m.dim = 3;
+    m.elements.resize(ne);
+    for (int64_t e = 0; e < ne; ++e)
+      for (int a = 0; a < 4; ++a) m.elements[e].nodes[a] = vconn[4 * e + a];
+    const fem::DofMap d = meshgen::kuhn_p2_dofs(n, m);
+    std::memcpy(dconn, d.dofs.data(), d.dofs.size() * sizeof(int32_t));
+  });
+}
+
+int ff_p2_dofs(int dim, const int32_t* vconn, int64_t ne, int64_t nv, int32_t* dconn, int64_t* n_dofs) {
+  return guarded([&] {
+    fem::Mesh m;
+    m.dim = dim;
+    m.nodes.resize(nv);
+    m.elements.resize(ne);
+    for (int64_t e = 0; e < ne; ++e)
+      for (int a = 0; a <= dim; ++a) m.elements[e].nodes[a] = vconn[(dim + 1) * e + a];
+    const fem::DofMap d = fem::lagrange_dofs(m, 2);
+    std::memcpy(dconn, d.dofs.data(), d.dofs.size() * sizeof(int32_t));
+    if (n_dofs) *n_dofs = d.n_dofs;
+  });
+}
+
+int ff_partition_rows(int64_t n_dofs, int n_parts, int part, int64_t* rb, int64_t* re) {
+  return guarded([&] {
+    require(n_parts > 0 && part >= 0 && part < n_parts, "invalid partition");
+    *rb = n_dofs * part / n_parts;
+    *re = n_dofs * (part + 1) / n_parts;
+  });
+}
+
+int ff_select_elements(const int32_t* dconn, int64_t ne, int32_t k, int64_t rb, int64_t re, int64_t* ids, int64_t* count) {
+  return guarded([&] {
+    require(dconn && count, "null argument");
+    int64_t n = 0;
+    for (int64_t e = 0; e < ne; ++e) {
+      bool touch = false;
+      for (int a = 0; a < k && !touch; ++a) touch = dconn[e * k + a] >= rb && dconn[e * k + a] < re;
+      if (touch) {
+        if (ids) ids[n] = e;
+        ++n;
+      }
+    }
+    *count = n;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,484 @@
+// The quadrature compiler: instantiated integrands (over reference
+// coordinates + per-element geometry symbols) -> straight-line CUDA that
+// computes every local matrix / load-vector entry of one element.
+//
+// The reference evaluates each entry at each quadrature point through an IR
+// interpreter and sums w_q * f_q in ascending q (device.cpp:176-192,
+// kernel.cpp:22-46). Two equivalent GPU strategies are generated here:
+//
+//  * ReferenceTensor -- when an integrand is a polynomial in the reference
+//    coordinates (affine simplices with polynomial coefficients), the sum
+//    over quadrature points is done at compile time in extended precision:
+//      K_ij = sum_q w_q f_ij(xi_q; g) = sum_t C_ij,t * m_t(g)
+//    where m_t are monomials in the geometry symbols (J, J^{-T}, det J, x_0).
+//    Monomials whose coefficient columns are identical across all entries are
+//    merged into one invariant (e.g. det*G0l*G0m + det*G1l*G1m + det*G2l*G2m
+//    for the Laplacian -> the 6 entries of det J^{-1}J^{-T}), and identical
+//    entry rows (symmetry) are computed once.
+//  * Pointwise -- the integrand at each quadrature point with the reference
+//    coordinates folded to constants, summed with the rule weights, lowered
+//    with CSE across all entries and all points (quadrature-invariant
+//    subexpressions are computed once per element).
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <optional>
+#include <set>
+#include <sstream>
+#include <unordered_map>
+
+#include "femforge/codegen.hpp"
+
+namespace femforge::codegen {
+
+using namespace symbolic;
+
+namespace {
+
+using Mono = std::vector<std::pair<int, int>>;  // (atom, exponent) sorted by atom
+using Poly = std::map<Mono, long double>;
+
+Mono mono_mul(const Mono& a, const Mono& b) {
+  Mono r;
+  r.reserve(a.size() + b.size());
+  std::size_t i = 0, j = 0;
+  while (i < a.size() || j < b.size()) {
+    if (j == b.size() || (i < a.size() && a[i].first < b[j].first)) {
+      r.push_back(a[i++]);
+    } else if (i == a.size() || b[j].first < a[i].first) {
+      r.push_back(b[j++]);
+    } else {
+      r.push_back({a[i].first, a[i].second + b[j].second});
+      ++i;
+      ++j;
+    }
+  }
+  return r;
+}
+
+Poly poly_mul(const Poly& a, const Poly& b) {
+  Poly r;
+  for (const auto& [ma, ca] : a)
+    for (const auto& [mb, cb] : b) r[mono_mul(ma, mb)] += ca * cb;
+  return r;
+}
+
+void poly_add(Poly& acc, const Poly& b, long double s = 1.0L) {
+  for (const auto& [m, c] : b) acc[m] += s * c;
+}
+
+long double number_value(const Number& n) {
+  return n.exact ? static_cast<long double>(n.rat.num) / static_cast<long double>(n.rat.den)
+                 : static_cast<long double>(n.flt);
+}
+
+// Converts expressions into polynomials over "atoms". Atoms 0..2 are the
+// reference coordinates; every other atom is a geometry symbol or an opaque
+// subexpression that does not depend on the reference coordinates.
+class PolyBuilder {
+ public:
+  PolyBuilder() {
+    for (const char* n : {"xi", "eta", "zeta"}) atom_of(sym(n));
+  }
+
+  std::optional<Poly> build(const Expr& e) {
+    auto m = memo_.find(e.raw());
+    if (m != memo_.end()) return m->second;
+    std::optional<Poly> r = convert(e);
+    memo_.emplace(e.raw(), r);
+    return r;
+  }
+
+  const std::vector<Expr>& atoms() const { return atoms_; }
+
+ private:
+  int atom_of(const Expr& e) {
+    auto it = index_.find(e.raw());
+    if (it != index_.end()) return it->second;
+    index_.emplace(e.raw(), static_cast<int>(atoms_.size()));
+    atoms_.push_back(e);
+    return static_cast<int>(atoms_.size()) - 1;
+  }
+  bool has_ref(const Expr& e) { return depends_on(e, {"xi", "eta", "zeta"}); }
+  Poly single(const Expr& atom) { return Poly{{Mono{{atom_of(atom), 1}}, 1.0L}}; }
+
+  std::optional<Poly> convert(const Expr& e) {
+    const auto& k = e.children();
+    switch (e.kind()) {
+      case Kind::Constant:
+        return Poly{{Mono{}, number_value(e.node().constant)}};
+      case Kind::Symbol:
+        return single(e);
+      case Kind::Add: {
+        Poly acc;
+        for (const Expr& c : k) {
+          auto p = build(c);
+          if (!p) return std::nullopt;
+          poly_add(acc, *p);
+        }
+        return acc;
+      }
+      case Kind::Mul: {
+        Poly acc{{Mono{}, 1.0L}};
+        for (const Expr& c : k) {
+          auto p = build(c);
+          if (!p) return std::nullopt;
+          acc = poly_mul(acc, *p);
+        }
+        return acc;
+      }
+      case Kind::Pow: {
+        if (e.exponent() > 0) {
+          auto b = build(k[0]);
+          if (!b) return std::nullopt;
+          Poly acc{{Mono{}, 1.0L}};
+          for (std::int64_t i = 0; i < e.exponent(); ++i) acc = poly_mul(acc, *b);
+          return acc;
+        }
+        if (has_ref(e)) return std::nullopt;
+        return single(e);
+      }
+      case Kind::Div: {
+        if (has_ref(k[1])) return std::nullopt;
+        auto num = build(k[0]);
+        if (!num) return std::nullopt;
+        return poly_mul(*num, single(integer(1) / k[1]));
+      }
+      default:  // sin, cos, sqrt
+        if (has_ref(e)) return std::nullopt;
+        return single(e);
+    }
+  }
+
+  std::vector<Expr> atoms_;
+  std::unordered_map<const Node*, int> index_;
+  std::unordered_map<const Node*, std::optional<Poly>> memo_;
+};
+
+// C identifier of a geometry symbol (the template declares gJrc, gGrc, gdet, gXr).
+bool is_geometry_symbol(const std::string& n) {
+  return n == "gdet" || (n.size() == 4 && (n[1] == 'J' || n[1] == 'G') && n[0] == 'g') ||
+         (n.size() == 3 && n[0] == 'g' && n[1] == 'X');
+}
+
+// Renders an opaque atom expression as CUDA (geometry symbols are in scope).
+std::string render_expr(const Expr& e);
+
+std::string render_expr(const Expr& e) {
+  const auto& k = e.children();
+  switch (e.kind()) {
+    case Kind::Constant: return "(" + double_literal(e.constant_value()) + ")";
+    case Kind::Symbol:
+      if (!is_geometry_symbol(e.name())) throw CodegenError("unbound symbol '" + e.name() + "' in element code");
+      return e.name();
+    case Kind::Add: {
+      std::string s = "(";
+      for (std::size_t i = 0; i < k.size(); ++i) s += (i ? " + " : "") + render_expr(k[i]);
+      return s + ")";
+    }
+    case Kind::Mul: {
+      std::string s = "(";
+      for (std::size_t i = 0; i < k.size(); ++i) s += (i ? " * " : "") + render_expr(k[i]);
+      return s + ")";
+    }
+    case Kind::Pow: return "ff_powi(" + render_expr(k[0]) + ", " + std::to_string(e.exponent()) + ")";
+    case Kind::Div: return "(" + render_expr(k[0]) + " / " + render_expr(k[1]) + ")";
+    case Kind::Sin: return "sin(" + render_expr(k[0]) + ")";
+    case Kind::Cos: return "cos(" + render_expr(k[0]) + ")";
+    case Kind::Sqrt: return "sqrt(" + render_expr(k[0]) + ")";
+  }
+  return "0.0";
+}
+
+struct Entry {
+  bool linear;
+  int i, j;
+};
+
+std::vector<Entry> entry_list(int n) {
+  std::vector<Entry> out;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) out.push_back({false, i, j});
+  for (int i = 0; i < n; ++i) out.push_back({true, i, 0});
+  return out;
+}
+
+std::string emit_call(const Entry& en, const std::string& v) {
+  if (en.linear) return "FF_EMIT_B(" + std::to_string(en.i) + ", " + v + ");";
+  return "FF_EMIT_A(" + std::to_string(en.i) + ", " + std::to_string(en.j) + ", " + v + ");";
+}
+
+// ---------------------------------------------------------------------------
+// ReferenceTensor
+
+std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
+  PolyBuilder pb;
+  std::vector<Expr> integrands = f.geo_bilinear;
+  integrands.insert(integrands.end(), f.geo_linear.begin(), f.geo_linear.end());
+  std::vector<Poly> polys;
+  for (const Expr& e : integrands) {
+    auto p = pb.build(e);
+    if (!p) return std::nullopt;
+    polys.push_back(std::move(*p));
+  }
+  // quadrature moments sum_q w_q xi^a eta^b zeta^c in extended precision
+  std::map<std::array<int, 3>, long double> moments;
+  auto moment = [&](const std::array<int, 3>& ex) {
+    auto it = moments.find(ex);
+    if (it != moments.end()) return it->second;
+    long double s = 0.0L;
+    for (int q = 0; q < rule.size(); ++q) {
+      long double t = rule.weights[q];
+      for (int c = 0; c < 3; ++c)
+        for (int p = 0; p < ex[c]; ++p) t *= static_cast<long double>(rule.points[q][c]);
+      s += t;
+    }
+    moments.emplace(ex, s);
+    return s;
+  };
+  // coefficient matrix over geometry monomials
+  std::map<Mono, int> columns;
+  std::vector<std::map<int, long double>> rows(polys.size());
+  for (std::size_t r = 0; r < polys.size(); ++r) {
+    for (const auto& [m, c] : polys[r]) {
+      std::array<int, 3> ex{0, 0, 0};
+      Mono geo;
+      for (const auto& [a, p] : m) {
+        if (a < 3)
+          ex[a] = p;
+        else
+          geo.push_back({a, p});
+      }
+      auto [it, fresh] = columns.emplace(geo, static_cast<int>(columns.size()));
+      rows[r][it->second] += c * moment(ex);
+    }
+  }
+  std::vector<Mono> col_mono(columns.size());
+  for (const auto& [m, k] : columns) col_mono[k] = m;
+  // round to double, drop numerical zeros (relative 1e-14 of the row's largest term)
+  std::vector<std::map<int, double>> C(rows.size());
+  for (std::size_t r = 0; r < rows.size(); ++r) {
+    long double mx = 0.0L;
+    for (const auto& [k, c] : rows[r]) mx = std::max(mx, std::fabs(c));
+    for (const auto& [k, c] : rows[r])
+      if (std::fabs(c) > 1e-14L * mx && c != 0.0L) C[r][k] = static_cast<double>(c);
+  }
+  // merge columns with identical coefficient vectors
+  std::map<std::vector<std::pair<int, double>>, std::vector<int>> groups;
+  for (std::size_t k = 0; k < col_mono.size(); ++k) {
+    std::vector<std::pair<int, double>> sig;
+    for (std::size_t r = 0; r < C.size(); ++r) {
+      auto it = C[r].find(static_cast<int>(k));
+      if (it != C[r].end()) sig.push_back({static_cast<int>(r), it->second});
+    }
+    if (!sig.empty()) groups[sig].push_back(static_cast<int>(k));
+  }
+  // deterministic invariant order: by first member column's monomial
+  std::vector<std::vector<int>> inv;
+  for (auto& [sig, cols] : groups) inv.push_back(cols);
+  std::sort(inv.begin(), inv.end(), [&](const std::vector<int>& a, const std::vector<int>& b) {
+    return col_mono[a[0]] < col_mono[b[0]];
+  });
+  std::vector<int> inv_of_col(col_mono.size(), -1);
+  for (std::size_t t = 0; t < inv.size(); ++t)
+    for (int k : inv[t]) inv_of_col[k] = static_cast<int>(t);
+
+  ElementPlan plan;
+  plan.strategy = Strategy::ReferenceTensor;
+  std::ostringstream os;
+  std::int64_t flops = 0;
+  // monomial products, memoised by prefix
+  std::map<Mono, std::string> prod_name;
+  int next_p = 0;
+  const auto& atoms = pb.atoms();
+  std::map<int, std::string> atom_name;
+  auto atom_ref = [&](int a) -> std::string {
+    auto it = atom_name.find(a);
+    if (it != atom_name.end()) return it->second;
+    const Expr& x = atoms[a];
+    std::string s;
+    if (x.is_symbol()) {
+      s = render_expr(x);
+    } else {
+      s = "ff_a" + std::to_string(a);
+      os << "  const double " << s << " = " << render_expr(x) << ";\n";
+      flops += 4;
+    }
+    atom_name.emplace(a, s);
+    return s;
+  };
+  auto product = [&](const Mono& m) -> std::string {
+    // expand exponents into a factor list, build left-to-right with memo
+    std::vector<int> factors;
+    for (const auto& [a, p] : m)
+      for (int t = 0; t < p; ++t) factors.push_back(a);
+    Mono prefix;
+    std::string cur;
+    for (std::size_t i = 0; i < factors.size(); ++i) {
+      prefix = mono_mul(prefix, Mono{{factors[i], 1}});
+      auto it = prod_name.find(prefix);
+      if (it != prod_name.end()) {
+        cur = it->second;
+        continue;
+      }
+      std::string name;
+      if (i == 0) {
+        name = atom_ref(factors[0]);
+      } else {
+        name = "ff_p" + std::to_string(next_p++);
+        os << "  const double " << name << " = " << cur << " * " << atom_ref(factors[i]) << ";\n";
+        ++flops;
+      }
+      prod_name.emplace(prefix, name);
+      cur = name;
+    }
+    return cur.empty() ? std::string("1.0") : cur;
+  };
+  os << "  // " << inv.size() << " geometric invariants\n";
+  for (std::size_t t = 0; t < inv.size(); ++t) {
+    std::string expr;
+    for (std::size_t q = 0; q < inv[t].size(); ++q) {
+      expr += (q ? " + " : "") + product(col_mono[inv[t][q]]);
+      if (q) ++flops;
+    }
+    os << "  const double ff_t" << t << " = " << expr << ";\n";
+  }
+  plan.n_invariants = static_cast<int>(inv.size());
+  // entries: sum_t c_t * inv_t; identical rows computed once
+  const std::vector<Entry> entries = entry_list(f.n_local);
+  std::map<std::vector<std::pair<int, double>>, std::vector<int>> same;
+  std::vector<std::vector<std::pair<int, double>>> row_sig(C.size());
+  for (std::size_t r = 0; r < C.size(); ++r) {
+    std::map<int, long double> by_inv;
+    for (const auto& [k, c] : C[r]) by_inv[inv_of_col[k]] = c;  // merged columns share c
+    for (const auto& [t, c] : by_inv) row_sig[r].push_back({t, static_cast<double>(c)});
+    same[row_sig[r]].push_back(static_cast<int>(r));
+  }
+  // rows already grouped; emit in entry order of the group's first member
+  std::vector<std::vector<int>> ordered;
+  for (auto& [sig, members] : same) ordered.push_back(members);
+  std::sort(ordered.begin(), ordered.end());
+  os << "  // " << ordered.size() << " distinct entries\n";
+  int vi = 0;
+  for (const auto& members : ordered) {
+    const auto& sig = row_sig[members[0]];
+    std::string v;
+    if (sig.empty()) {
+      v = "0.0";
+    } else {
+      for (std::size_t q = 0; q < sig.size(); ++q) {
+        const double c = sig[q].second;
+        const std::string t = "ff_t" + std::to_string(sig[q].first);
+        if (q == 0) {
+          v = c == 1.0 ? t : c == -1.0 ? "-" + t : double_literal(c) + " * " + t;
+        } else {
+          v += c == 1.0 ? " + " + t : c == -1.0 ? " - " + t : " + " + double_literal(c) + " * " + t;
+        }
+        flops += 2;
+      }
+    }
+    const std::string name = "ff_v" + std::to_string(vi++);
+    os << "  { const double " << name << " = " << v << ";";
+    for (int r : members) os << " " << emit_call(entries[r], name);
+    os << " }\n";
+  }
+  plan.n_unique_entries = static_cast<int>(ordered.size());
+  plan.flops = flops;
+  plan.body = os.str();
+  return plan;
+}
+
+// ---------------------------------------------------------------------------
+// Pointwise
+
+ElementPlan plan_pointwise(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
+  const Expr ref[3] = {fem::arg_xi(), fem::arg_eta(), fem::arg_zeta()};
+  std::vector<Expr> integrands = f.geo_bilinear;
+  integrands.insert(integrands.end(), f.geo_linear.begin(), f.geo_linear.end());
+  std::vector<Expr> sums;
+  for (const Expr& e : integrands) {
+    std::vector<Expr> terms;
+    for (int q = 0; q < rule.size(); ++q) {
+      std::vector<std::pair<Expr, Expr>> b;
+      for (int c = 0; c < f.dim; ++c) b.push_back({ref[c], constant(rule.points[q][c])});
+      terms.push_back(constant(rule.weights[q]) * substitute(e, b));
+    }
+    sums.push_back(add(terms));
+  }
+  SymbolTable args;
+  const fem::GeometrySymbols& g = fem::geometry_symbols();
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      args.add(g.J[r][c].name());
+      args.add(g.G[r][c].name());
+    }
+  for (int r = 0; r < 3; ++r) args.add(g.X[r].name());
+  args.add(g.det.name());
+  MultiProgram p = lower_many(sums, args);
+  ElementPlan plan;
+  plan.strategy = Strategy::Pointwise;
+  std::ostringstream os;
+  std::int64_t flops = 0;
+  for (std::size_t k = 0; k < p.code.size(); ++k) {
+    const Instr& in = p.code[k];
+    auto r = [](int i) { return "ff_r" + std::to_string(i); };
+    std::string rhs;
+    switch (in.op) {
+      case Op::LoadArg: rhs = p.arg_names[in.imm]; break;
+      case Op::LoadConst: rhs = double_literal(p.consts[in.imm]); break;
+      case Op::Add: rhs = r(in.a) + " + " + r(in.b); ++flops; break;
+      case Op::Sub: rhs = r(in.a) + " - " + r(in.b); ++flops; break;
+      case Op::Mul: rhs = r(in.a) + " * " + r(in.b); ++flops; break;
+      case Op::Div: rhs = r(in.a) + " / " + r(in.b); flops += 4; break;
+      case Op::Neg: rhs = "-" + r(in.a); break;
+      case Op::PowInt: rhs = "ff_powi(" + r(in.a) + ", " + std::to_string(in.imm) + ")"; flops += 8; break;
+      case Op::Sin: rhs = "sin(" + r(in.a) + ")"; flops += 20; break;
+      case Op::Cos: rhs = "cos(" + r(in.a) + ")"; flops += 20; break;
+      case Op::Sqrt: rhs = "sqrt(" + r(in.a) + ")"; flops += 4; break;
+    }
+    os << "  const double ff_r" << k << " = " << rhs << ";\n";
+  }
+  const std::vector<Entry> entries = entry_list(f.n_local);
+  std::set<int> distinct;
+  for (std::size_t r = 0; r < entries.size(); ++r) {
+    os << "  " << emit_call(entries[r], "ff_r" + std::to_string(p.results[r])) << "\n";
+    distinct.insert(p.results[r]);
+  }
+  plan.n_unique_entries = static_cast<int>(distinct.size());
+  plan.flops = flops;
+  plan.body = os.str();
+  return plan;
+}
+
+}  // namespace
+
+ElementPlan plan_element(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule, Strategy strategy) {
+  if (f.geo_bilinear.size() != static_cast<std::size_t>(f.n_local * f.n_local) ||
+      f.geo_linear.size() != static_cast<std::size_t>(f.n_local))
+    throw CodegenError("instantiated form has no geometry-symbol entries");
+  if (rule.dim != f.dim) throw CodegenError("quadrature rule dimension does not match the form");
+  ElementPlan plan;
+  if (strategy == Strategy::Pointwise) {
+    plan = plan_pointwise(f, rule);
+  } else {
+    auto t = plan_tensor(f, rule);
+    if (!t) {
+      if (strategy == Strategy::ReferenceTensor)
+        throw CodegenError("integrand is not polynomial in the reference coordinates; use the pointwise strategy");
+      plan = plan_pointwise(f, rule);
+    } else if (strategy == Strategy::Auto && t->flops > 4000) {
+      // large tensor expansions (e.g. high-degree coefficients): keep the cheaper
+      ElementPlan p = plan_pointwise(f, rule);
+      plan = p.flops < t->flops ? p : *t;
+    } else {
+      plan = *t;
+    }
+  }
+  plan.dim = f.dim;
+  plan.degree = f.degree;
+  plan.n_local = f.n_local;
+  plan.n_quad = rule.size();
+  return plan;
+}
+
+}  // namespace femforge::codegen

@@ -1,0 +1,56 @@
+// Source emission: the hand-written assembly template with the generated
+// element body spliced in (the reference's template route, kernel.cpp:
+// 290-449, made executable: the output is what NVRTC compiles).
+#include <string>
+
+#include "femforge/codegen.hpp"
+
+namespace femforge::codegen {
+
+namespace {
+
+const char* const kAssemblyTemplate =
+#include "../kernels/assemble_template.inc"
+    ;
+
+void fill(std::string& text, const std::string& key, const std::string& value) {
+  const std::string tag = "{{" + key + "}}";
+  const std::size_t at = text.find(tag);
+  if (at == std::string::npos) throw CodegenError("missing placeholder " + tag);
+  if (text.find(tag, at + 1) != std::string::npos) throw CodegenError("duplicate placeholder " + tag);
+  text.replace(at, tag.size(), value);
+}
+
+}  // namespace
+
+std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg) {
+  return emit_source(f, cfg, nullptr);
+}
+
+std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg, ElementPlan* plan_out) {
+  if (cfg.elems_per_block <= 0 || cfg.max_nz <= 0 || cfg.n_quad <= 0 || cfg.n_local <= 0)
+    throw CodegenError("missing placeholder value in launch parameters");
+  if (cfg.block_size < 32 || cfg.block_size > 1024 || cfg.block_size % 32 != 0)
+    throw CodegenError("block_size must be a multiple of 32 in [32, 1024]");
+  if (cfg.slot_bytes != 1 && cfg.slot_bytes != 2) throw CodegenError("slot_bytes must be 1 or 2");
+  if (cfg.scatter != Scatter::Atomic && cfg.scatter != Scatter::Auto)
+    throw CodegenError("this template renders the atomic scatter only");
+  const int rule_id = cfg.quad_rule > 0 ? cfg.quad_rule : default_quad_rule(f.dim, f.degree);
+  const fem::QuadratureRule rule = fem::quadrature_rule(f.dim, rule_id);
+  ElementPlan plan = plan_element(f, rule, cfg.strategy);
+  std::string text = kAssemblyTemplate;
+  fill(text, "SLOT_T", cfg.slot_bytes == 1 ? "unsigned char" : "unsigned short");
+  fill(text, "DIM", std::to_string(f.dim));
+  fill(text, "DEGREE", std::to_string(f.degree));
+  fill(text, "NLOC", std::to_string(f.n_local));
+  fill(text, "BLOCK", std::to_string(cfg.block_size));
+  std::string body = "  // element body: " + std::string(plan.strategy == Strategy::ReferenceTensor ? "reference-tensor" : "pointwise") +
+                     " strategy, " + std::to_string(plan.n_quad) + "-point rule " + std::to_string(rule_id) + ", ~" +
+                     std::to_string(plan.flops) + " flops\n" + plan.body;
+  fill(text, "ELEMENT_BODY", body);
+  if (text.find("{{") != std::string::npos) throw CodegenError("unresolved placeholder");
+  if (plan_out) *plan_out = std::move(plan);
+  return text;
+}
+
+}  // namespace femforge::codegen

@@ -1,0 +1,135 @@
+// femforge-b200 code generation: symbolic integrands -> SSA register IR ->
+// CUDA C++ for NVRTC (sm_100a).
+//
+// API parity with /root/reference/proj/include/femforge/codegen/kernel.hpp:13-78
+// (Op, Instr, CodegenError, KernelProgram{run,disassemble}, lower,
+// CompiledForm, compile_form, LaunchParams, emit_source). Differences, by
+// design: emit_source renders the REAL kernel that NVRTC compiles (the
+// reference's template is inspection-only), and the element body
+// comes from a quadrature compiler (plan_element) instead of one __device__
+// function per entry and quadrature point.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "femforge/fem.hpp"
+#include "femforge/symbolic.hpp"
+
+namespace femforge::codegen {
+
+using symbolic::Expr;
+using symbolic::SymbolTable;
+
+enum class Op : std::uint8_t { LoadArg, LoadConst, Add, Sub, Mul, Div, Neg, PowInt, Sin, Cos, Sqrt };
+
+struct Instr {
+  Op op;
+  int a = -1;
+  int b = -1;
+  std::int64_t imm = 0;
+};
+
+class CodegenError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+// Flat SSA program: instruction k writes register k (kernel.hpp:43-54).
+struct KernelProgram {
+  std::vector<Instr> code;
+  std::vector<double> consts;
+  int arity = 0;
+  int result = 0;
+
+  double run(std::span<const double> args) const;
+  double run(std::span<const double> args, std::vector<double>& scratch) const;
+  std::string disassemble() const;
+};
+
+KernelProgram lower(const Expr& e, const SymbolTable& args);
+
+// Several outputs lowered into one SSA program with common-subexpression
+// elimination across all of them (the reference lowers entries separately,
+// kernel.cpp:277-283, so det J is recomputed per entry).
+struct MultiProgram {
+  std::vector<Instr> code;
+  std::vector<double> consts;
+  std::vector<std::string> arg_names;
+  std::vector<int> results;
+  void run(std::span<const double> args, std::span<double> out) const;
+};
+MultiProgram lower_many(const std::vector<Expr>& outputs, const SymbolTable& args);
+
+struct CompiledForm {
+  std::vector<KernelProgram> bilinear;  // n_local^2
+  std::vector<KernelProgram> linear;    // n_local
+  int n_quad = 3;
+  int n_local = 3;
+  int dim = 2;
+};
+
+CompiledForm compile_form(const fem::InstantiatedForm& f);
+
+// ---------------------------------------------------------------------------
+// GPU element code
+
+enum class Strategy : int {
+  Auto = 0,
+  // Quadrature summed at compile time: every entry becomes a constant-weight
+  // combination of per-element geometric invariants (reference-tensor form).
+  // Requires integrands polynomial in the reference coordinates.
+  ReferenceTensor = 1,
+  // Integrand evaluated at each quadrature point in registers, weighted sum
+  // in ascending q (device.cpp:176-192 order); always applicable.
+  Pointwise = 2,
+};
+
+struct ElementPlan {
+  int dim = 2;
+  int degree = 1;
+  int n_local = 3;
+  int n_quad = 3;
+  Strategy strategy = Strategy::ReferenceTensor;
+  std::string body;        // CUDA statements; emits FF_EMIT_A(i,j,v) / FF_EMIT_B(i,v)
+  int n_invariants = 0;    // ReferenceTensor: merged geometric invariants
+  int n_unique_entries = 0;
+  std::int64_t flops = 0;  // fp64 operations per element after CSE (estimate)
+};
+
+ElementPlan plan_element(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule,
+                         Strategy strategy = Strategy::Auto);
+
+// Scatter variants of the assembly template.
+enum class Scatter : int {
+  Auto = 0,
+  Atomic = 1,     // element-parallel, fp64 RED into CSR slots (K0 zero-fill first)
+  RowTiles = 2,   // row-tile ownership: atomic-free, each CSR slot written once
+};
+
+struct LaunchParams {
+  int n_quad = 3;           // informational (taken from the rule)
+  int n_local = 3;          // informational (taken from the form)
+  int elems_per_block = 4;  // reference knob; maps to the CUDA block size (x32 threads)
+  int max_nz = 7;           // informational (ELL width of the reference layout)
+  int quad_rule = 0;        // 0: default rule for (dim, degree)
+  Strategy strategy = Strategy::Auto;
+  Scatter scatter = Scatter::Atomic;
+  int block_size = 256;     // threads per CTA of the element kernel
+  int slot_bytes = 1;       // 1 or 2: width of the element slot plan entries
+};
+
+int default_quad_rule(int dim, int degree);
+
+// Renders the complete NVRTC translation unit (template + element body).
+// Byte-deterministic for identical inputs; throws CodegenError on bad params.
+std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg);
+std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg, ElementPlan* plan_out);
+
+// Shortest round-trip double literal valid in C/CUDA source.
+std::string double_literal(double v);
+
+}  // namespace femforge::codegen

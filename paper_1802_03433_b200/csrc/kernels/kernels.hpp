@@ -1,0 +1,24 @@
+// Host launchers of the offline-compiled (nvcc, sm_100a) kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ffb::kernels {
+
+// K1: CSR pattern of rows [rb, re) from device DOF connectivity [ne][k].
+// Allocates *row_ptr (n_rows+1, int64) and *col_idx (nnz, int32) with cudaMalloc.
+cudaError_t build_pattern(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t re, int sm_count,
+                          cudaStream_t s, int64_t** row_ptr, int32_t** col_idx, int64_t* nnz, int* max_row_len);
+
+// Element slot plan [ne][k][k] (u8 or u16): position of dof[b] in row dof[a].
+cudaError_t build_slots(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t re, const int64_t* row_ptr,
+                        const int32_t* col_idx, int slot_bytes, void* d_slots, unsigned long long* d_bad_row,
+                        int sm_count, cudaStream_t s);
+
+// K0: values[0:na] = 0, rhs[0:nb] = 0, status[0:2] = ~0 (one launch).
+cudaError_t zero_fill(double* a, int64_t na, double* b, int64_t nb, unsigned long long* status, int sm_count,
+                      cudaStream_t s);
+
+}  // namespace ffb::kernels

@@ -1,0 +1,110 @@
+// NVRTC compilation of emitted assembly kernels for sm_100a (the runtime
+// compilation step of the paper, §5; the reference only renders the
+// template text, kernel.cpp:409-449, and never compiles it -- SPEC.md:15).
+#include <nvrtc.h>
+
+#include <chrono>
+#include <cstdlib>
+#include <fstream>
+#include <functional>
+#include <mutex>
+#include <regex>
+#include <sstream>
+#include <unordered_map>
+
+#include "femforge_b200.h"
+#include "runtime.hpp"
+
+namespace ffb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(FF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+const char* const kOptions[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--diag-suppress=177",
+                                "--ptxas-options=-v"};
+
+std::mutex g_cache_mu;
+std::unordered_map<std::string, CompiledModule> g_cache;
+
+std::string cache_key(const std::string& src) {
+  std::string k = src;
+  for (const char* o : kOptions) k += '\n', k += o;
+  return k;
+}
+
+std::string disk_path(const std::string& key) {
+  const char* dir = std::getenv("FF_CUBIN_CACHE");
+  if (!dir || !*dir) return {};
+  std::ostringstream os;
+  os << dir << "/ff_" << std::hex << std::hash<std::string>()(key) << "_" << key.size() << ".cubin";
+  return os.str();
+}
+
+void parse_resources(CompiledModule& m) {
+  std::smatch r;
+  if (std::regex_search(m.log, r, std::regex("Used ([0-9]+) registers"))) m.registers = std::stoi(r[1]);
+  if (std::regex_search(m.log, r, std::regex("([0-9]+) bytes smem"))) m.shared_bytes = std::stoi(r[1]);
+}
+
+}  // namespace
+
+CompiledModule nvrtc_compile(const std::string& source, const std::string& name) {
+  const std::string key = cache_key(source);
+  {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) return it->second;
+  }
+  CompiledModule m;
+  const std::string path = disk_path(key);
+  if (!path.empty()) {
+    std::ifstream in(path, std::ios::binary);
+    if (in) {
+      std::stringstream ss;
+      ss << in.rdbuf();
+      std::string blob = ss.str();
+      const std::size_t cut = blob.find('\0');
+      if (cut != std::string::npos && cut + 1 < blob.size()) {
+        m.log = blob.substr(0, cut);
+        m.cubin = blob.substr(cut + 1);
+        parse_resources(m);
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        g_cache.emplace(key, m);
+        return m;
+      }
+    }
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  nvrtcProgram prog = nullptr;
+  if (nvrtcCreateProgram(&prog, source.c_str(), name.c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    throw Error(FF_E_NVRTC, "nvrtcCreateProgram failed");
+  const nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(sizeof kOptions / sizeof kOptions[0]), kOptions);
+  std::size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  m.log.assign(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, m.log.data());
+  while (!m.log.empty() && m.log.back() == '\0') m.log.pop_back();
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    throw Error(FF_E_NVRTC, std::string("NVRTC compilation failed (") + nvrtcGetErrorString(rc) + "):\n" + m.log);
+  }
+  std::size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  m.cubin.assign(n, '\0');
+  nvrtcGetCUBIN(prog, m.cubin.data());
+  nvrtcDestroyProgram(&prog);
+  m.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  parse_resources(m);
+  if (!path.empty()) {
+    std::ofstream out(path, std::ios::binary);
+    out << m.log << '\0' << m.cubin;
+  }
+  std::lock_guard<std::mutex> g(g_cache_mu);
+  g_cache.emplace(key, m);
+  return m;
+}
+
+}  // namespace ffb

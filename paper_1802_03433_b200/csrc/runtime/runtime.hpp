@@ -1,0 +1,89 @@
+// femforge-b200 runtime internals: NVRTC compilation with a CUBIN cache,
+// error types, and the C-ABI handle structures.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "femforge/codegen.hpp"
+#include "femforge/fem.hpp"
+
+namespace ffb {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct CompiledModule {
+  std::string cubin;
+  std::string log;
+  int registers = 0;
+  int shared_bytes = 0;
+  double ms = 0.0;
+};
+
+// NVRTC -> sm_100a CUBIN. Cached in memory by (source, options); optionally
+// on disk under $FF_CUBIN_CACHE. Throws Error(FF_E_NVRTC) with the log.
+CompiledModule nvrtc_compile(const std::string& source, const std::string& name);
+
+}  // namespace ffb
+
+struct ff_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  unsigned long long* d_status = nullptr;  // [bad_elem, bad_row]
+  unsigned long long* h_status = nullptr;  // pinned mirror
+};
+
+struct ff_form {
+  ff_ctx* ctx = nullptr;
+  int dim = 2, degree = 1, n_local = 3, block = 256;
+  femforge::codegen::ElementPlan plan;
+  bool raw = false;                 // ff_compile route (caller source)
+  femforge::fem::InstantiatedForm inst;
+  femforge::codegen::LaunchParams params;
+  int quad_rule = 0;
+  double compile_ms = 0.0;
+  // one module per slot width (1: u8 plans, 2: u16 plans)
+  std::string source[3];
+  ffb::CompiledModule module[3];
+  cudaLibrary_t lib[3] = {nullptr, nullptr, nullptr};
+  cudaKernel_t kernel[3] = {nullptr, nullptr, nullptr};
+};
+
+struct ff_mesh {
+  ff_ctx* ctx = nullptr;
+  int dim = 2;
+  int k = 3;  // DOFs per element
+  int64_t nv = 0, ne = 0, n_dofs = 0;
+  double* coords = nullptr;
+  int32_t* vconn = nullptr;
+  int32_t* dconn = nullptr;  // == vconn for P1
+  std::uint64_t generation = 0;
+};
+
+struct ff_pattern {
+  ff_ctx* ctx = nullptr;
+  int64_t rb = 0, re = 0, nnz = 0;
+  int max_row_len = 0;
+  int k = 0;
+  int64_t ne = 0;
+  int64_t* row_ptr = nullptr;
+  int32_t* col_idx = nullptr;
+  // element slot plan for one mesh
+  const ff_mesh* plan_mesh = nullptr;
+  std::uint64_t plan_generation = ~0ull;
+  void* slots = nullptr;
+  int slot_bytes = 1;
+  // device scratch of the host-buffer (end-to-end) entry point
+  double* e2e_values = nullptr;
+  double* e2e_rhs = nullptr;
+};

@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+golden outputs, the oracle, and size-independent properties at the
+BASELINE.json sizes. Tolerances: sparsity bit-exact; values/rhs <= 1e-12
+normwise (acceptance.cpp:58-67; BASELINE.json north star)."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+from conftest import GOLDEN, normwise
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _golden(pattern):
+    return sorted(glob.glob(os.path.join(GOLDEN, pattern)))
+
+
+def gpu_system(ff, ctx, dim, deg, form, coords, vconn, dconn, n_dofs, quad=0, strategy="auto",
+               row_begin=0, row_end=None, block=256):
+    bil, lin = ff.named_form(form, dim) if isinstance(form, str) else form
+    f = ff.Form(ctx, dim, deg, bil, lin, quad_rule=quad, strategy=strategy, block_size=block)
+    m = ff.Mesh(ctx, dim, coords, vconn, None if deg == 1 else dconn, n_dofs)
+    p = ff.Pattern(ctx, m, row_begin, row_end)
+    rp, ci = p.export()
+    v, b = ff.assemble(f, m, p)
+    return rp, ci, v, b, f, m, p
+
+
+@pytest.mark.parametrize("path", _golden("ref2d_*.npz"), ids=os.path.basename)
+def test_gpu_matches_reference_2d(ff, ctx, path):
+    g = np.load(path)
+    _, form, n = os.path.basename(path)[:-4].split("_")
+    xy, conn = ff.unit_square_mesh(int(n[1:]))
+    rp, ci, v, b, *_ = gpu_system(ff, ctx, 2, 1, form, xy, conn, conn, xy.shape[0])
+    assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(ci, g["col_idx"])
+    assert normwise(v, g["values"]) <= TOL
+    assert normwise(b, g["rhs"]) <= TOL
+
+
+@pytest.mark.parametrize("path", _golden("ref3d_*.npz"), ids=os.path.basename)
+@pytest.mark.parametrize("strategy", ["tensor", "pointwise"])
+def test_gpu_matches_reference_cas_3d(ff, ctx, path, strategy):
+    g = np.load(path)
+    _, p, form, n, q = os.path.basename(path)[:-4].split("_")
+    deg, n, q = int(p[1:]), int(n[1:]), int(q[1:])
+    xyz, vc = ff.kuhn_mesh(n)
+    dc, nd = (vc, xyz.shape[0]) if deg == 1 else ff.kuhn_p2_dofs(n, vc)
+    rp, ci, v, b, *_ = gpu_system(ff, ctx, 3, deg, form, xyz, vc, dc, nd, quad=q, strategy=strategy)
+    assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(ci, g["col_idx"])
+    assert normwise(v, g["values"]) <= TOL
+    assert normwise(b, g["rhs"]) <= TOL
+
+
+CASES = [  # (dim, degree, form, n, quad)
+    (2, 1, "demo2d", 96, 3),
+    (2, 1, "poisson", 64, 3),
+    (2, 2, "helmholtz", 24, 1),
+    (3, 1, "poisson", 14, 4),
+    (3, 1, "varcoef", 8, 14),
+    (3, 2, "poisson", 10, 4),
+    (3, 2, "helmholtz", 8, 11),
+    (3, 2, "varcoef", 6, 14),
+]
+
+
+def _mesh(ff, dim, deg, n):
+    if dim == 2:
+        c, v = ff.unit_square_mesh(n)
+        d, nd = (v, c.shape[0]) if deg == 1 else ff.p2_dofs(2, v, c.shape[0])
+    else:
+        c, v = ff.kuhn_mesh(n)
+        d, nd = (v, c.shape[0]) if deg == 1 else ff.kuhn_p2_dofs(n, v)
+    return c, v, d, nd
+
+
+@pytest.mark.parametrize("dim,deg,form,n,quad", CASES)
+def test_gpu_matches_oracle(ff, ctx, dim, deg, form, n, quad):
+    c, v, d, nd = _mesh(ff, dim, deg, n)
+    rp, ci, val, rhs, *_ = gpu_system(ff, ctx, dim, deg, form, c, v, d, nd, quad=quad)
+    orp, oci = po.build_pattern(d, nd)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    ov, ob = po.assemble(form, dim, deg, quad, c, v, d, orp, oci, workers=8)
+    assert normwise(val, ov) <= TOL
+    assert normwise(rhs, ob) <= TOL
+
+
+def test_ell_view_matches_reference_layout(ff, ctx):
+    g = np.load(os.path.join(GOLDEN, "ref2d_demo2d_n8.npz"))
+    xy, conn = ff.unit_square_mesh(8)
+    *_, p = gpu_system(ff, ctx, 2, 1, "demo2d", xy, conn, conn, xy.shape[0])
+    assert p.max_row_len == 7  # MAX_NZ 7 (test_device.cpp:85-90)
+    rl, rc = p.export_ell()
+    assert np.array_equal(rl, np.diff(g["row_ptr"]))
+    for i in range(p.n_rows):
+        assert np.array_equal(rc[i, :rl[i]], g["col_idx"][g["row_ptr"][i]:g["row_ptr"][i + 1]])
+        assert np.all(rc[i, rl[i]:] == -1)
+
+
+def test_device_path_equals_e2e_path(ff, ctx):
+    import torch
+    c, v, d, nd = _mesh(ff, 3, 2, 6)
+    rp, ci, val, rhs, f, m, p = gpu_system(ff, ctx, 3, 2, "poisson", c, v, d, nd)
+    dv = torch.empty(p.nnz, dtype=torch.float64, device="cuda")
+    db = torch.empty(p.n_rows, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        ff.assemble_device(f, m, p, dv.data_ptr(), db.data_ptr(), s)
+    torch.cuda.synchronize()
+    ctx.check()
+    # same kernel, atomics reorder fp64 adds only
+    assert normwise(dv.cpu().numpy(), val) <= 1e-14
+    assert normwise(db.cpu().numpy(), rhs) <= 1e-14
+
+
+def test_degenerate_element_reported_by_lowest_index(ff, ctx):
+    xy, conn = ff.unit_square_mesh(4)
+    b, l = ff.named_form("stiffness", 2)
+    f = ff.Form(ctx, 2, 1, b, l)
+    m = ff.Mesh(ctx, 2, xy, conn)
+    p = ff.Pattern(ctx, m)
+    bad = xy.copy()
+    bad[conn[9]] = 0.25  # collapses element 9 and every element sharing an edge with it
+    touching = [e for e in range(conn.shape[0]) if len(set(conn[e]) & set(conn[9])) >= 2]
+    with pytest.raises(ff.DeviceError, match=f"degenerate element {min(touching)} "):
+        ff.assemble(f, m, p, coords=bad)
+    ff.assemble(f, m, p, coords=xy)  # recovers
+
+
+def test_pattern_from_other_mesh_is_a_hard_error(ff, ctx):
+    # test_device.cpp:262-279: same node count, disjoint connectivity
+    xy, conn = ff.unit_square_mesh(2)
+    b, l = ff.named_form("demo2d", 2)
+    f = ff.Form(ctx, 2, 1, b, l)
+    m = ff.Mesh(ctx, 2, xy, conn)
+    p = ff.Pattern(ctx, m)
+    other = conn.copy()
+    other[0] = [0, 1, 5]
+    with pytest.raises(ff.DeviceError, match="not present in sparsity row"):
+        ff.assemble(f, m, p, vconn=other)
+
+
+@pytest.mark.parametrize("parts", [2, 3, 4])
+def test_row_blocks_concatenate_to_full_system(ff, ctx, parts):
+    c, v, d, nd = _mesh(ff, 3, 2, 6)
+    rp, ci, val, rhs, *_ = gpu_system(ff, ctx, 3, 2, "poisson", c, v, d, nd)
+    rp_parts, cis, vals, rhss, off = [], [], [], [], 0
+    for part in range(parts):
+        rb, re = ff.partition_rows(nd, parts, part)
+        ids = ff.select_elements(d, rb, re)  # owned + halo elements, duplicated across blocks
+        sub = gpu_system(ff, ctx, 3, 2, "poisson", c, v[ids], d[ids], nd, row_begin=rb, row_end=re)
+        rp_parts.append(sub[0][:-1] + off)
+        off += sub[0][-1]
+        cis.append(sub[1]); vals.append(sub[2]); rhss.append(sub[3])
+    rp_cat = np.concatenate(rp_parts + [np.array([off])])
+    assert np.array_equal(rp_cat, rp)
+    assert np.array_equal(np.concatenate(cis), ci)
+    assert normwise(np.concatenate(vals), val) <= TOL
+    assert normwise(np.concatenate(rhss), rhs) <= TOL
+
+
+def test_north_star_size_properties(ff, ctx):
+    """Kuhn 128^3 P2 Poisson (12.58M tets): nnz cubic, zero row sums of the
+    stiffness, symmetry, and sum(rhs) = integral of f (partition of unity;
+    the 4-point rule is exact for the quadratic f) -- checked on the GPU."""
+    import torch
+    n = 128
+    c, v, d, nd = _mesh(ff, 3, 2, n)
+    b, l = ff.named_form("poisson", 3)
+    f = ff.Form(ctx, 3, 2, b, l)
+    m = ff.Mesh(ctx, 3, c, v, d, nd)
+    p = ff.Pattern(ctx, m)
+    assert p.nnz == 230 * n ** 3 + 138 * n ** 2 + 24 * n + 1
+    vals = torch.empty(p.nnz, dtype=torch.float64, device="cuda")
+    rhs = torch.empty(p.n_rows, dtype=torch.float64, device="cuda")
+    ff.assemble_device(f, m, p, vals.data_ptr(), rhs.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ctx.check()
+    rp_ptr, ci_ptr = p.device_pointers()
+    rp, ci = p.export()
+    rp_t = torch.from_numpy(rp).cuda()
+    ci_t = torch.from_numpy(ci).cuda().long()
+    rows = torch.repeat_interleave(torch.arange(p.n_rows, device="cuda"), rp_t[1:] - rp_t[:-1])
+    amax = vals.abs().max()
+    rowsum = torch.zeros(p.n_rows, dtype=torch.float64, device="cuda").index_add_(0, rows, vals)
+    rowmax = torch.zeros(p.n_rows, dtype=torch.float64, device="cuda").index_reduce_(0, rows, vals.abs(), "amax")
+    assert float((rowsum.abs() / rowmax).max()) <= 1e-12
+    # symmetry: value of (i,j) equals value of (j,i); keys sorted => compare via sort
+    key = rows * nd + ci_t
+    tkey = ci_t * nd + rows
+    order = torch.argsort(tkey)
+    assert torch.equal(tkey[order], key)  # pattern symmetric
+    assert float((vals[order] - vals).abs().max() / amax) <= 1e-12
+    assert abs(float(rhs.sum()) - 34.0) <= 1e-9
