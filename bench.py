@@ -254,7 +254,7 @@ def main():
     plan_ms = 1e3 * (time.perf_counter() - t)
     values = torch.empty(pat.nnz, dtype=torch.float64, device="cuda")
     rhs = torch.empty(pat.n_rows, dtype=torch.float64, device="cuda")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()       # every launch and every event on this one stream
     sp = stream.cuda_stream
     l2_bytes = 126 * 2 ** 20
     need_flush = values.numel() * 8 < 2 * l2_bytes
@@ -274,7 +274,8 @@ def main():
     with ClockSampler(local) as clocks:
         for i in range(args.steps):
             if flush is not None:
-                flush.fill_(i)
+                with torch.cuda.stream(stream):
+                    flush.fill_(i)
             ev[i][0].record(stream)
             ff.assemble_device_ex(form, mesh, pat, values.data_ptr(), rhs.data_ptr(), sp, ff.FF_ZERO_ONLY)
             ev[i][1].record(stream)

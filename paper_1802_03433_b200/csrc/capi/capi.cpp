@@ -80,6 +80,11 @@ void load_module(ff_form* f, int w) {
   ffb::cuda_check(cudaLibraryLoadData(&f->lib[w], f->module[w].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
                   "cudaLibraryLoadData");
   ffb::cuda_check(cudaLibraryGetKernel(&f->kernel[w], f->lib[w], "ff_assemble_atomic"), "cudaLibraryGetKernel");
+  cudaFuncAttributes attr{};
+  if (cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(f->kernel[w])) == cudaSuccess) {
+    f->module[w].registers = attr.numRegs;
+    f->module[w].shared_bytes = static_cast<int>(attr.sharedSizeBytes);
+  }
 }
 
 // Renders + compiles the template for slot width w (1 or 2).

@@ -302,10 +302,15 @@ class Pattern:
         self.close()
 
 
+def _stream(s):
+    """None -> the context stream; 0 (torch's default stream) -> cudaStreamLegacy."""
+    return None if s is None else C.c_void_p(1 if s == 0 else s)
+
+
 def assemble_device(form, mesh, pattern, values_ptr, rhs_ptr, stream=None):
     """K0 + K2 on device buffers, asynchronous on `stream` (a cudaStream_t int)."""
     _ok(lib().ff_assemble_device(form.h, mesh.h, pattern.h, C.c_void_p(values_ptr), C.c_void_p(rhs_ptr),
-                                 C.c_void_p(stream) if stream else None))
+                                 _stream(stream)))
 
 
 FF_SKIP_ZERO, FF_ZERO_ONLY = 1, 2
@@ -313,7 +318,7 @@ FF_SKIP_ZERO, FF_ZERO_ONLY = 1, 2
 
 def assemble_device_ex(form, mesh, pattern, values_ptr, rhs_ptr, stream=None, flags=0):
     _ok(lib().ff_assemble_device_ex(form.h, mesh.h, pattern.h, C.c_void_p(values_ptr), C.c_void_p(rhs_ptr),
-                                    C.c_void_p(stream) if stream else None, flags))
+                                    _stream(stream), flags))
 
 
 def assemble(form, mesh, pattern, coords=None, vconn=None, dconn=None, values=None, rhs=None):

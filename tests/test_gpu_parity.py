@@ -123,9 +123,11 @@ def test_degenerate_element_reported_by_lowest_index(ff, ctx):
     m = ff.Mesh(ctx, 2, xy, conn)
     p = ff.Pattern(ctx, m)
     bad = xy.copy()
-    bad[conn[9]] = 0.25  # collapses element 9 and every element sharing an edge with it
-    touching = [e for e in range(conn.shape[0]) if len(set(conn[e]) & set(conn[9])) >= 2]
-    with pytest.raises(ff.DeviceError, match=f"degenerate element {min(touching)} "):
+    bad[conn[9]] = [0.3, 0.35]  # collapse element 9 (and every element sharing an edge with it)
+    x = bad[conn]
+    det = (x[:, 1, 0] - x[:, 0, 0]) * (x[:, 2, 1] - x[:, 0, 1]) - (x[:, 2, 0] - x[:, 0, 0]) * (x[:, 1, 1] - x[:, 0, 1])
+    lowest = int(np.nonzero(np.abs(det) <= 1e-14)[0].min())
+    with pytest.raises(ff.DeviceError, match=f"degenerate element {lowest} "):
         ff.assemble(f, m, p, coords=bad)
     ff.assemble(f, m, p, coords=xy)  # recovers
 
