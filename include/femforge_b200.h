@@ -92,6 +92,10 @@ int ff_init(int device, ff_ctx** out);
 int ff_ctx_destroy(ff_ctx* ctx);
 int ff_ctx_synchronize(ff_ctx* ctx);
 void* ff_ctx_stream(ff_ctx* ctx); /* cudaStream_t of the context */
+/* Default scatter of the context: FF_SCATTER_ROWTILE (atomic-free, default)
+ * or FF_SCATTER_ATOMIC_MODE (fp64 RED); per-call flags override it. */
+enum { FF_SCATTER_ROWTILE = 0, FF_SCATTER_ATOMIC_MODE = 1 };
+int ff_ctx_set_scatter(ff_ctx* ctx, int mode);
 
 /* ---- forms: weak form text -> symbolic -> CUDA source -> NVRTC (sm_100a) - */
 /* ctx may be NULL: compile-only (no device needed; ff_assemble* then fail). */
@@ -135,9 +139,12 @@ int ff_pattern_prepare(ff_pattern* p, const ff_mesh* mesh);
  * detected on the device are reported by ff_check(). */
 int ff_assemble_device(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double* d_values, double* d_rhs,
                        void* stream);
-/* Same with flags: FF_SKIP_ZERO (values/rhs already zero: K2 only) or
- * FF_ZERO_ONLY (K0 only); lets callers time the two kernels separately. */
-enum { FF_SKIP_ZERO = 1, FF_ZERO_ONLY = 2 };
+/* Same with flags. Scatter: the default is the atomic-free row-tile kernel
+ * (each CSR slot written once, bitwise reproducible, no zero-fill);
+ * FF_SCATTER_ATOMIC selects the element-parallel fp64-RED kernel, which needs
+ * K0: FF_SKIP_ZERO (values/rhs already zero: K2 only) or FF_ZERO_ONLY (K0
+ * only) let callers time K0 and K2 separately. */
+enum { FF_SKIP_ZERO = 1, FF_ZERO_ONLY = 2, FF_SCATTER_ATOMIC = 4 };
 int ff_assemble_device_ex(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double* d_values, double* d_rhs,
                           void* stream, unsigned flags);
 /* Synchronises the context stream and reports device-side errors of the

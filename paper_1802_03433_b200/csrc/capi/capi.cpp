@@ -80,6 +80,16 @@ void load_module(ff_form* f, int w) {
   ffb::cuda_check(cudaLibraryLoadData(&f->lib[w], f->module[w].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
                   "cudaLibraryLoadData");
   ffb::cuda_check(cudaLibraryGetKernel(&f->kernel[w], f->lib[w], "ff_assemble_atomic"), "cudaLibraryGetKernel");
+  if (cudaLibraryGetKernel(&f->kernel_tile[w], f->lib[w], "ff_assemble_rowtile") == cudaSuccess) {
+    f->tile = codegen::rowtile_params(f->n_local, f->block);
+    f->tile_smem[w] = f->tile.smem_bytes(f->n_local, w);
+    ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_tile[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    f->tile_smem[w], f->ctx->device),
+                    "row-tile shared memory attribute");
+  } else {
+    cudaGetLastError();
+    f->kernel_tile[w] = nullptr;
+  }
   cudaFuncAttributes attr{};
   if (cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(f->kernel[w])) == cudaSuccess) {
     f->module[w].registers = attr.numRegs;
@@ -130,6 +140,50 @@ void ensure_plan(ff_pattern* p, const ff_mesh* m) {
   }
 }
 
+void free_tile_plan(ff_pattern* p) {
+  cudaFree(p->tile_row);
+  cudaFree(p->tile_vptr);
+  cudaFree(p->visit_elem);
+  cudaFree(p->visit_stage);
+  p->tile_row = p->tile_vptr = nullptr;
+  p->visit_elem = nullptr;
+  p->visit_stage = nullptr;
+  p->tile_generation = ~0ull;
+}
+
+// Row tiles: greedy contiguous row ranges with <= tp.rows rows and <= tp.acc
+// CSR slots, then the element visits of every tile (K1-style sort + unique).
+void ensure_tile_plan(ff_pattern* p, const ff_mesh* m, const codegen::RowTileParams& tp) {
+  if (p->tile_generation == m->generation && p->plan_mesh == m && p->tile_acc == tp.acc && p->tile_rows == tp.rows &&
+      p->tile_stage == tp.stage && p->tile_chunk == tp.chunk && p->tile_row)
+    return;
+  free_tile_plan(p);
+  ff_ctx* ctx = p->ctx;
+  bind(ctx);
+  const int64_t n = p->re - p->rb;
+  std::vector<int64_t> rp(n + 1);
+  ffb::cuda_check(cudaMemcpy(rp.data(), p->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "row_ptr D2H");
+  std::vector<int64_t> tiles{0};
+  for (int64_t r = 0; r < n;) {
+    const int64_t start = r;
+    if (rp[r + 1] - rp[r] > tp.acc) throw Error(FF_E_ARG, "row " + std::to_string(p->rb + r) + " is longer than a row tile");
+    while (r < n && r - start < tp.rows && rp[r + 1] - rp[start] <= tp.acc) ++r;
+    tiles.push_back(r);
+  }
+  p->n_tiles = static_cast<int64_t>(tiles.size()) - 1;
+  p->tile_row = device_alloc<int64_t>(tiles.size(), "tile rows");
+  ffb::cuda_check(cudaMemcpy(p->tile_row, tiles.data(), tiles.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "H2D");
+  ffb::cuda_check(ffb::kernels::build_rowtile_plan(m->dconn, m->ne, m->k, p->rb, n, p->tile_row, p->n_tiles, tp.stage,
+                                                   tp.chunk, ctx->sm_count, ctx->stream, &p->tile_vptr, &p->visit_elem,
+                                                   &p->visit_stage, &p->n_visits),
+                  "row-tile plan");
+  p->tile_generation = m->generation;
+  p->tile_acc = tp.acc;
+  p->tile_rows = tp.rows;
+  p->tile_stage = tp.stage;
+  p->tile_chunk = tp.chunk;
+}
+
 void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
                      unsigned flags = 0) {
   require(f->ctx && f->ctx == m->ctx && m->ctx == p->ctx, "form, mesh and pattern must share one context");
@@ -140,6 +194,30 @@ void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_valu
   build_variant(f, w);
   ff_ctx* ctx = f->ctx;
   const int64_t n_rows = p->re - p->rb;
+  const bool tiles = !(flags & FF_SCATTER_ATOMIC) && ctx->scatter == FF_SCATTER_ROWTILE && f->kernel_tile[w] &&
+                     !(flags & (FF_ZERO_ONLY | FF_SKIP_ZERO));
+  if (tiles) {
+    ensure_tile_plan(p, m, f->tile);
+    ffb::cuda_check(cudaMemsetAsync(ctx->d_status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
+    if (p->n_tiles == 0) return;
+    const double* coords = m->coords;
+    const int32_t* vconn = m->vconn;
+    const int32_t* dconn = m->dconn;
+    const void* slots = p->slots;
+    const int64_t* row_ptr = p->row_ptr;
+    long long rb = p->rb, nt = p->n_tiles;
+    const int64_t* tile_row = p->tile_row;
+    const int64_t* tile_vptr = p->tile_vptr;
+    const int32_t* visit_elem = p->visit_elem;
+    const uint16_t* visit_stage = p->visit_stage;
+    unsigned long long* status = ctx->d_status;
+    void* args[] = {&coords, &vconn, &dconn, &slots, &row_ptr, &d_values, &d_rhs, &rb,
+                    &tile_row, &tile_vptr, &visit_elem, &visit_stage, &nt, &status};
+    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_tile[w]), dim3(static_cast<unsigned>(nt)),
+                                     dim3(f->block), args, f->tile_smem[w], s),
+                    "K2 (row tiles) launch");
+    return;
+  }
   if (!(flags & FF_SKIP_ZERO))
     ffb::cuda_check(ffb::kernels::zero_fill(d_values, p->nnz, d_rhs, n_rows, ctx->d_status, ctx->sm_count, s), "K0");
   if (m->ne == 0 || (flags & FF_ZERO_ONLY)) return;
@@ -222,6 +300,14 @@ int ff_ctx_synchronize(ff_ctx* ctx) {
 }
 
 void* ff_ctx_stream(ff_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int ff_ctx_set_scatter(ff_ctx* ctx, int mode) {
+  return guarded([&] {
+    require(ctx, "null context");
+    require(mode == FF_SCATTER_ROWTILE || mode == FF_SCATTER_ATOMIC_MODE, "unknown scatter mode");
+    ctx->scatter = mode;
+  });
+}
 
 int ff_form_create(ff_ctx* ctx, const ff_form_desc* d, ff_form** out) {
   return guarded([&] {
@@ -457,6 +543,7 @@ int ff_pattern_destroy(ff_pattern* p) {
     cudaFree(p->row_ptr);
     cudaFree(p->col_idx);
     cudaFree(p->slots);
+    free_tile_plan(p);
     cudaFree(p->e2e_values);
     cudaFree(p->e2e_rhs);
     delete p;
@@ -483,7 +570,7 @@ int ff_assemble_device_ex(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d
                           unsigned flags) {
   return guarded([&] {
     require(f && m && p && d_values && d_rhs, "ff_assemble_device_ex: null argument");
-    require(flags <= 2, "unknown flags");
+    require(flags < 8, "unknown flags");
     bind(f->ctx);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : f->ctx->stream;
     launch_assembly(f, m, p, d_values, d_rhs, s, flags);

@@ -23,6 +23,26 @@ void fill(std::string& text, const std::string& key, const std::string& value) {
 
 }  // namespace
 
+int RowTileParams::smem_bytes(int n_local, int slot_bytes) const {
+  return 8 * acc + 8 * stage * n_local + 8 * stage + 8 * rows + 4 * 2 * (rows + 1) + 4 * 2 * stage +
+         slot_bytes * stage * n_local;
+}
+
+RowTileParams rowtile_params(int n_local, int block_size) {
+  RowTileParams p;
+  p.chunk = block_size;
+  if (n_local >= 10) {        // 3D P2: ~28 nnz/row
+    p.acc = 6144, p.rows = 256, p.stage = 384;
+  } else if (n_local >= 6) {  // 2D P2
+    p.acc = 6144, p.rows = 512, p.stage = 512;
+  } else if (n_local >= 4) {  // 3D P1: ~15 nnz/row
+    p.acc = 6144, p.rows = 512, p.stage = 768;
+  } else {                    // 2D P1: ~7 nnz/row
+    p.acc = 4096, p.rows = 512, p.stage = 768;
+  }
+  return p;
+}
+
 std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg) {
   return emit_source(f, cfg, nullptr);
 }
@@ -33,8 +53,6 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   if (cfg.block_size < 32 || cfg.block_size > 1024 || cfg.block_size % 32 != 0)
     throw CodegenError("block_size must be a multiple of 32 in [32, 1024]");
   if (cfg.slot_bytes != 1 && cfg.slot_bytes != 2) throw CodegenError("slot_bytes must be 1 or 2");
-  if (cfg.scatter != Scatter::Atomic && cfg.scatter != Scatter::Auto)
-    throw CodegenError("this template renders the atomic scatter only");
   const int rule_id = cfg.quad_rule > 0 ? cfg.quad_rule : default_quad_rule(f.dim, f.degree);
   const fem::QuadratureRule rule = fem::quadrature_rule(f.dim, rule_id);
   ElementPlan plan = plan_element(f, rule, cfg.strategy);
@@ -44,6 +62,10 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   fill(text, "DEGREE", std::to_string(f.degree));
   fill(text, "NLOC", std::to_string(f.n_local));
   fill(text, "BLOCK", std::to_string(cfg.block_size));
+  const RowTileParams tp = rowtile_params(f.n_local, cfg.block_size);
+  fill(text, "TILE_ACC", std::to_string(tp.acc));
+  fill(text, "TILE_ROWS", std::to_string(tp.rows));
+  fill(text, "TILE_STAGE", std::to_string(tp.stage));
   std::string body = "  // element body: " + std::string(plan.strategy == Strategy::ReferenceTensor ? "reference-tensor" : "pointwise") +
                      " strategy, " + std::to_string(plan.n_quad) + "-point rule " + std::to_string(rule_id) + ", ~" +
                      std::to_string(plan.flops) + " flops\n" + plan.body;

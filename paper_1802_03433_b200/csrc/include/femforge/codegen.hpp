@@ -124,6 +124,17 @@ struct LaunchParams {
 
 int default_quad_rule(int dim, int degree);
 
+// Shared-memory geometry of the row-tile kernel for n_local DOFs per element
+// (the template and the host plan builder must agree on these numbers).
+struct RowTileParams {
+  int acc = 6144;    // max CSR slots per tile (fp64 accumulators)
+  int rows = 256;    // max rows per tile
+  int stage = 384;   // max staged element rows per chunk
+  int chunk = 256;   // max element visits per chunk (= block size)
+  int smem_bytes(int n_local, int slot_bytes) const;
+};
+RowTileParams rowtile_params(int n_local, int block_size);
+
 // Renders the complete NVRTC translation unit (template + element body).
 // Byte-deterministic for identical inputs; throws CodegenError on bad params.
 std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg);

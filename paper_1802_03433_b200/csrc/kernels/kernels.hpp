@@ -17,6 +17,15 @@ cudaError_t build_slots(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, i
                         const int32_t* col_idx, int slot_bytes, void* d_slots, unsigned long long* d_bad_row,
                         int sm_count, cudaStream_t s);
 
+// Row-tile plan: tiles are row ranges [tile_row[t], tile_row[t+1]) (local rows,
+// device array of n_tiles+1). Produces the element visits of every tile
+// (elements with >= 1 DOF in the tile, ascending), and per visit its staging
+// offset inside its chunk with bit 15 set on chunk starts.
+cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
+                               const int64_t* d_tile_row, int64_t n_tiles, int stage_cap, int chunk_cap, int sm_count,
+                               cudaStream_t s, int64_t** tile_vptr, int32_t** visit_elem, uint16_t** visit_stage,
+                               int64_t* n_visits);
+
 // K0: values[0:na] = 0, rhs[0:nb] = 0, status[0:2] = ~0 (one launch).
 cudaError_t zero_fill(double* a, int64_t na, double* b, int64_t nb, unsigned long long* status, int sm_count,
                       cudaStream_t s);

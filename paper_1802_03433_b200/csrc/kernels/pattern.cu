@@ -125,6 +125,77 @@ __global__ void zero_kernel(double* __restrict__ a, int64_t na, double* __restri
   for (int64_t i = tid; i < nb; i += stride) b[i] = 0.0;
 }
 
+
+// ---- row-tile plan ---------------------------------------------------------
+
+__global__ void row_tile_map(const int64_t* __restrict__ tile_row, int64_t n_tiles, int64_t n_rows,
+                             int32_t* __restrict__ row_tile) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = n_tiles;  // last t with tile_row[t] <= r
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (tile_row[mid] <= r)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    row_tile[r] = static_cast<int32_t>(lo);
+  }
+}
+
+__global__ void visit_keys(const int32_t* __restrict__ dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
+                           const int32_t* __restrict__ row_tile, int64_t n_tiles, uint64_t* __restrict__ keys) {
+  const uint64_t invalid = static_cast<uint64_t>(n_tiles) << 32;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ne * k;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t e = t / k;
+    const int64_t row = static_cast<int64_t>(dconn[t]) - rb;
+    keys[t] = (row >= 0 && row < n_rows) ? (static_cast<uint64_t>(row_tile[row]) << 32) | static_cast<uint32_t>(e)
+                                         : invalid;
+  }
+}
+
+__global__ void split_visits(const uint64_t* __restrict__ keys, const int64_t* __restrict__ n_unique, int64_t n_tiles,
+                             int64_t* __restrict__ tile_vptr, int32_t* __restrict__ visit_elem) {
+  const int64_t n = *n_unique;
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t tile = static_cast<int64_t>(keys[v] >> 32);
+    if (tile >= n_tiles) continue;
+    visit_elem[v] = static_cast<int32_t>(keys[v] & 0xffffffffu);
+    const int64_t prev = v == 0 ? -1 : static_cast<int64_t>(keys[v - 1] >> 32);
+    for (int64_t t = prev + 1; t <= tile; ++t) tile_vptr[t] = v;
+    if (v == n - 1 || static_cast<int64_t>(keys[v + 1] >> 32) >= n_tiles)
+      for (int64_t t = tile + 1; t <= n_tiles; ++t) tile_vptr[t] = v + 1;
+  }
+}
+
+// one thread per tile: staging offsets and chunk starts (bit 15)
+__global__ void chunk_visits(const int32_t* __restrict__ dconn, int k, int64_t rb, const int64_t* __restrict__ tile_row,
+                             const int64_t* __restrict__ tile_vptr, const int32_t* __restrict__ visit_elem,
+                             int64_t n_tiles, int stage_cap, int chunk_cap, uint16_t* __restrict__ visit_stage) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_tiles;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t lo = rb + tile_row[t], hi = rb + tile_row[t + 1];
+    int stage = 0, count = 0;
+    for (int64_t v = tile_vptr[t]; v < tile_vptr[t + 1]; ++v) {
+      const int32_t* d = dconn + static_cast<int64_t>(visit_elem[v]) * k;
+      int own = 0;
+      for (int a = 0; a < k; ++a) own += d[a] >= lo && d[a] < hi;
+      bool start = count == 0;
+      if (count == chunk_cap || stage + own > stage_cap) {
+        stage = 0;
+        count = 0;
+        start = true;
+      }
+      visit_stage[v] = static_cast<uint16_t>(stage | (start ? 0x8000 : 0));
+      stage += own;
+      ++count;
+    }
+  }
+}
+
 int grid_for(int64_t n, int sm_blocks) {
   const int64_t g = (n + kThreads - 1) / kThreads;
   return static_cast<int>(g < sm_blocks ? (g < 1 ? 1 : g) : sm_blocks);
@@ -193,6 +264,58 @@ cudaError_t build_pattern(const int32_t* d_dconn, int64_t ne, int k, int64_t rb,
   *nnz = n_cols;
   *max_row_len = mx;
   return fail(cudaGetLastError());
+}
+
+
+cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
+                               const int64_t* d_tile_row, int64_t n_tiles, int stage_cap, int chunk_cap, int sm_count,
+                               cudaStream_t s, int64_t** tile_vptr, int32_t** visit_elem, uint16_t** visit_stage,
+                               int64_t* n_visits) {
+  const int cap = sm_count * 16;
+  const int64_t n_keys = ne * k;
+  int32_t* row_tile = nullptr;
+  uint64_t *keys = nullptr, *sorted = nullptr;
+  int64_t* d_count = nullptr;
+  void* temp = nullptr;
+  cudaError_t err = cudaSuccess;
+  auto done = [&](cudaError_t e) {
+    cudaFree(row_tile);
+    cudaFree(keys);
+    cudaFree(sorted);
+    cudaFree(d_count);
+    cudaFree(temp);
+    return e;
+  };
+  if ((err = cudaMalloc(&row_tile, (n_rows > 0 ? n_rows : 1) * sizeof(int32_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&keys, (n_keys > 0 ? n_keys : 1) * sizeof(uint64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&sorted, (n_keys > 0 ? n_keys : 1) * sizeof(uint64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&d_count, sizeof(int64_t))) != cudaSuccess) return done(err);
+  row_tile_map<<<grid_for(n_rows, cap), kThreads, 0, s>>>(d_tile_row, n_tiles, n_rows, row_tile);
+  visit_keys<<<grid_for(n_keys, cap), kThreads, 0, s>>>(d_dconn, ne, k, rb, n_rows, row_tile, n_tiles, keys);
+  int end_bit = 32;
+  while ((static_cast<int64_t>(1) << (end_bit - 32)) <= n_tiles) ++end_bit;
+  size_t t_sort = 0, t_uniq = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, t_sort, keys, sorted, n_keys, 0, end_bit, s);
+  cub::DeviceSelect::Unique(nullptr, t_uniq, sorted, keys, d_count, n_keys, s);
+  if ((err = cudaMalloc(&temp, t_sort > t_uniq ? t_sort : t_uniq)) != cudaSuccess) return done(err);
+  if ((err = cub::DeviceRadixSort::SortKeys(temp, t_sort, keys, sorted, n_keys, 0, end_bit, s)) != cudaSuccess)
+    return done(err);
+  if ((err = cub::DeviceSelect::Unique(temp, t_uniq, sorted, keys, d_count, n_keys, s)) != cudaSuccess) return done(err);
+  int64_t n_unique = 0;
+  cudaMemcpyAsync(&n_unique, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(tile_vptr, (n_tiles + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(visit_elem, (n_unique > 0 ? n_unique : 1) * sizeof(int32_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(visit_stage, (n_unique > 0 ? n_unique : 1) * sizeof(uint16_t))) != cudaSuccess) return done(err);
+  cudaMemsetAsync(*tile_vptr, 0, (n_tiles + 1) * sizeof(int64_t), s);
+  split_visits<<<grid_for(n_unique, cap), kThreads, 0, s>>>(keys, d_count, n_tiles, *tile_vptr, *visit_elem);
+  chunk_visits<<<grid_for(n_tiles, cap), 64, 0, s>>>(d_dconn, k, rb, d_tile_row, *tile_vptr, *visit_elem, n_tiles,
+                                                     stage_cap, chunk_cap, *visit_stage);
+  int64_t last_key = 0;
+  if (n_unique > 0) cudaMemcpyAsync(&last_key, keys + (n_unique - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+  *n_visits = n_unique - ((static_cast<uint64_t>(last_key) >> 32) >= static_cast<uint64_t>(n_tiles) ? 1 : 0);
+  return done(cudaGetLastError());
 }
 
 cudaError_t build_slots(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t re, const int64_t* row_ptr,

@@ -41,6 +41,7 @@ struct ff_ctx {
   cudaStream_t stream = nullptr;
   unsigned long long* d_status = nullptr;  // [bad_elem, bad_row]
   unsigned long long* h_status = nullptr;  // pinned mirror
+  int scatter = 0;                          // FF_SCATTER_ROWTILE / FF_SCATTER_ATOMIC_MODE
 };
 
 struct ff_form {
@@ -56,7 +57,10 @@ struct ff_form {
   std::string source[3];
   ffb::CompiledModule module[3];
   cudaLibrary_t lib[3] = {nullptr, nullptr, nullptr};
-  cudaKernel_t kernel[3] = {nullptr, nullptr, nullptr};
+  cudaKernel_t kernel[3] = {nullptr, nullptr, nullptr};          // ff_assemble_atomic
+  cudaKernel_t kernel_tile[3] = {nullptr, nullptr, nullptr};     // ff_assemble_rowtile
+  femforge::codegen::RowTileParams tile;
+  int tile_smem[3] = {0, 0, 0};
 };
 
 struct ff_mesh {
@@ -83,6 +87,14 @@ struct ff_pattern {
   std::uint64_t plan_generation = ~0ull;
   void* slots = nullptr;
   int slot_bytes = 1;
+  // row-tile plan (atomic-free scatter) for plan_mesh
+  std::uint64_t tile_generation = ~0ull;
+  int64_t n_tiles = 0, n_visits = 0;
+  int64_t* tile_row = nullptr;     // [n_tiles + 1] local rows
+  int64_t* tile_vptr = nullptr;    // [n_tiles + 1]
+  int32_t* visit_elem = nullptr;   // [n_visits]
+  uint16_t* visit_stage = nullptr; // [n_visits]
+  int tile_acc = 0, tile_rows = 0, tile_stage = 0, tile_chunk = 0;
   // device scratch of the host-buffer (end-to-end) entry point
   double* e2e_values = nullptr;
   double* e2e_rhs = nullptr;

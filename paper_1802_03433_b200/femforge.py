@@ -88,6 +88,7 @@ SIGNATURES = [
     ("ff_ctx_destroy", C.c_int, [_P]),
     ("ff_ctx_synchronize", C.c_int, [_P]),
     ("ff_ctx_stream", _P, [_P]),
+    ("ff_ctx_set_scatter", C.c_int, [_P, C.c_int]),
     ("ff_form_create", C.c_int, [_P, C.POINTER(_FormDesc), C.POINTER(_P)]),
     ("ff_compile", C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P), C.c_char_p, C.c_size_t]),
     ("ff_form_source", C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
@@ -163,6 +164,11 @@ class Context:
 
     def synchronize(self):
         _ok(lib().ff_ctx_synchronize(self.h))
+
+    def set_scatter(self, mode):
+        """'rowtile' (atomic-free, default) or 'atomic' (fp64 RED after a zero-fill)."""
+        _ok(lib().ff_ctx_set_scatter(self.h, {"rowtile": 0, "atomic": 1}[mode]))
+        self.scatter = mode
 
     def check(self):
         st = Stats()
@@ -313,7 +319,7 @@ def assemble_device(form, mesh, pattern, values_ptr, rhs_ptr, stream=None):
                                  _stream(stream)))
 
 
-FF_SKIP_ZERO, FF_ZERO_ONLY = 1, 2
+FF_SKIP_ZERO, FF_ZERO_ONLY, FF_SCATTER_ATOMIC = 1, 2, 4
 
 
 def assemble_device_ex(form, mesh, pattern, values_ptr, rhs_ptr, stream=None, flags=0):

@@ -19,8 +19,12 @@ def _golden(pattern):
     return sorted(glob.glob(os.path.join(GOLDEN, pattern)))
 
 
+SCATTERS = ["rowtile", "atomic"]
+
+
 def gpu_system(ff, ctx, dim, deg, form, coords, vconn, dconn, n_dofs, quad=0, strategy="auto",
-               row_begin=0, row_end=None, block=256):
+               row_begin=0, row_end=None, block=256, scatter="rowtile"):
+    ctx.set_scatter(scatter)
     bil, lin = ff.named_form(form, dim) if isinstance(form, str) else form
     f = ff.Form(ctx, dim, deg, bil, lin, quad_rule=quad, strategy=strategy, block_size=block)
     m = ff.Mesh(ctx, dim, coords, vconn, None if deg == 1 else dconn, n_dofs)
@@ -31,11 +35,12 @@ def gpu_system(ff, ctx, dim, deg, form, coords, vconn, dconn, n_dofs, quad=0, st
 
 
 @pytest.mark.parametrize("path", _golden("ref2d_*.npz"), ids=os.path.basename)
-def test_gpu_matches_reference_2d(ff, ctx, path):
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_gpu_matches_reference_2d(ff, ctx, path, scatter):
     g = np.load(path)
     _, form, n = os.path.basename(path)[:-4].split("_")
     xy, conn = ff.unit_square_mesh(int(n[1:]))
-    rp, ci, v, b, *_ = gpu_system(ff, ctx, 2, 1, form, xy, conn, conn, xy.shape[0])
+    rp, ci, v, b, *_ = gpu_system(ff, ctx, 2, 1, form, xy, conn, conn, xy.shape[0], scatter=scatter)
     assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(ci, g["col_idx"])
     assert normwise(v, g["values"]) <= TOL
     assert normwise(b, g["rhs"]) <= TOL
@@ -43,13 +48,14 @@ def test_gpu_matches_reference_2d(ff, ctx, path):
 
 @pytest.mark.parametrize("path", _golden("ref3d_*.npz"), ids=os.path.basename)
 @pytest.mark.parametrize("strategy", ["tensor", "pointwise"])
-def test_gpu_matches_reference_cas_3d(ff, ctx, path, strategy):
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_gpu_matches_reference_cas_3d(ff, ctx, path, strategy, scatter):
     g = np.load(path)
     _, p, form, n, q = os.path.basename(path)[:-4].split("_")
     deg, n, q = int(p[1:]), int(n[1:]), int(q[1:])
     xyz, vc = ff.kuhn_mesh(n)
     dc, nd = (vc, xyz.shape[0]) if deg == 1 else ff.kuhn_p2_dofs(n, vc)
-    rp, ci, v, b, *_ = gpu_system(ff, ctx, 3, deg, form, xyz, vc, dc, nd, quad=q, strategy=strategy)
+    rp, ci, v, b, *_ = gpu_system(ff, ctx, 3, deg, form, xyz, vc, dc, nd, quad=q, strategy=strategy, scatter=scatter)
     assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(ci, g["col_idx"])
     assert normwise(v, g["values"]) <= TOL
     assert normwise(b, g["rhs"]) <= TOL
@@ -78,9 +84,10 @@ def _mesh(ff, dim, deg, n):
 
 
 @pytest.mark.parametrize("dim,deg,form,n,quad", CASES)
-def test_gpu_matches_oracle(ff, ctx, dim, deg, form, n, quad):
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_gpu_matches_oracle(ff, ctx, dim, deg, form, n, quad, scatter):
     c, v, d, nd = _mesh(ff, dim, deg, n)
-    rp, ci, val, rhs, *_ = gpu_system(ff, ctx, dim, deg, form, c, v, d, nd, quad=quad)
+    rp, ci, val, rhs, *_ = gpu_system(ff, ctx, dim, deg, form, c, v, d, nd, quad=quad, scatter=scatter)
     orp, oci = po.build_pattern(d, nd)
     assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
     ov, ob = po.assemble(form, dim, deg, quad, c, v, d, orp, oci, workers=8)
@@ -100,10 +107,11 @@ def test_ell_view_matches_reference_layout(ff, ctx):
         assert np.all(rc[i, rl[i]:] == -1)
 
 
-def test_device_path_equals_e2e_path(ff, ctx):
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_device_path_equals_e2e_path(ff, ctx, scatter):
     import torch
     c, v, d, nd = _mesh(ff, 3, 2, 6)
-    rp, ci, val, rhs, f, m, p = gpu_system(ff, ctx, 3, 2, "poisson", c, v, d, nd)
+    rp, ci, val, rhs, f, m, p = gpu_system(ff, ctx, 3, 2, "poisson", c, v, d, nd, scatter=scatter)
     dv = torch.empty(p.nnz, dtype=torch.float64, device="cuda")
     db = torch.empty(p.n_rows, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
@@ -116,7 +124,9 @@ def test_device_path_equals_e2e_path(ff, ctx):
     assert normwise(db.cpu().numpy(), rhs) <= 1e-14
 
 
-def test_degenerate_element_reported_by_lowest_index(ff, ctx):
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_degenerate_element_reported_by_lowest_index(ff, ctx, scatter):
+    ctx.set_scatter(scatter)
     xy, conn = ff.unit_square_mesh(4)
     b, l = ff.named_form("stiffness", 2)
     f = ff.Form(ctx, 2, 1, b, l)
@@ -132,7 +142,9 @@ def test_degenerate_element_reported_by_lowest_index(ff, ctx):
     ff.assemble(f, m, p, coords=xy)  # recovers
 
 
-def test_pattern_from_other_mesh_is_a_hard_error(ff, ctx):
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_pattern_from_other_mesh_is_a_hard_error(ff, ctx, scatter):
+    ctx.set_scatter(scatter)
     # test_device.cpp:262-279: same node count, disjoint connectivity
     xy, conn = ff.unit_square_mesh(2)
     b, l = ff.named_form("demo2d", 2)
@@ -146,14 +158,15 @@ def test_pattern_from_other_mesh_is_a_hard_error(ff, ctx):
 
 
 @pytest.mark.parametrize("parts", [2, 3, 4])
-def test_row_blocks_concatenate_to_full_system(ff, ctx, parts):
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_row_blocks_concatenate_to_full_system(ff, ctx, parts, scatter):
     c, v, d, nd = _mesh(ff, 3, 2, 6)
-    rp, ci, val, rhs, *_ = gpu_system(ff, ctx, 3, 2, "poisson", c, v, d, nd)
+    rp, ci, val, rhs, *_ = gpu_system(ff, ctx, 3, 2, "poisson", c, v, d, nd, scatter=scatter)
     rp_parts, cis, vals, rhss, off = [], [], [], [], 0
     for part in range(parts):
         rb, re = ff.partition_rows(nd, parts, part)
         ids = ff.select_elements(d, rb, re)  # owned + halo elements, duplicated across blocks
-        sub = gpu_system(ff, ctx, 3, 2, "poisson", c, v[ids], d[ids], nd, row_begin=rb, row_end=re)
+        sub = gpu_system(ff, ctx, 3, 2, "poisson", c, v[ids], d[ids], nd, row_begin=rb, row_end=re, scatter=scatter)
         rp_parts.append(sub[0][:-1] + off)
         off += sub[0][-1]
         cis.append(sub[1]); vals.append(sub[2]); rhss.append(sub[3])
@@ -164,6 +177,22 @@ def test_row_blocks_concatenate_to_full_system(ff, ctx, parts):
     assert normwise(np.concatenate(rhss), rhs) <= TOL
 
 
+@pytest.mark.parametrize("dim,deg,n", [(3, 1, 20), (3, 2, 12), (2, 1, 128)])
+def test_rowtile_is_bitwise_reproducible_and_matches_atomic(ff, ctx, dim, deg, n):
+    """Atomic-free row tiles: fixed summation order -> identical bits on every
+    run (the reference's deterministic-mode property, criterion 7/8)."""
+    c, v, d, nd = _mesh(ff, dim, deg, n)
+    form = "varcoef" if dim == 3 else "demo2d"
+    quad = 14 if dim == 3 else 3
+    rp, ci, v1, b1, f, m, p = gpu_system(ff, ctx, dim, deg, form, c, v, d, nd, quad=quad, scatter="rowtile")
+    v2, b2 = ff.assemble(f, m, p)
+    assert v1.tobytes() == v2.tobytes() and b1.tobytes() == b2.tobytes()
+    ctx.set_scatter("atomic")
+    va, ba = ff.assemble(f, m, p)
+    ctx.set_scatter("rowtile")
+    assert normwise(va, v1) <= 1e-14 and normwise(ba, b1) <= 1e-14
+
+
 def test_north_star_size_properties(ff, ctx):
     """Kuhn 128^3 P2 Poisson (12.58M tets): nnz cubic, zero row sums of the
     stiffness, symmetry, and sum(rhs) = integral of f (partition of unity;
@@ -172,6 +201,7 @@ def test_north_star_size_properties(ff, ctx):
     n = 128
     c, v, d, nd = _mesh(ff, 3, 2, n)
     b, l = ff.named_form("poisson", 3)
+    ctx.set_scatter("rowtile")
     f = ff.Form(ctx, 3, 2, b, l)
     m = ff.Mesh(ctx, 3, c, v, d, nd)
     p = ff.Pattern(ctx, m)
