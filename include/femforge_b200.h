@@ -76,6 +76,8 @@ typedef struct ff_form_info {
   int registers;         /* per thread, from the loaded cubin (0 if not loaded) */
   int shared_bytes;      /* static shared memory per CTA */
   double compile_ms;     /* symbolic + emit + NVRTC */
+  int n_kinv;            /* bilinear invariants stored per element by the row gather (0: no gather) */
+  int64_t row_flops;     /* fp64 operations of the n_local gather rows of one element */
 } ff_form_info;
 
 typedef struct ff_stats {
@@ -92,9 +94,14 @@ int ff_init(int device, ff_ctx** out);
 int ff_ctx_destroy(ff_ctx* ctx);
 int ff_ctx_synchronize(ff_ctx* ctx);
 void* ff_ctx_stream(ff_ctx* ctx); /* cudaStream_t of the context */
-/* Default scatter of the context: FF_SCATTER_ROWTILE (atomic-free, default)
- * or FF_SCATTER_ATOMIC_MODE (fp64 RED); per-call flags override it. */
-enum { FF_SCATTER_ROWTILE = 0, FF_SCATTER_ATOMIC_MODE = 1 };
+/* Default scatter of the context; per-call flags override it.
+ *   FF_SCATTER_GATHER_MODE (default): row gather -- element invariants, then one
+ *     CSR row per lane accumulated in shared memory and written once
+ *     (atomic-free, deterministic; needs a reference-tensor form, <= 12 DOFs
+ *     per element and rows of <= 221 entries, else the atomic kernel runs);
+ *   FF_SCATTER_ROWTILE: CTA row tiles with staged element rows (atomic-free);
+ *   FF_SCATTER_ATOMIC_MODE: element-parallel fp64 RED after a zero-fill. */
+enum { FF_SCATTER_ROWTILE = 0, FF_SCATTER_ATOMIC_MODE = 1, FF_SCATTER_GATHER_MODE = 2 };
 int ff_ctx_set_scatter(ff_ctx* ctx, int mode);
 
 /* ---- forms: weak form text -> symbolic -> CUDA source -> NVRTC (sm_100a) - */
@@ -132,6 +139,16 @@ int ff_pattern_destroy(ff_pattern* p);
  * position of column dof[b] inside row dof[a]. Built on first assembly;
  * exposed for tests. Returns FF_E_PATTERN on a missing column. */
 int ff_pattern_prepare(ff_pattern* p, const ff_mesh* mesh);
+/* Gather plan statistics (built by the first gather assembly or here):
+ * warp items, lock-step steps (records / 32) and incidences (row, element). */
+typedef struct ff_gather_info {
+  int64_t n_items, n_steps, n_incidences;
+  int record_bytes;
+  double build_ms;
+} ff_gather_info;
+int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* mesh, ff_gather_info* out);
+/* Which scatter the next assembly of (form, pattern) runs: FF_SCATTER_*_MODE. */
+int ff_scatter_selected(const ff_form* form, const ff_pattern* p, unsigned flags, int* mode);
 
 /* ---- numeric assembly (K0 zero-fill + K2 element kernel with scatter) ---- */
 /* Device-resident, asynchronous on `stream` (NULL: the context stream).
@@ -139,12 +156,20 @@ int ff_pattern_prepare(ff_pattern* p, const ff_mesh* mesh);
  * detected on the device are reported by ff_check(). */
 int ff_assemble_device(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double* d_values, double* d_rhs,
                        void* stream);
-/* Same with flags. Scatter: the default is the atomic-free row-tile kernel
- * (each CSR slot written once, bitwise reproducible, no zero-fill);
- * FF_SCATTER_ATOMIC selects the element-parallel fp64-RED kernel, which needs
- * K0: FF_SKIP_ZERO (values/rhs already zero: K2 only) or FF_ZERO_ONLY (K0
- * only) let callers time K0 and K2 separately. */
-enum { FF_SKIP_ZERO = 1, FF_ZERO_ONLY = 2, FF_SCATTER_ATOMIC = 4 };
+/* Same with flags. Scatter flags override the context mode:
+ * FF_SCATTER_ATOMIC (element-parallel fp64 RED, needs K0: FF_SKIP_ZERO = K2
+ * only on already-zero buffers, FF_ZERO_ONLY = K0 only), FF_SCATTER_TILES
+ * (row tiles), FF_SCATTER_GATHER (row gather; FF_GATHER_INVARIANTS_ONLY /
+ * FF_GATHER_ROWS_ONLY launch only its first / second kernel, for timing). */
+enum {
+  FF_SKIP_ZERO = 1,
+  FF_ZERO_ONLY = 2,
+  FF_SCATTER_ATOMIC = 4,
+  FF_SCATTER_TILES = 8,
+  FF_SCATTER_GATHER = 16,
+  FF_GATHER_INVARIANTS_ONLY = 32,
+  FF_GATHER_ROWS_ONLY = 64
+};
 int ff_assemble_device_ex(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double* d_values, double* d_rhs,
                           void* stream, unsigned flags);
 /* Synchronises the context stream and reports device-side errors of the

@@ -74,6 +74,13 @@ void bind(const ff_ctx* ctx) {
   if (ctx) ffb::cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
 }
 
+// row gather: 4 warps per CTA (FF_GATHER_THREADS), each with a [32][pitch]
+// fp64 row accumulator; pitch = longest row rounded up to odd
+constexpr int kGatherWarps = 4;
+constexpr int kGatherSmemMax = 227 * 1024;
+int gather_pitch(int max_row_len) { return max_row_len | 1; }
+int gather_smem(int pitch) { return kGatherWarps * 32 * pitch * 8; }
+
 void load_module(ff_form* f, int w) {
   if (f->kernel[w] || !f->ctx) return;
   bind(f->ctx);
@@ -89,6 +96,15 @@ void load_module(ff_form* f, int w) {
   } else {
     cudaGetLastError();
     f->kernel_tile[w] = nullptr;
+  }
+  if (cudaLibraryGetKernel(&f->kernel_ginv[w], f->lib[w], "ff_gather_invariants") == cudaSuccess &&
+      cudaLibraryGetKernel(&f->kernel_grows[w], f->lib[w], "ff_gather_rows") == cudaSuccess) {
+    ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_grows[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    kGatherSmemMax, f->ctx->device),
+                    "row-gather shared memory attribute");
+  } else {
+    cudaGetLastError();
+    f->kernel_ginv[w] = f->kernel_grows[w] = nullptr;
   }
   cudaFuncAttributes attr{};
   if (cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(f->kernel[w])) == cudaSuccess) {
@@ -184,6 +200,107 @@ void ensure_tile_plan(ff_pattern* p, const ff_mesh* m, const codegen::RowTilePar
   p->tile_chunk = tp.chunk;
 }
 
+void free_gather(ff_pattern* p) {
+  ffb::kernels::free_gather_plan(&p->gather);
+  p->gather_generation = ~0ull;
+  p->gather_mesh = nullptr;
+}
+
+void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
+  ensure_plan(p, m);
+  if (p->gather_mesh == m && p->gather_generation == m->generation && p->gather.rec) return;
+  require(p->slot_bytes == 1, "row gather needs rows of <= 256 entries");
+  free_gather(p);
+  ff_ctx* ctx = p->ctx;
+  bind(ctx);
+  const auto t0 = std::chrono::steady_clock::now();
+  const cudaError_t e = ffb::kernels::build_gather_plan(m->dconn, m->ne, m->k, p->rb, p->re - p->rb,
+                                                        static_cast<const uint8_t*>(p->slots), 4096, ctx->sm_count,
+                                                        ctx->stream, &p->gather);
+  if (e != cudaSuccess) {
+    ffb::kernels::free_gather_plan(&p->gather);
+    check_alloc(e, "row-gather plan");
+  }
+  p->gather_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  p->gather_mesh = m;
+  p->gather_generation = m->generation;
+}
+
+// The scatter a (form, pattern, flags) assembly runs (FF_SCATTER_*_MODE).
+int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w) {
+  int mode = f->ctx ? f->ctx->scatter : FF_SCATTER_GATHER_MODE;
+  if (flags & FF_SCATTER_ATOMIC) mode = FF_SCATTER_ATOMIC_MODE;
+  if (flags & FF_SCATTER_TILES) mode = FF_SCATTER_ROWTILE;
+  if (flags & (FF_SCATTER_GATHER | FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) mode = FF_SCATTER_GATHER_MODE;
+  if (flags & (FF_ZERO_ONLY | FF_SKIP_ZERO)) mode = FF_SCATTER_ATOMIC_MODE;
+  if (mode == FF_SCATTER_GATHER_MODE &&
+      !(f->kernel_grows[w] && p->max_row_len <= 256 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax))
+    mode = FF_SCATTER_ATOMIC_MODE;
+  if (mode == FF_SCATTER_ROWTILE && !f->kernel_tile[w]) mode = FF_SCATTER_ATOMIC_MODE;
+  return mode;
+}
+
+void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
+                   unsigned flags, int w) {
+  ff_ctx* ctx = f->ctx;
+  ensure_gather_plan(p, m);
+  const int nkp = f->plan.n_kinv + (f->plan.n_kinv & 1);
+  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * nkp;
+  const std::size_t nb = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * m->k;
+  if (p->ginv_cap < ng) {
+    cudaFree(p->ginv);
+    p->ginv = nullptr;
+    p->ginv = device_alloc<double>(ng, "element invariants");
+    p->ginv_cap = ng;
+  }
+  if (p->bvec_cap < nb) {
+    cudaFree(p->bvec);
+    p->bvec = nullptr;
+    p->bvec = device_alloc<double>(nb, "element load vectors");
+    p->bvec_cap = nb;
+  }
+  unsigned long long* status = ctx->d_status;
+  if (!(flags & FF_GATHER_ROWS_ONLY)) {
+    ffb::cuda_check(cudaMemsetAsync(status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
+    if (m->ne > 0) {
+      const double* coords = m->coords;
+      const int32_t* vconn = m->vconn;
+      const int32_t* dconn = m->dconn;
+      long long ne = m->ne;
+      double* ginv = p->ginv;
+      double* bvec = p->bvec;
+      void* args[] = {&coords, &vconn, &dconn, &ne, &ginv, &bvec, &status};
+      const unsigned grid = static_cast<unsigned>((m->ne + f->block - 1) / f->block);
+      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_ginv[w]), dim3(grid), dim3(f->block),
+                                       args, 0, s),
+                      "K2a (element invariants) launch");
+    }
+  }
+  if (flags & FF_GATHER_INVARIANTS_ONLY) return;
+  if (p->gather.n_items == 0) return;
+  const int pitch = gather_pitch(p->max_row_len);
+  const int smem = gather_smem(pitch);
+  int per_sm = 0;
+  ffb::cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                      &per_sm, reinterpret_cast<const void*>(f->kernel_grows[w]), kGatherWarps * 32, smem),
+                  "row-gather occupancy");
+  const int64_t want = (p->gather.n_items + kGatherWarps - 1) / kGatherWarps;
+  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(per_sm, 1)) * ctx->sm_count)));
+  const double* ginv = p->ginv;
+  const double* bvec = p->bvec;
+  const int64_t* row_ptr = p->row_ptr;
+  const int32_t* wrows = p->gather.warp_rows;
+  const int32_t* wsteps = p->gather.warp_steps;
+  const int64_t* wrec = p->gather.warp_rec;
+  const void* rec = p->gather.rec;
+  long long n_items = p->gather.n_items;
+  int pitch_arg = pitch;
+  void* args[] = {&ginv, &bvec, &row_ptr, &d_values, &d_rhs, &wrows, &wsteps, &wrec, &rec, &n_items, &pitch_arg};
+  ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
+                                   dim3(kGatherWarps * 32), args, smem, s),
+                  "K2b (row gather) launch");
+}
+
 void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
                      unsigned flags = 0) {
   require(f->ctx && f->ctx == m->ctx && m->ctx == p->ctx, "form, mesh and pattern must share one context");
@@ -194,9 +311,12 @@ void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_valu
   build_variant(f, w);
   ff_ctx* ctx = f->ctx;
   const int64_t n_rows = p->re - p->rb;
-  const bool tiles = !(flags & FF_SCATTER_ATOMIC) && ctx->scatter == FF_SCATTER_ROWTILE && f->kernel_tile[w] &&
-                     !(flags & (FF_ZERO_ONLY | FF_SKIP_ZERO));
-  if (tiles) {
+  const int mode = select_scatter(f, p, flags, w);
+  if (mode == FF_SCATTER_GATHER_MODE) {
+    launch_gather(f, m, p, d_values, d_rhs, s, flags, w);
+    return;
+  }
+  if (mode == FF_SCATTER_ROWTILE) {
     ensure_tile_plan(p, m, f->tile);
     ffb::cuda_check(cudaMemsetAsync(ctx->d_status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
     if (p->n_tiles == 0) return;
@@ -272,7 +392,7 @@ int ff_init(int device, ff_ctx** out) {
     ffb::cuda_check(cudaSetDevice(device), "cudaSetDevice");
     ffb::cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attribute");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    c->d_status = device_alloc<unsigned long long>(2, "status");
+    c->d_status = device_alloc<unsigned long long>(3, "status");  // [bad_elem, bad_row, scratch]
     ffb::cuda_check(cudaMallocHost(&c->h_status, 2 * sizeof(unsigned long long)), "cudaMallocHost");
     ffb::cuda_check(cudaMemset(c->d_status, 0xff, 2 * sizeof(unsigned long long)), "memset");
     *out = c.release();
@@ -304,7 +424,8 @@ void* ff_ctx_stream(ff_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) 
 int ff_ctx_set_scatter(ff_ctx* ctx, int mode) {
   return guarded([&] {
     require(ctx, "null context");
-    require(mode == FF_SCATTER_ROWTILE || mode == FF_SCATTER_ATOMIC_MODE, "unknown scatter mode");
+    require(mode == FF_SCATTER_ROWTILE || mode == FF_SCATTER_ATOMIC_MODE || mode == FF_SCATTER_GATHER_MODE,
+            "unknown scatter mode");
     ctx->scatter = mode;
   });
 }
@@ -405,6 +526,8 @@ int ff_form_info_get(const ff_form* f, ff_form_info* o) {
     o->registers = f->module[1].registers;
     o->shared_bytes = f->module[1].shared_bytes;
     o->compile_ms = f->compile_ms;
+    o->n_kinv = (!f->raw && f->plan.n_kinv > 0 && f->n_local <= 12) ? f->plan.n_kinv : 0;
+    o->row_flops = f->plan.row_flops;
   });
 }
 
@@ -544,6 +667,9 @@ int ff_pattern_destroy(ff_pattern* p) {
     cudaFree(p->col_idx);
     cudaFree(p->slots);
     free_tile_plan(p);
+    free_gather(p);
+    cudaFree(p->ginv);
+    cudaFree(p->bvec);
     cudaFree(p->e2e_values);
     cudaFree(p->e2e_rhs);
     delete p;
@@ -554,6 +680,26 @@ int ff_pattern_prepare(ff_pattern* p, const ff_mesh* m) {
   return guarded([&] {
     require(p && m, "null argument");
     ensure_plan(p, m);
+  });
+}
+
+int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* m, ff_gather_info* out) {
+  return guarded([&] {
+    require(p && m && out, "null argument");
+    require(m->k <= 12, "row gather supports at most 12 DOFs per element");
+    ensure_gather_plan(p, m);
+    out->n_items = p->gather.n_items;
+    out->n_steps = p->gather.n_steps;
+    out->n_incidences = p->gather.n_incidences;
+    out->record_bytes = p->gather.rec_bytes;
+    out->build_ms = p->gather_ms;
+  });
+}
+
+int ff_scatter_selected(const ff_form* f, const ff_pattern* p, unsigned flags, int* mode) {
+  return guarded([&] {
+    require(f && p && mode, "null argument");
+    *mode = select_scatter(f, p, flags, p->max_row_len <= 256 ? 1 : 2);
   });
 }
 
@@ -570,7 +716,7 @@ int ff_assemble_device_ex(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d
                           unsigned flags) {
   return guarded([&] {
     require(f && m && p && d_values && d_rhs, "ff_assemble_device_ex: null argument");
-    require(flags < 8, "unknown flags");
+    require(flags < 128, "unknown flags");
     bind(f->ctx);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : f->ctx->stream;
     launch_assembly(f, m, p, d_values, d_rhs, s, flags);
@@ -601,8 +747,29 @@ int ff_assemble(ff_form* f, ff_mesh* m, ff_pattern* p, const double* coords, con
       ffb::cuda_check(cudaMemcpyAsync(m->vconn, vconn, m->ne * (m->dim + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
     if (dconn && m->dconn != m->vconn)
       ffb::cuda_check(cudaMemcpyAsync(m->dconn, dconn, m->ne * m->k * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    if (vconn || dconn) ++m->generation;  // re-derive + re-validate the slot plan, as the
-                                          // reference re-searches every column (device.cpp:274-288)
+    if (vconn || dconn) {
+      // The reference re-searches every column on every call (device.cpp:274-288);
+      // here the slot and gather plans are re-derived (and re-validated) whenever
+      // the uploaded connectivity differs from the one they were built for.
+      ffb::cuda_check(ffb::kernels::content_hash(m->dconn, m->ne * m->k, ctx->d_status + 2, ctx->sm_count, ctx->stream),
+                      "connectivity hash");
+      unsigned long long h = 0;
+      ffb::cuda_check(cudaMemcpyAsync(&h, ctx->d_status + 2, sizeof h, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+      ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "connectivity hash");
+      if (m->dconn != m->vconn) {
+        ffb::cuda_check(ffb::kernels::content_hash(m->vconn, m->ne * (m->dim + 1), ctx->d_status + 2, ctx->sm_count,
+                                                   ctx->stream),
+                        "connectivity hash");
+        unsigned long long hv = 0;
+        ffb::cuda_check(cudaMemcpyAsync(&hv, ctx->d_status + 2, sizeof hv, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "connectivity hash");
+        h = h * 31 + hv;
+      }
+      if (h != m->conn_hash || m->generation == 0) {
+        m->conn_hash = h;
+        ++m->generation;
+      }
+    }
     const int64_t n_rows = p->re - p->rb;
     if (!p->e2e_values) p->e2e_values = device_alloc<double>(p->nnz, "values");
     if (!p->e2e_rhs) p->e2e_rhs = device_alloc<double>(n_rows, "rhs");

@@ -354,6 +354,42 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
     for (const auto& [t, c] : by_inv) row_sig[r].push_back({t, static_cast<double>(c)});
     same[row_sig[r]].push_back(static_cast<int>(r));
   }
+  // row-gather split: invariants read by the bilinear entries, in t order
+  const int nn = f.n_local * f.n_local;
+  std::map<int, int> kq;
+  for (int r = 0; r < nn; ++r)
+    for (const auto& [t, c] : row_sig[r]) kq.emplace(t, 0);
+  {
+    int q = 0;
+    for (auto& [t, slot] : kq) slot = q++;
+  }
+  plan.n_kinv = static_cast<int>(kq.size());
+  for (const auto& [t, q] : kq) os << "  FF_KINV(" << q << ", ff_t" << t << ");\n";
+  {
+    // ff_row<i>: v[j] = K_ij with the same expression (term order, literals)
+    // as the element body, so both scatters compute bit-identical entries
+    std::ostringstream rc;
+    for (int i = 0; i < f.n_local; ++i) {
+      rc << "template <> __device__ __forceinline__ void ff_row<" << i
+         << ">(const double* __restrict__ g, double* __restrict__ v) {\n";
+      for (int j = 0; j < f.n_local; ++j) {
+        const auto& sig = row_sig[i * f.n_local + j];
+        std::string v = sig.empty() ? "0.0" : "";
+        for (std::size_t q = 0; q < sig.size(); ++q) {
+          const double c = sig[q].second;
+          const std::string t = "g[" + std::to_string(kq.at(sig[q].first)) + "]";
+          if (q == 0)
+            v = c == 1.0 ? t : c == -1.0 ? "-" + t : double_literal(c) + " * " + t;
+          else
+            v += c == 1.0 ? " + " + t : c == -1.0 ? " - " + t : " + " + double_literal(c) + " * " + t;
+          plan.row_flops += 2;
+        }
+        rc << "  v[" << j << "] = " << v << ";\n";
+      }
+      rc << "}\n";
+    }
+    plan.row_code = rc.str();
+  }
   // rows already grouped; emit in entry order of the group's first member
   std::vector<std::vector<int>> ordered;
   for (auto& [sig, members] : same) ordered.push_back(members);

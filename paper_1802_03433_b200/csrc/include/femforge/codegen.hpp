@@ -98,6 +98,13 @@ struct ElementPlan {
   int n_invariants = 0;    // ReferenceTensor: merged geometric invariants
   int n_unique_entries = 0;
   std::int64_t flops = 0;  // fp64 operations per element after CSE (estimate)
+  // Row-gather split (ReferenceTensor only): the invariants the bilinear
+  // entries read (stored per element by the invariants kernel, body lines
+  // FF_KINV(q, ff_tT)), and per local row i the static code computing
+  // v[j] = K_ij from g[q] (ff_row<i> specialisations).
+  int n_kinv = 0;
+  std::string row_code;
+  std::int64_t row_flops = 0;  // fp64 operations of all n_local rows
 };
 
 ElementPlan plan_element(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule,
@@ -108,6 +115,7 @@ enum class Scatter : int {
   Auto = 0,
   Atomic = 1,     // element-parallel, fp64 RED into CSR slots (K0 zero-fill first)
   RowTiles = 2,   // row-tile ownership: atomic-free, each CSR slot written once
+  Gather = 3,     // row per lane: element invariants + lock-step row gather
 };
 
 struct LaunchParams {

@@ -26,6 +26,24 @@ cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_
                                cudaStream_t s, int64_t** tile_vptr, int32_t** visit_elem, uint16_t** visit_stage,
                                int64_t* n_visits);
 
+// Row-gather plan (one CSR row per lane, 32 rows per warp item, lock-step
+// records [step][32] of (element id, k slot bytes); see pattern.cu).
+struct GatherPlan {
+  int64_t n_items = 0, n_steps = 0, n_incidences = 0;
+  int rec_bytes = 0;                 // 8 (k <= 4) or 16 (k <= 12)
+  int32_t* warp_rows = nullptr;      // [n_items][32] local row or -1
+  int32_t* warp_steps = nullptr;     // [n_items][k]
+  int64_t* warp_rec = nullptr;       // [n_items + 1] first record step of each item
+  void* rec = nullptr;               // [n_steps][32] records
+};
+cudaError_t build_gather_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
+                              const uint8_t* d_slots, int window, int sm_count, cudaStream_t s, GatherPlan* out);
+void free_gather_plan(GatherPlan* p);
+
+// Order-independent 64-bit content hash of n int32 values (sum of mixed
+// (index, value) pairs), written to *d_out.
+cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_out, int sm_count, cudaStream_t s);
+
 // K0: values[0:na] = 0, rhs[0:nb] = 0, status[0:2] = ~0 (one launch).
 cudaError_t zero_fill(double* a, int64_t na, double* b, int64_t nb, unsigned long long* status, int sm_count,
                       cudaStream_t s);

@@ -12,6 +12,7 @@
 // entry) is derived from the finished pattern with one binary search per
 // entry; it is what lets the numeric kernel scatter without any search.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
 #include <cstdint>
@@ -196,6 +197,166 @@ __global__ void chunk_visits(const int32_t* __restrict__ dconn, int k, int64_t r
   }
 }
 
+
+// ---- row-gather plan ---------------------------------------------------------
+//
+// The row-gather kernel (assemble_template.inc: ff_gather_rows) gives every
+// owned CSR row to one lane. This plan (built once per (pattern, mesh)):
+//  1. lists the incidences (e, i) of every row (element e has the row's DOF at
+//     local index i) and sorts them by (i, slot bytes, e);
+//  2. hashes that (i, slot bytes) sequence into a row signature and orders the
+//     rows by (window of consecutive rows, signature), so that warps of 32
+//     rows step in lock-step through identical incidence sequences (on a
+//     structured mesh the 32 lanes then read the same slot pattern and their
+//     shared-memory row accumulators never collide on a bank);
+//  3. per warp item and local index i, the lock-step count = max over lanes;
+//  4. the records [step][32]: element id + the k slot bytes of (e, i).
+
+__global__ void inc_count(const int32_t* __restrict__ dconn, int64_t nk, int64_t rb, int64_t n_rows,
+                          int32_t* __restrict__ cnt) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nk;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = static_cast<int64_t>(dconn[t]) - rb;
+    if (r >= 0 && r < n_rows) atomicAdd(cnt + r, 1);
+  }
+}
+
+__global__ void inc_fill(const int32_t* __restrict__ dconn, int64_t nk, int64_t rb, int64_t n_rows,
+                         int64_t* __restrict__ cursor, int32_t* __restrict__ inc) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nk;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = static_cast<int64_t>(dconn[t]) - rb;
+    if (r >= 0 && r < n_rows) inc[atomicAdd(reinterpret_cast<unsigned long long*>(cursor + r), 1ull)] =
+        static_cast<int32_t>(t);
+  }
+}
+
+// (i, slot bytes, e) order of two incidences t = e*k + i
+__device__ __forceinline__ bool inc_less(int32_t a, int32_t b, int k, const uint8_t* __restrict__ slots) {
+  const int ia = a % k, ib = b % k;
+  if (ia != ib) return ia < ib;
+  const uint8_t* sa = slots + static_cast<int64_t>(a) * k;
+  const uint8_t* sb = slots + static_cast<int64_t>(b) * k;
+  for (int j = 0; j < k; ++j)
+    if (sa[j] != sb[j]) return sa[j] < sb[j];
+  return a < b;
+}
+
+__global__ void inc_sort_sign(const int64_t* __restrict__ inc_ptr, int64_t n_rows, int k,
+                              const uint8_t* __restrict__ slots, int32_t* __restrict__ inc, uint64_t* __restrict__ sig) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = inc_ptr[r], e = inc_ptr[r + 1];
+    for (int64_t p = b + 1; p < e; ++p) {  // insertion sort (rows hold a few dozen incidences)
+      const int32_t x = inc[p];
+      int64_t q = p - 1;
+      while (q >= b && inc_less(x, inc[q], k, slots)) {
+        inc[q + 1] = inc[q];
+        --q;
+      }
+      inc[q + 1] = x;
+    }
+    uint64_t h = 1469598103934665603ull;  // FNV-1a over (i, slot bytes) of the sorted list
+    for (int64_t p = b; p < e; ++p) {
+      const int32_t t = inc[p];
+      h = (h ^ static_cast<uint64_t>(t % k + 1)) * 1099511628211ull;
+      const uint8_t* sl = slots + static_cast<int64_t>(t) * k;
+      for (int j = 0; j < k; ++j) h = (h ^ sl[j]) * 1099511628211ull;
+    }
+    sig[r] = h;
+  }
+}
+
+__global__ void row_order_keys(const uint64_t* __restrict__ sig, int64_t n_rows, int window, uint64_t* __restrict__ keys,
+                               int32_t* __restrict__ rows) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    keys[r] = (static_cast<uint64_t>(r / window) << 40) | (sig[r] >> 24);
+    rows[r] = static_cast<int32_t>(r);
+  }
+}
+
+__global__ void item_steps(const int32_t* __restrict__ order, int64_t n_rows, int64_t n_items, int k,
+                           const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
+                           int32_t* __restrict__ warp_rows, int32_t* __restrict__ warp_steps,
+                           int64_t* __restrict__ item_total) {
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < n_items;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int mx[32];
+    for (int i = 0; i < k; ++i) mx[i] = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int64_t pos = w * 32 + l;
+      const int32_t row = pos < n_rows ? order[pos] : -1;
+      warp_rows[pos] = row;
+      if (row < 0) continue;
+      int64_t p = inc_ptr[row];
+      const int64_t e = inc_ptr[row + 1];
+      for (int i = 0; i < k; ++i) {
+        int c = 0;
+        while (p < e && inc[p] % k == i) {
+          ++c;
+          ++p;
+        }
+        mx[i] = max(mx[i], c);
+      }
+    }
+    int64_t tot = 0;
+    for (int i = 0; i < k; ++i) {
+      warp_steps[w * k + i] = mx[i];
+      tot += mx[i];
+    }
+    item_total[w] = tot;
+  }
+}
+
+template <int K>
+__global__ void fill_records(const int32_t* __restrict__ warp_rows, const int32_t* __restrict__ warp_steps,
+                             const int64_t* __restrict__ warp_rec, int64_t n_items, const int64_t* __restrict__ inc_ptr,
+                             const int32_t* __restrict__ inc, const uint8_t* __restrict__ slots, void* __restrict__ rec) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_items * 32;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = t / 32;
+    const int lane = static_cast<int>(t % 32);
+    const int32_t row = warp_rows[t];
+    int64_t p = row >= 0 ? inc_ptr[row] : 0;
+    const int64_t pe = row >= 0 ? inc_ptr[row + 1] : 0;
+    int64_t step = warp_rec[w];
+    for (int i = 0; i < K; ++i) {
+      const int n = warp_steps[w * K + i];
+      for (int s = 0; s < n; ++s, ++step) {
+        uint32_t word[4] = {0xffffffffu, 0u, 0u, 0u};
+        if (p < pe && inc[p] % K == i) {
+          const int32_t x = inc[p++];
+          word[0] = static_cast<uint32_t>(x / K);
+          const uint8_t* sl = slots + static_cast<int64_t>(x) * K;
+          for (int j = 0; j < K; ++j) word[1 + j / 4] |= static_cast<uint32_t>(sl[j]) << (8 * (j & 3));
+        }
+        if (K <= 4)
+          reinterpret_cast<uint2*>(rec)[step * 32 + lane] = make_uint2(word[0], word[1]);
+        else
+          reinterpret_cast<uint4*>(rec)[step * 32 + lane] = make_uint4(word[0], word[1], word[2], word[3]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  return x ^ (x >> 33);
+}
+
+__global__ void hash_kernel(const int32_t* __restrict__ a, int64_t n, unsigned long long* __restrict__ out) {
+  unsigned long long h = 0;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    h += mix64((static_cast<unsigned long long>(t) << 32) ^ static_cast<uint32_t>(a[t]));
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
 int grid_for(int64_t n, int sm_blocks) {
   const int64_t g = (n + kThreads - 1) / kThreads;
   return static_cast<int>(g < sm_blocks ? (g < 1 ? 1 : g) : sm_blocks);
@@ -316,6 +477,123 @@ cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_
   if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
   *n_visits = n_unique - ((static_cast<uint64_t>(last_key) >> 32) >= static_cast<uint64_t>(n_tiles) ? 1 : 0);
   return done(cudaGetLastError());
+}
+
+
+cudaError_t build_gather_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
+                              const uint8_t* d_slots, int window, int sm_count, cudaStream_t s, GatherPlan* out) {
+  if (k > 12) return cudaErrorInvalidValue;
+  if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  const int cap = sm_count * 16;
+  const int64_t nk = ne * k;
+  int32_t* cnt = nullptr;
+  int64_t *inc_ptr = nullptr, *cursor = nullptr, *item_total = nullptr;
+  int32_t *inc = nullptr, *rows = nullptr, *order = nullptr;
+  uint64_t *sig = nullptr, *keys = nullptr, *keys2 = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  cudaError_t err = cudaSuccess;
+  auto done = [&](cudaError_t e) {
+    cudaFree(cnt);
+    cudaFree(inc_ptr);
+    cudaFree(cursor);
+    cudaFree(item_total);
+    cudaFree(inc);
+    cudaFree(rows);
+    cudaFree(order);
+    cudaFree(sig);
+    cudaFree(keys);
+    cudaFree(keys2);
+    cudaFree(temp);
+    return e;
+  };
+  auto need_temp = [&](size_t b) -> cudaError_t {
+    if (b <= temp_bytes) return cudaSuccess;
+    cudaFree(temp);
+    temp = nullptr;
+    temp_bytes = b;
+    return cudaMalloc(&temp, b);
+  };
+  const int64_t nr1 = n_rows + 1;
+  if ((err = cudaMalloc(&cnt, nr1 * sizeof(int32_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&inc_ptr, nr1 * sizeof(int64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&cursor, nr1 * sizeof(int64_t))) != cudaSuccess) return done(err);
+  cudaMemsetAsync(cnt, 0, nr1 * sizeof(int32_t), s);
+  if (nk > 0) inc_count<<<grid_for(nk, cap), kThreads, 0, s>>>(d_dconn, nk, rb, n_rows, cnt);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, inc_ptr, nr1, s);
+  if ((err = need_temp(tb)) != cudaSuccess) return done(err);
+  if ((err = cub::DeviceScan::ExclusiveSum(temp, tb, cnt, inc_ptr, nr1, s)) != cudaSuccess) return done(err);
+  int64_t n_inc = 0;
+  cudaMemcpyAsync(&n_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&inc, (n_inc > 0 ? n_inc : 1) * sizeof(int32_t))) != cudaSuccess) return done(err);
+  cudaMemcpyAsync(cursor, inc_ptr, nr1 * sizeof(int64_t), cudaMemcpyDeviceToDevice, s);
+  if (nk > 0) inc_fill<<<grid_for(nk, cap), kThreads, 0, s>>>(d_dconn, nk, rb, n_rows, cursor, inc);
+  if ((err = cudaMalloc(&sig, nr1 * sizeof(uint64_t))) != cudaSuccess) return done(err);
+  if (n_rows > 0) inc_sort_sign<<<grid_for(n_rows, cap), kThreads, 0, s>>>(inc_ptr, n_rows, k, d_slots, inc, sig);
+  // rows ordered by (window, signature); stable, so ties keep ascending rows
+  if ((err = cudaMalloc(&keys, nr1 * sizeof(uint64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&keys2, nr1 * sizeof(uint64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&rows, nr1 * sizeof(int32_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&order, nr1 * sizeof(int32_t))) != cudaSuccess) return done(err);
+  if (n_rows > 0) row_order_keys<<<grid_for(n_rows, cap), kThreads, 0, s>>>(sig, n_rows, window, keys, rows);
+  tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, order, n_rows, 0, 64, s);
+  if ((err = need_temp(tb)) != cudaSuccess) return done(err);
+  if ((err = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, rows, order, n_rows, 0, 64, s)) != cudaSuccess)
+    return done(err);
+  const int64_t n_items = (n_rows + 31) / 32;
+  out->n_items = n_items;
+  if ((err = cudaMalloc(&out->warp_rows, (n_items > 0 ? n_items : 1) * 32 * sizeof(int32_t))) != cudaSuccess)
+    return done(err);
+  if ((err = cudaMalloc(&out->warp_steps, (n_items > 0 ? n_items : 1) * k * sizeof(int32_t))) != cudaSuccess)
+    return done(err);
+  if ((err = cudaMalloc(&out->warp_rec, (n_items + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&item_total, (n_items + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
+  cudaMemsetAsync(item_total, 0, (n_items + 1) * sizeof(int64_t), s);
+  if (n_items > 0)
+    item_steps<<<grid_for(n_items, cap), kThreads, 0, s>>>(order, n_rows, n_items, k, inc_ptr, inc, out->warp_rows,
+                                                           out->warp_steps, item_total);
+  tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, item_total, out->warp_rec, n_items + 1, s);
+  if ((err = need_temp(tb)) != cudaSuccess) return done(err);
+  if ((err = cub::DeviceScan::ExclusiveSum(temp, tb, item_total, out->warp_rec, n_items + 1, s)) != cudaSuccess)
+    return done(err);
+  int64_t total = 0;
+  cudaMemcpyAsync(&total, out->warp_rec + n_items, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+  out->n_steps = total;
+  out->n_incidences = n_inc;
+  out->rec_bytes = k <= 4 ? 8 : 16;
+  if ((err = cudaMalloc(&out->rec, (total > 0 ? total : 1) * 32 * out->rec_bytes)) != cudaSuccess) return done(err);
+  if (n_items > 0) {
+    const int g = grid_for(n_items * 32, cap);
+    switch (k) {
+#define FF_FILL(K) \
+  case K: fill_records<K><<<g, kThreads, 0, s>>>(out->warp_rows, out->warp_steps, out->warp_rec, n_items, inc_ptr, inc, d_slots, out->rec); break;
+      FF_FILL(1) FF_FILL(2) FF_FILL(3) FF_FILL(4) FF_FILL(5) FF_FILL(6) FF_FILL(7) FF_FILL(8) FF_FILL(9) FF_FILL(10)
+      FF_FILL(11) FF_FILL(12)
+#undef FF_FILL
+      default: return done(cudaErrorInvalidValue);
+    }
+  }
+  if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+  return done(cudaGetLastError());
+}
+
+cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_out, int sm_count, cudaStream_t s) {
+  cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s);
+  if (n > 0) hash_kernel<<<grid_for(n, sm_count * 8), kThreads, 0, s>>>(d_a, n, d_out);
+  return cudaGetLastError();
+}
+
+void free_gather_plan(GatherPlan* p) {
+  cudaFree(p->warp_rows);
+  cudaFree(p->warp_steps);
+  cudaFree(p->warp_rec);
+  cudaFree(p->rec);
+  *p = GatherPlan{};
 }
 
 cudaError_t build_slots(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t re, const int64_t* row_ptr,

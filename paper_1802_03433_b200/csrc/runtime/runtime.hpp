@@ -11,6 +11,7 @@
 
 #include "femforge/codegen.hpp"
 #include "femforge/fem.hpp"
+#include "../kernels/kernels.hpp"
 
 namespace ffb {
 
@@ -41,7 +42,7 @@ struct ff_ctx {
   cudaStream_t stream = nullptr;
   unsigned long long* d_status = nullptr;  // [bad_elem, bad_row]
   unsigned long long* h_status = nullptr;  // pinned mirror
-  int scatter = 0;                          // FF_SCATTER_ROWTILE / FF_SCATTER_ATOMIC_MODE
+  int scatter = 2;                          // FF_SCATTER_*_MODE (default: row gather)
 };
 
 struct ff_form {
@@ -61,6 +62,8 @@ struct ff_form {
   cudaKernel_t kernel_tile[3] = {nullptr, nullptr, nullptr};     // ff_assemble_rowtile
   femforge::codegen::RowTileParams tile;
   int tile_smem[3] = {0, 0, 0};
+  cudaKernel_t kernel_ginv[3] = {nullptr, nullptr, nullptr};     // ff_gather_invariants
+  cudaKernel_t kernel_grows[3] = {nullptr, nullptr, nullptr};    // ff_gather_rows
 };
 
 struct ff_mesh {
@@ -72,6 +75,7 @@ struct ff_mesh {
   int32_t* vconn = nullptr;
   int32_t* dconn = nullptr;  // == vconn for P1
   std::uint64_t generation = 0;
+  unsigned long long conn_hash = 0;  // content hash of vconn/dconn (e2e re-upload check)
 };
 
 struct ff_pattern {
@@ -95,6 +99,14 @@ struct ff_pattern {
   int32_t* visit_elem = nullptr;   // [n_visits]
   uint16_t* visit_stage = nullptr; // [n_visits]
   int tile_acc = 0, tile_rows = 0, tile_stage = 0, tile_chunk = 0;
+  // row-gather plan for plan_mesh, and the per-element invariant buffers
+  std::uint64_t gather_generation = ~0ull;
+  const ff_mesh* gather_mesh = nullptr;
+  ffb::kernels::GatherPlan gather;
+  double gather_ms = 0.0;
+  double* ginv = nullptr;   // [ne][nkp]
+  double* bvec = nullptr;   // [ne][k]
+  std::size_t ginv_cap = 0, bvec_cap = 0;
   // device scratch of the host-buffer (end-to-end) entry point
   double* e2e_values = nullptr;
   double* e2e_rhs = nullptr;

@@ -21,6 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libfemforge_b200.so")
 FF_OK, FF_E_ARG, FF_E_DEGENERATE, FF_E_PATTERN, FF_E_NVRTC, FF_E_CUDA, FF_E_FORM, FF_E_MESH, FF_E_SYMBOLIC, FF_E_NOMEM = \
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9
 STRATEGY = {"auto": 0, "tensor": 1, "pointwise": 2}
+SCATTER_MODE = {"rowtile": 0, "atomic": 1, "gather": 2}
+SCATTER_NAME = {v: k for k, v in SCATTER_MODE.items()}
 
 
 class FFError(RuntimeError):
@@ -63,7 +65,15 @@ class FormInfo(C.Structure):
     _fields_ = [("dim", C.c_int), ("degree", C.c_int), ("n_local", C.c_int), ("n_quad", C.c_int),
                 ("strategy", C.c_int), ("n_invariants", C.c_int), ("n_unique_entries", C.c_int),
                 ("flops_per_element", C.c_int64), ("registers", C.c_int), ("shared_bytes", C.c_int),
-                ("compile_ms", C.c_double)]
+                ("compile_ms", C.c_double), ("n_kinv", C.c_int), ("row_flops", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class GatherInfo(C.Structure):
+    _fields_ = [("n_items", C.c_int64), ("n_steps", C.c_int64), ("n_incidences", C.c_int64),
+                ("record_bytes", C.c_int), ("build_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -105,6 +115,8 @@ SIGNATURES = [
     ("ff_pattern_device", C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),
     ("ff_pattern_destroy", C.c_int, [_P]),
     ("ff_pattern_prepare", C.c_int, [_P, _P]),
+    ("ff_pattern_gather_info", C.c_int, [_P, _P, C.POINTER(GatherInfo)]),
+    ("ff_scatter_selected", C.c_int, [_P, _P, C.c_uint, C.POINTER(C.c_int)]),
     ("ff_assemble_device", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("ff_assemble_device_ex", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint]),
     ("ff_check", C.c_int, [_P, C.POINTER(Stats)]),
@@ -166,8 +178,9 @@ class Context:
         _ok(lib().ff_ctx_synchronize(self.h))
 
     def set_scatter(self, mode):
-        """'rowtile' (atomic-free, default) or 'atomic' (fp64 RED after a zero-fill)."""
-        _ok(lib().ff_ctx_set_scatter(self.h, {"rowtile": 0, "atomic": 1}[mode]))
+        """'gather' (row gather, atomic-free, default), 'rowtile' (CTA row tiles,
+        atomic-free) or 'atomic' (fp64 RED after a zero-fill)."""
+        _ok(lib().ff_ctx_set_scatter(self.h, SCATTER_MODE[mode]))
         self.scatter = mode
 
     def check(self):
@@ -299,6 +312,18 @@ class Pattern:
     def prepare(self, mesh):
         _ok(lib().ff_pattern_prepare(self.h, mesh.h))
 
+    def gather_info(self, mesh):
+        """Builds (if needed) and describes the row-gather plan of (pattern, mesh)."""
+        gi = GatherInfo()
+        _ok(lib().ff_pattern_gather_info(self.h, mesh.h, C.byref(gi)))
+        return gi.as_dict()
+
+    def scatter_for(self, form, flags=0):
+        """Name of the scatter the next assembly with `form` runs."""
+        m = C.c_int(0)
+        _ok(lib().ff_scatter_selected(form.h, self.h, flags, C.byref(m)))
+        return SCATTER_NAME[m.value]
+
     def close(self):
         if getattr(self, "h", None):
             lib().ff_pattern_destroy(self.h)
@@ -319,7 +344,8 @@ def assemble_device(form, mesh, pattern, values_ptr, rhs_ptr, stream=None):
                                  _stream(stream)))
 
 
-FF_SKIP_ZERO, FF_ZERO_ONLY, FF_SCATTER_ATOMIC = 1, 2, 4
+FF_SKIP_ZERO, FF_ZERO_ONLY, FF_SCATTER_ATOMIC, FF_SCATTER_TILES, FF_SCATTER_GATHER = 1, 2, 4, 8, 16
+FF_GATHER_INVARIANTS_ONLY, FF_GATHER_ROWS_ONLY = 32, 64
 
 
 def assemble_device_ex(form, mesh, pattern, values_ptr, rhs_ptr, stream=None, flags=0):

@@ -19,11 +19,11 @@ def _golden(pattern):
     return sorted(glob.glob(os.path.join(GOLDEN, pattern)))
 
 
-SCATTERS = ["rowtile", "atomic"]
+SCATTERS = ["gather", "rowtile", "atomic"]
 
 
 def gpu_system(ff, ctx, dim, deg, form, coords, vconn, dconn, n_dofs, quad=0, strategy="auto",
-               row_begin=0, row_end=None, block=256, scatter="rowtile"):
+               row_begin=0, row_end=None, block=256, scatter="gather"):
     ctx.set_scatter(scatter)
     bil, lin = ff.named_form(form, dim) if isinstance(form, str) else form
     f = ff.Form(ctx, dim, deg, bil, lin, quad_rule=quad, strategy=strategy, block_size=block)
@@ -177,20 +177,74 @@ def test_row_blocks_concatenate_to_full_system(ff, ctx, parts, scatter):
     assert normwise(np.concatenate(rhss), rhs) <= TOL
 
 
-@pytest.mark.parametrize("dim,deg,n", [(3, 1, 20), (3, 2, 12), (2, 1, 128)])
-def test_rowtile_is_bitwise_reproducible_and_matches_atomic(ff, ctx, dim, deg, n):
-    """Atomic-free row tiles: fixed summation order -> identical bits on every
+ATOMIC_FREE = [  # (scatter, dim, degree, n, form, quad)
+    ("rowtile", 3, 1, 20, "varcoef", 14),
+    ("rowtile", 3, 2, 12, "varcoef", 14),
+    ("rowtile", 2, 1, 128, "demo2d", 3),
+    ("gather", 3, 1, 20, "helmholtz", 4),
+    ("gather", 3, 2, 12, "poisson", 4),
+    ("gather", 2, 1, 128, "demo2d", 3),
+    ("gather", 2, 2, 40, "helmholtz", 3),
+]
+
+
+@pytest.mark.parametrize("scatter,dim,deg,n,form,quad", ATOMIC_FREE)
+def test_atomic_free_scatter_is_bitwise_reproducible_and_matches_atomic(ff, ctx, scatter, dim, deg, n, form, quad):
+    """Atomic-free scatters: fixed summation order -> identical bits on every
     run (the reference's deterministic-mode property, criterion 7/8)."""
     c, v, d, nd = _mesh(ff, dim, deg, n)
-    form = "varcoef" if dim == 3 else "demo2d"
-    quad = 14 if dim == 3 else 3
-    rp, ci, v1, b1, f, m, p = gpu_system(ff, ctx, dim, deg, form, c, v, d, nd, quad=quad, scatter="rowtile")
+    rp, ci, v1, b1, f, m, p = gpu_system(ff, ctx, dim, deg, form, c, v, d, nd, quad=quad, scatter=scatter)
+    assert p.scatter_for(f) == scatter
     v2, b2 = ff.assemble(f, m, p)
     assert v1.tobytes() == v2.tobytes() and b1.tobytes() == b2.tobytes()
     ctx.set_scatter("atomic")
     va, ba = ff.assemble(f, m, p)
-    ctx.set_scatter("rowtile")
+    ctx.set_scatter(scatter)
     assert normwise(va, v1) <= 1e-14 and normwise(ba, b1) <= 1e-14
+
+
+@pytest.mark.parametrize("dim,deg,n", [(3, 2, 8), (3, 1, 12), (2, 1, 32), (2, 2, 16)])
+def test_gather_plan_covers_every_incidence(ff, ctx, dim, deg, n):
+    c, v, d, nd = _mesh(ff, dim, deg, n)
+    ctx.set_scatter("gather")
+    b, l = ff.named_form("poisson", dim)
+    f = ff.Form(ctx, dim, deg, b, l)
+    m = ff.Mesh(ctx, dim, c, v, None if deg == 1 else d, nd)
+    p = ff.Pattern(ctx, m)
+    gi = p.gather_info(m)
+    k = d.shape[1]
+    assert gi["n_incidences"] == d.shape[0] * k           # every (element, local row) once
+    assert gi["n_items"] == -(-nd // 32)
+    assert gi["n_steps"] * 32 >= gi["n_incidences"]
+    assert gi["record_bytes"] == (8 if k <= 4 else 16)
+    assert f.info["n_kinv"] > 0
+
+
+def test_gather_falls_back_to_atomic_for_pointwise_forms(ff, ctx):
+    c, v, d, nd = _mesh(ff, 3, 2, 4)
+    ctx.set_scatter("gather")
+    b, l = ff.named_form("varcoef", 3)
+    f = ff.Form(ctx, 3, 2, b, l, quad_rule=14)
+    assert f.info["strategy"] == 2 and f.info["n_kinv"] == 0
+    m = ff.Mesh(ctx, 3, c, v, d, nd)
+    p = ff.Pattern(ctx, m)
+    assert p.scatter_for(f) == "atomic"
+    assert p.scatter_for(f, ff.FF_SCATTER_TILES) == "rowtile"
+
+
+def test_gather_phases_compose(ff, ctx):
+    """K2a (invariants) then K2b (rows) launched separately == one call."""
+    import torch
+    c, v, d, nd = _mesh(ff, 3, 2, 6)
+    rp, ci, val, rhs, f, m, p = gpu_system(ff, ctx, 3, 2, "poisson", c, v, d, nd, scatter="gather")
+    dv = torch.full((p.nnz,), float("nan"), dtype=torch.float64, device="cuda")
+    db = torch.full((p.n_rows,), float("nan"), dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    ff.assemble_device_ex(f, m, p, dv.data_ptr(), db.data_ptr(), s, ff.FF_GATHER_INVARIANTS_ONLY)
+    ff.assemble_device_ex(f, m, p, dv.data_ptr(), db.data_ptr(), s, ff.FF_GATHER_ROWS_ONLY)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert dv.cpu().numpy().tobytes() == val.tobytes() and db.cpu().numpy().tobytes() == rhs.tobytes()
 
 
 def test_north_star_size_properties(ff, ctx):
@@ -201,7 +255,7 @@ def test_north_star_size_properties(ff, ctx):
     n = 128
     c, v, d, nd = _mesh(ff, 3, 2, n)
     b, l = ff.named_form("poisson", 3)
-    ctx.set_scatter("rowtile")
+    ctx.set_scatter("gather")
     f = ff.Form(ctx, 3, 2, b, l)
     m = ff.Mesh(ctx, 3, c, v, d, nd)
     p = ff.Pattern(ctx, m)
@@ -227,3 +281,12 @@ def test_north_star_size_properties(ff, ctx):
     assert torch.equal(tkey[order], key)  # pattern symmetric
     assert float((vals[order] - vals).abs().max() / amax) <= 1e-12
     assert abs(float(rhs.sum()) - 34.0) <= 1e-9
+    # the atomic-free gather against the element-parallel fp64-RED kernel
+    va = torch.empty_like(vals)
+    ra = torch.empty_like(rhs)
+    ff.assemble_device_ex(f, m, p, va.data_ptr(), ra.data_ptr(), torch.cuda.current_stream().cuda_stream,
+                          ff.FF_SCATTER_ATOMIC)
+    torch.cuda.synchronize()
+    ctx.check()
+    assert float((va - vals).abs().max() / amax) <= 1e-12
+    assert float((ra - rhs).abs().max() / rhs.abs().max()) <= 1e-12
