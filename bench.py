@@ -241,12 +241,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1802_03433_b200 import femforge as ff
+    from paper_1802_03433_b200 import rowblocks
 
     coords, vconn, dconn, n_dofs = make_mesh(ff, cfg)
     E = vconn.shape[0]
-    rb, re = ff.partition_rows(n_dofs, world, rank)
+    rb, re = rowblocks.row_block(n_dofs, world, rank)
     if world > 1:
-        ids = ff.select_elements(dconn, rb, re)   # owned + halo elements
+        ids = rowblocks.local_elements(dconn, rb, re)   # owned + halo elements
         vconn_l, dconn_l = np.ascontiguousarray(vconn[ids]), np.ascontiguousarray(dconn[ids])
     else:
         vconn_l, dconn_l = vconn, dconn
@@ -338,9 +339,9 @@ def main():
         e2e = {"value": E / float(e2e_s), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(hval.nbytes + hrhs.nbytes), "ms_per_step": 1e3 * float(e2e_s)}
 
-    nnz_tot = torch.tensor([pat.nnz], dtype=torch.int64, device="cuda")
-    if world > 1:
-        dist.all_reduce(nnz_tot)
+    nnz_tot = pat.nnz
+    if world > 1:  # global CSR offsets: exclusive prefix over the ranks' (rows, nnz), SURVEY §8e
+        _, _, _, nnz_tot = rowblocks.global_offsets(pat.nnz, pat.n_rows)
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -370,7 +371,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic structured mesh)",
         "config": {"workload": cfg["workload"], "n": cfg["n"], "elements": int(E), "dofs": int(n_dofs),
-                   "nnz": int(nnz_tot.item()), "form": cfg["form"], "quad_rule": cfg["quad"],
+                   "nnz": int(nnz_tot), "form": cfg["form"], "quad_rule": cfg["quad"],
                    "parallelism": f"row-blocks x{world} (halo elements duplicated, no collective)",
                    "l2": "flushed (256 MiB write) between steps" if need_flush else
                          f"inputs > L2 (CSR values {values.numel() * 8 / 1e9:.2f} GB)",
