@@ -214,9 +214,25 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
   ff_ctx* ctx = p->ctx;
   bind(ctx);
   const auto t0 = std::chrono::steady_clock::now();
-  const cudaError_t e = ffb::kernels::build_gather_plan(m->dconn, m->ne, m->k, p->rb, p->re - p->rb,
-                                                        static_cast<const uint8_t*>(p->slots), 4096, ctx->sm_count,
-                                                        ctx->stream, &p->gather);
+  // bounding box of the coordinates (host copy; the Morton order of the DOF
+  // points only needs it to quantise)
+  std::vector<double> xyz(static_cast<std::size_t>(m->nv) * m->dim);
+  if (!xyz.empty())
+    ffb::cuda_check(cudaMemcpy(xyz.data(), m->coords, xyz.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  double bbox[6] = {0, 0, 0, 0, 0, 0};
+  for (int c = 0; c < m->dim; ++c) {
+    double lo = 0, hi = 0;
+    for (int64_t v = 0; v < m->nv; ++v) {
+      const double x = xyz[v * m->dim + c];
+      if (v == 0 || x < lo) lo = x;
+      if (v == 0 || x > hi) hi = x;
+    }
+    bbox[c] = lo;
+    bbox[3 + c] = hi;
+  }
+  const cudaError_t e = ffb::kernels::build_gather_plan(m->coords, m->vconn, m->dim, bbox, m->dconn, m->ne, m->k, p->rb,
+                                                        p->re - p->rb, static_cast<const uint8_t*>(p->slots), 4096,
+                                                        ctx->sm_count, ctx->stream, &p->gather);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
@@ -244,20 +260,13 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
                    unsigned flags, int w) {
   ff_ctx* ctx = f->ctx;
   ensure_gather_plan(p, m);
-  const int nkp = f->plan.n_kinv + (f->plan.n_kinv & 1);
-  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * nkp;
-  const std::size_t nb = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * m->k;
+  const int erec = (f->plan.n_kinv + m->k + 1) & ~1;  // FF_EREC
+  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * erec;
   if (p->ginv_cap < ng) {
     cudaFree(p->ginv);
     p->ginv = nullptr;
     p->ginv = device_alloc<double>(ng, "element invariants");
     p->ginv_cap = ng;
-  }
-  if (p->bvec_cap < nb) {
-    cudaFree(p->bvec);
-    p->bvec = nullptr;
-    p->bvec = device_alloc<double>(nb, "element load vectors");
-    p->bvec_cap = nb;
   }
   unsigned long long* status = ctx->d_status;
   if (!(flags & FF_GATHER_ROWS_ONLY)) {
@@ -268,8 +277,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       const int32_t* dconn = m->dconn;
       long long ne = m->ne;
       double* ginv = p->ginv;
-      double* bvec = p->bvec;
-      void* args[] = {&coords, &vconn, &dconn, &ne, &ginv, &bvec, &status};
+      void* args[] = {&coords, &vconn, &dconn, &ne, &ginv, &status};
       const unsigned grid = static_cast<unsigned>((m->ne + f->block - 1) / f->block);
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_ginv[w]), dim3(grid), dim3(f->block),
                                        args, 0, s),
@@ -287,7 +295,6 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   const int64_t want = (p->gather.n_items + kGatherWarps - 1) / kGatherWarps;
   const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(per_sm, 1)) * ctx->sm_count)));
   const double* ginv = p->ginv;
-  const double* bvec = p->bvec;
   const int64_t* row_ptr = p->row_ptr;
   const int32_t* wrows = p->gather.warp_rows;
   const int32_t* wsteps = p->gather.warp_steps;
@@ -295,7 +302,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   const void* rec = p->gather.rec;
   long long n_items = p->gather.n_items;
   int pitch_arg = pitch;
-  void* args[] = {&ginv, &bvec, &row_ptr, &d_values, &d_rhs, &wrows, &wsteps, &wrec, &rec, &n_items, &pitch_arg};
+  void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &wrows, &wsteps, &wrec, &rec, &n_items, &pitch_arg};
   ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
                                    dim3(kGatherWarps * 32), args, smem, s),
                   "K2b (row gather) launch");
@@ -526,7 +533,8 @@ int ff_form_info_get(const ff_form* f, ff_form_info* o) {
     o->registers = f->module[1].registers;
     o->shared_bytes = f->module[1].shared_bytes;
     o->compile_ms = f->compile_ms;
-    o->n_kinv = (!f->raw && f->plan.n_kinv > 0 && f->n_local <= 12) ? f->plan.n_kinv : 0;
+    o->n_kinv = (!f->raw && f->plan.n_kinv > 0 && f->n_local <= 12 && f->plan.n_kinv + f->n_local <= 24)
+                    ? f->plan.n_kinv : 0;
     o->row_flops = f->plan.row_flops;
   });
 }

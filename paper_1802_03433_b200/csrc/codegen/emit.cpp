@@ -71,7 +71,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
                      std::to_string(plan.flops) + " flops\n" + plan.body;
   fill(text, "ELEMENT_BODY", body);
   // the row gather needs a reference-tensor plan and <= 12 slot bytes per record
-  const bool gather = plan.n_kinv > 0 && f.n_local <= 12;
+  const bool gather = plan.n_kinv > 0 && f.n_local <= 12 && plan.n_kinv + f.n_local <= 24;
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
   if (text.find("{{") != std::string::npos) throw CodegenError("unresolved placeholder");

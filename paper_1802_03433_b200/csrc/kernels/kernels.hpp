@@ -36,7 +36,9 @@ struct GatherPlan {
   int64_t* warp_rec = nullptr;       // [n_items + 1] first record step of each item
   void* rec = nullptr;               // [n_steps][32] records
 };
-cudaError_t build_gather_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
+// bbox: {min x, min y, min z, max x, max y, max z} of the mesh coordinates.
+cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
+                              const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const uint8_t* d_slots, int window, int sm_count, cudaStream_t s, GatherPlan* out);
 void free_gather_plan(GatherPlan* p);
 

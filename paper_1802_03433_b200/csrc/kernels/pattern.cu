@@ -205,7 +205,8 @@ __global__ void chunk_visits(const int32_t* __restrict__ dconn, int k, int64_t r
 //  1. lists the incidences (e, i) of every row (element e has the row's DOF at
 //     local index i) and sorts them by (i, slot bytes, e);
 //  2. hashes that (i, slot bytes) sequence into a row signature and orders the
-//     rows by (window of consecutive rows, signature), so that warps of 32
+//     rows by (window of consecutive Morton ranks of the DOF points,
+//     signature), so that warps of 32
 //     rows step in lock-step through identical incidence sequences (on a
 //     structured mesh the 32 lanes then read the same slot pattern and their
 //     shared-memory row accumulators never collide on a bank);
@@ -267,12 +268,74 @@ __global__ void inc_sort_sign(const int64_t* __restrict__ inc_ptr, int64_t n_row
   }
 }
 
-__global__ void row_order_keys(const uint64_t* __restrict__ sig, int64_t n_rows, int window, uint64_t* __restrict__ keys,
-                               int32_t* __restrict__ rows) {
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {  // 21 bits -> every third bit
+  x &= 0x1fffffull;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+__device__ __forceinline__ uint64_t spread2(uint64_t x) {  // 31 bits -> every other bit
+  x &= 0x7fffffffull;
+  x = (x | x << 16) & 0x0000ffff0000ffffull;
+  x = (x | x << 8) & 0x00ff00ff00ff00ffull;
+  x = (x | x << 4) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | x << 2) & 0x3333333333333333ull;
+  x = (x | x << 1) & 0x5555555555555555ull;
+  return x;
+}
+
+// Morton code of every owned DOF's point (vertex, or edge midpoint for the
+// P2 local DOFs dim+1.. in fem.cpp's edge order), quantised over the mesh
+// bounding box. Several elements write the same row with the same value.
+__global__ void dof_morton(const double* __restrict__ coords, const int32_t* __restrict__ vconn,
+                           const int32_t* __restrict__ dconn, int64_t ne, int k, int dim, int64_t rb, int64_t n_rows,
+                           double lx, double ly, double lz, double sx, double sy, double sz,
+                           uint64_t* __restrict__ code) {
+  const int e3[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+  const int e2[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+  const int nv = dim + 1;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ne * k;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = static_cast<int64_t>(dconn[t]) - rb;
+    if (r < 0 || r >= n_rows) continue;
+    const int64_t e = t / k;
+    const int a = static_cast<int>(t - e * k);
+    double p[3] = {0.0, 0.0, 0.0};
+    if (a < nv) {
+      const int64_t v = vconn[e * nv + a];
+      for (int c = 0; c < dim; ++c) p[c] = coords[v * dim + c];
+    } else {
+      const int q = a - nv;
+      const int64_t v0 = vconn[e * nv + (dim == 3 ? e3[q][0] : e2[q][0])];
+      const int64_t v1 = vconn[e * nv + (dim == 3 ? e3[q][1] : e2[q][1])];
+      for (int c = 0; c < dim; ++c) p[c] = 0.5 * (coords[v0 * dim + c] + coords[v1 * dim + c]);
+    }
+    const double lo[3] = {lx, ly, lz}, sc[3] = {sx, sy, sz};
+    uint64_t qv[3] = {0, 0, 0};
+    const double qmax = dim == 3 ? 2097151.0 : 2147483647.0;
+    for (int c = 0; c < dim; ++c) qv[c] = static_cast<uint64_t>(fmin(fmax((p[c] - lo[c]) * sc[c], 0.0), qmax));
+    code[r] = dim == 3 ? (spread3(qv[0]) | spread3(qv[1]) << 1 | spread3(qv[2]) << 2)
+                       : (spread2(qv[0]) | spread2(qv[1]) << 1);
+  }
+}
+
+__global__ void iota_rows(int64_t n_rows, int32_t* __restrict__ rows) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    keys[r] = (static_cast<uint64_t>(r / window) << 40) | (sig[r] >> 24);
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x)
     rows[r] = static_cast<int32_t>(r);
+}
+
+// rows in Morton order -> key (window of `window` consecutive Morton ranks, signature)
+__global__ void row_order_keys(const uint64_t* __restrict__ sig, const int32_t* __restrict__ morton_order, int64_t n_rows,
+                               int window, uint64_t* __restrict__ keys, int32_t* __restrict__ rows) {
+  for (int64_t pos = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; pos < n_rows;
+       pos += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t r = morton_order[pos];
+    keys[pos] = (static_cast<uint64_t>(pos / window) << 40) | (sig[r] >> 24);
+    rows[pos] = r;
   }
 }
 
@@ -480,7 +543,8 @@ cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_
 }
 
 
-cudaError_t build_gather_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
+cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
+                              const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const uint8_t* d_slots, int window, int sm_count, cudaStream_t s, GatherPlan* out) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
@@ -532,15 +596,31 @@ cudaError_t build_gather_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t
   if (nk > 0) inc_fill<<<grid_for(nk, cap), kThreads, 0, s>>>(d_dconn, nk, rb, n_rows, cursor, inc);
   if ((err = cudaMalloc(&sig, nr1 * sizeof(uint64_t))) != cudaSuccess) return done(err);
   if (n_rows > 0) inc_sort_sign<<<grid_for(n_rows, cap), kThreads, 0, s>>>(inc_ptr, n_rows, k, d_slots, inc, sig);
-  // rows ordered by (window, signature); stable, so ties keep ascending rows
+  // rows in Morton order of their DOF points (3D-compact windows keep the
+  // element data of a window hot in L2), then by (window, signature);
+  // radix sorts are stable, so ties keep the previous order
   if ((err = cudaMalloc(&keys, nr1 * sizeof(uint64_t))) != cudaSuccess) return done(err);
   if ((err = cudaMalloc(&keys2, nr1 * sizeof(uint64_t))) != cudaSuccess) return done(err);
   if ((err = cudaMalloc(&rows, nr1 * sizeof(int32_t))) != cudaSuccess) return done(err);
   if ((err = cudaMalloc(&order, nr1 * sizeof(int32_t))) != cudaSuccess) return done(err);
-  if (n_rows > 0) row_order_keys<<<grid_for(n_rows, cap), kThreads, 0, s>>>(sig, n_rows, window, keys, rows);
+  if (n_rows > 0) {
+    double sc[3] = {0.0, 0.0, 0.0};
+    const double qmax = dim == 3 ? 2097151.0 : 2147483647.0;
+    for (int c = 0; c < dim; ++c) {
+      const double ext = bbox[3 + c] - bbox[c];
+      sc[c] = ext > 0 ? qmax / ext : 0.0;
+    }
+    cudaMemsetAsync(keys, 0, nr1 * sizeof(uint64_t), s);
+    dof_morton<<<grid_for(nk, cap), kThreads, 0, s>>>(d_coords, d_vconn, d_dconn, ne, k, dim, rb, n_rows, bbox[0],
+                                                     bbox[1], bbox[2], sc[0], sc[1], sc[2], keys);
+    iota_rows<<<grid_for(n_rows, cap), kThreads, 0, s>>>(n_rows, rows);
+  }
   tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, order, n_rows, 0, 64, s);
   if ((err = need_temp(tb)) != cudaSuccess) return done(err);
+  if ((err = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, rows, order, n_rows, 0, 64, s)) != cudaSuccess)
+    return done(err);
+  if (n_rows > 0) row_order_keys<<<grid_for(n_rows, cap), kThreads, 0, s>>>(sig, order, n_rows, window, keys, rows);
   if ((err = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, rows, order, n_rows, 0, 64, s)) != cudaSuccess)
     return done(err);
   const int64_t n_items = (n_rows + 31) / 32;
