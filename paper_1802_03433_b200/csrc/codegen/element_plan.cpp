@@ -368,10 +368,20 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
   {
     // ff_row<i>: v[j] = K_ij with the same expression (term order, literals)
     // as the element body, so both scatters compute bit-identical entries
+    // coefficients live in a __constant__ table so the fp64 FMAs read them as
+    // constant-bank operands instead of materialising 64-bit immediates
     std::ostringstream rc;
+    std::map<double, int> coef;
+    std::vector<double> coefs;
+    auto cref = [&](double c) {
+      auto [it, fresh] = coef.emplace(c, static_cast<int>(coefs.size()));
+      if (fresh) coefs.push_back(c);
+      return "ff_kc[" + std::to_string(it->second) + "]";
+    };
+    std::ostringstream body;
     for (int i = 0; i < f.n_local; ++i) {
-      rc << "template <> __device__ __forceinline__ void ff_row<" << i
-         << ">(const double* __restrict__ g, double* __restrict__ v) {\n";
+      body << "template <> __device__ __forceinline__ void ff_row<" << i
+           << ">(const double* __restrict__ g, double* __restrict__ v) {\n";
       for (int j = 0; j < f.n_local; ++j) {
         const auto& sig = row_sig[i * f.n_local + j];
         std::string v = sig.empty() ? "0.0" : "";
@@ -379,15 +389,19 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
           const double c = sig[q].second;
           const std::string t = "g[" + std::to_string(kq.at(sig[q].first)) + "]";
           if (q == 0)
-            v = c == 1.0 ? t : c == -1.0 ? "-" + t : double_literal(c) + " * " + t;
+            v = c == 1.0 ? t : c == -1.0 ? "-" + t : cref(c) + " * " + t;
           else
-            v += c == 1.0 ? " + " + t : c == -1.0 ? " - " + t : " + " + double_literal(c) + " * " + t;
+            v += c == 1.0 ? " + " + t : c == -1.0 ? " - " + t : " + " + cref(c) + " * " + t;
           plan.row_flops += 2;
         }
-        rc << "  v[" << j << "] = " << v << ";\n";
+        body << "  v[" << j << "] = " << v << ";\n";
       }
-      rc << "}\n";
+      body << "}\n";
     }
+    rc << "__constant__ double ff_kc[" << std::max<std::size_t>(coefs.size(), 1) << "] = {";
+    for (std::size_t q = 0; q < coefs.size(); ++q) rc << (q ? ", " : "") << double_literal(coefs[q]);
+    if (coefs.empty()) rc << "0.0";
+    rc << "};\n" << body.str();
     plan.row_code = rc.str();
   }
   // rows already grouped; emit in entry order of the group's first member
