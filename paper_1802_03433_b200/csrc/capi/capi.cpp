@@ -231,8 +231,8 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
     bbox[3 + c] = hi;
   }
   const cudaError_t e = ffb::kernels::build_gather_plan(m->coords, m->vconn, m->dim, bbox, m->dconn, m->ne, m->k, p->rb,
-                                                        p->re - p->rb, static_cast<const uint8_t*>(p->slots), 4096,
-                                                        ctx->sm_count, ctx->stream, &p->gather);
+                                                        p->re - p->rb, p->row_ptr, static_cast<const uint8_t*>(p->slots),
+                                                        4096, ctx->sm_count, ctx->stream, &p->gather);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
@@ -250,7 +250,7 @@ int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w)
   if (flags & (FF_SCATTER_GATHER | FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) mode = FF_SCATTER_GATHER_MODE;
   if (flags & (FF_ZERO_ONLY | FF_SKIP_ZERO)) mode = FF_SCATTER_ATOMIC_MODE;
   if (mode == FF_SCATTER_GATHER_MODE &&
-      !(f->kernel_grows[w] && p->max_row_len <= 256 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax))
+      !(f->kernel_grows[w] && p->max_row_len <= 255 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax))
     mode = FF_SCATTER_ATOMIC_MODE;
   if (mode == FF_SCATTER_ROWTILE && !f->kernel_tile[w]) mode = FF_SCATTER_ATOMIC_MODE;
   return mode;
@@ -285,27 +285,35 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     }
   }
   if (flags & FF_GATHER_INVARIANTS_ONLY) return;
-  if (p->gather.n_items == 0) return;
-  const int pitch = gather_pitch(p->max_row_len);
-  const int smem = gather_smem(pitch);
-  int per_sm = 0;
-  ffb::cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                      &per_sm, reinterpret_cast<const void*>(f->kernel_grows[w]), kGatherWarps * 32, smem),
-                  "row-gather occupancy");
-  const int64_t want = (p->gather.n_items + kGatherWarps - 1) / kGatherWarps;
-  const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(per_sm, 1)) * ctx->sm_count)));
-  const double* ginv = p->ginv;
-  const int64_t* row_ptr = p->row_ptr;
-  const int32_t* wrows = p->gather.warp_rows;
-  const int32_t* wsteps = p->gather.warp_steps;
-  const int64_t* wrec = p->gather.warp_rec;
-  const void* rec = p->gather.rec;
-  long long n_items = p->gather.n_items;
-  int pitch_arg = pitch;
-  void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &wrows, &wsteps, &wrec, &rec, &n_items, &pitch_arg};
-  ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
-                                   dim3(kGatherWarps * 32), args, smem, s),
-                  "K2b (row gather) launch");
+  // K2b in two launches: short-pitch items, then long-pitch items
+  const ffb::kernels::GatherPlan& gp = p->gather;
+  const int64_t ranges[2][2] = {{0, gp.n_short}, {gp.n_short, gp.n_items}};
+  const int pitches[2] = {gp.pitch_short, gp.pitch_long};
+  for (int c = 0; c < 2; ++c) {
+    long long i0 = ranges[c][0], i1 = ranges[c][1];
+    if (i1 <= i0) continue;
+    int pitch = pitches[c];
+    const int smem = gather_smem(pitch);
+    require(smem <= kGatherSmemMax, "row gather: rows too long for the shared-memory accumulators");
+    int per_sm = 0;
+    ffb::cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                        &per_sm, reinterpret_cast<const void*>(f->kernel_grows[w]), kGatherWarps * 32, smem),
+                    "row-gather occupancy");
+    const int64_t want = (i1 - i0 + kGatherWarps - 1) / kGatherWarps;
+    const unsigned grid =
+        static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(per_sm, 1)) * ctx->sm_count)));
+    const double* ginv = p->ginv;
+    const int64_t* row_ptr = p->row_ptr;
+    const int32_t* order = gp.item_order;
+    const int32_t* wrows = gp.warp_rows;
+    const int32_t* wsteps = gp.warp_steps;
+    const int64_t* wrec = gp.warp_rec;
+    const void* rec = gp.rec;
+    void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &order, &i0, &i1, &wrows, &wsteps, &wrec, &rec, &pitch};
+    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
+                                     dim3(kGatherWarps * 32), args, smem, s),
+                    "K2b (row gather) launch");
+  }
 }
 
 void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,

@@ -74,6 +74,15 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   const bool gather = plan.n_kinv > 0 && f.n_local <= 12 && plan.n_kinv + f.n_local <= 24;
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
+  {
+    std::string d =
+        "__device__ __forceinline__ void ff_gather_dispatch(int i, const FfRec& r, const double (&g)[FF_NKP],\n"
+        "                                                   double* __restrict__ arow) {\n  switch (i) {\n";
+    for (int i = 0; i < f.n_local; ++i)
+      d += "    case " + std::to_string(i) + ": ff_gather_apply<" + std::to_string(i) + ">(r, g, arow); break;\n";
+    d += "    default: break;\n  }\n}\n";
+    fill(text, "ROW_DISPATCH", gather ? d : std::string());
+  }
   if (text.find("{{") != std::string::npos) throw CodegenError("unresolved placeholder");
   if (plan_out) *plan_out = std::move(plan);
   return text;

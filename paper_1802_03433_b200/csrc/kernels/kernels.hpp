@@ -35,11 +35,15 @@ struct GatherPlan {
   int32_t* warp_steps = nullptr;     // [n_items][k]
   int64_t* warp_rec = nullptr;       // [n_items + 1] first record step of each item
   void* rec = nullptr;               // [n_steps][32] records
+  int32_t* item_order = nullptr;     // [n_items]: the n_short short-pitch items, then the long ones
+  int64_t n_short = 0;
+  int pitch_short = 1, pitch_long = 1;  // odd accumulator pitches (longest row of the class, | 1)
 };
 // bbox: {min x, min y, min z, max x, max y, max z} of the mesh coordinates.
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
-                              const uint8_t* d_slots, int window, int sm_count, cudaStream_t s, GatherPlan* out);
+                              const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
+                              cudaStream_t s, GatherPlan* out);
 void free_gather_plan(GatherPlan* p);
 
 // Order-independent 64-bit content hash of n int32 values (sum of mixed

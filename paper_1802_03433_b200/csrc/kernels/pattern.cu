@@ -15,7 +15,9 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "kernels.hpp"
 
@@ -341,17 +343,20 @@ __global__ void row_order_keys(const uint64_t* __restrict__ sig, const int32_t* 
 
 __global__ void item_steps(const int32_t* __restrict__ order, int64_t n_rows, int64_t n_items, int k,
                            const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
-                           int32_t* __restrict__ warp_rows, int32_t* __restrict__ warp_steps,
-                           int64_t* __restrict__ item_total) {
+                           const int64_t* __restrict__ row_ptr, int32_t* __restrict__ warp_rows,
+                           int32_t* __restrict__ warp_steps, int64_t* __restrict__ item_total,
+                           int32_t* __restrict__ item_len) {
   for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < n_items;
        w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int mx[32];
+    int ml = 0;
     for (int i = 0; i < k; ++i) mx[i] = 0;
     for (int l = 0; l < 32; ++l) {
       const int64_t pos = w * 32 + l;
       const int32_t row = pos < n_rows ? order[pos] : -1;
       warp_rows[pos] = row;
       if (row < 0) continue;
+      ml = max(ml, static_cast<int>(row_ptr[row + 1] - row_ptr[row]));
       int64_t p = inc_ptr[row];
       const int64_t e = inc_ptr[row + 1];
       for (int i = 0; i < k; ++i) {
@@ -369,6 +374,7 @@ __global__ void item_steps(const int32_t* __restrict__ order, int64_t n_rows, in
       tot += mx[i];
     }
     item_total[w] = tot;
+    item_len[w] = ml;
   }
 }
 
@@ -545,7 +551,8 @@ cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_
 
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
-                              const uint8_t* d_slots, int window, int sm_count, cudaStream_t s, GatherPlan* out) {
+                              const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
+                              cudaStream_t s, GatherPlan* out) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   const int cap = sm_count * 16;
@@ -631,10 +638,34 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     return done(err);
   if ((err = cudaMalloc(&out->warp_rec, (n_items + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
   if ((err = cudaMalloc(&item_total, (n_items + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&out->item_order, (n_items > 0 ? n_items : 1) * sizeof(int32_t))) != cudaSuccess)
+    return done(err);
+  int32_t* item_len = cnt;  // reuse: n_items <= n_rows + 1
   cudaMemsetAsync(item_total, 0, (n_items + 1) * sizeof(int64_t), s);
   if (n_items > 0)
-    item_steps<<<grid_for(n_items, cap), kThreads, 0, s>>>(order, n_rows, n_items, k, inc_ptr, inc, out->warp_rows,
-                                                           out->warp_steps, item_total);
+    item_steps<<<grid_for(n_items, cap), kThreads, 0, s>>>(order, n_rows, n_items, k, inc_ptr, inc, d_row_ptr,
+                                                           out->warp_rows, out->warp_steps, item_total, item_len);
+  // item order: items whose rows fit the short accumulator pitch first, then
+  // the long ones (two launches, each at the occupancy its pitch allows)
+  {
+    std::vector<int32_t> len(n_items > 0 ? n_items : 1);
+    if (n_items > 0) cudaMemcpyAsync(len.data(), item_len, n_items * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+    int mx = 1;
+    for (int64_t w = 0; w < n_items; ++w) mx = std::max(mx, len[w] | 1);
+    out->pitch_long = mx;
+    out->pitch_short = std::min(mx, 33);
+    std::vector<int32_t> ord;
+    ord.reserve(n_items);
+    for (int64_t w = 0; w < n_items; ++w)
+      if ((len[w] | 1) <= out->pitch_short) ord.push_back(static_cast<int32_t>(w));
+    out->n_short = static_cast<int64_t>(ord.size());
+    for (int64_t w = 0; w < n_items; ++w)
+      if ((len[w] | 1) > out->pitch_short) ord.push_back(static_cast<int32_t>(w));
+    if (n_items > 0)
+      cudaMemcpyAsync(out->item_order, ord.data(), n_items * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+  }
   tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, item_total, out->warp_rec, n_items + 1, s);
   if ((err = need_temp(tb)) != cudaSuccess) return done(err);
@@ -669,6 +700,7 @@ cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_ou
 }
 
 void free_gather_plan(GatherPlan* p) {
+  cudaFree(p->item_order);
   cudaFree(p->warp_rows);
   cudaFree(p->warp_steps);
   cudaFree(p->warp_rec);
