@@ -43,10 +43,21 @@ std::string disk_path(const std::string& key) {
   return os.str();
 }
 
+// ptxas -v lines of the element kernel (ff_assemble_atomic; else the first
+// entry function of the module)
 void parse_resources(CompiledModule& m) {
+  const std::regex entry("entry function '([A-Za-z_0-9]+)'");
+  std::string block = m.log;
+  for (auto it = std::sregex_iterator(m.log.begin(), m.log.end(), entry); it != std::sregex_iterator(); ++it) {
+    if ((*it)[1] != "ff_assemble_atomic") continue;
+    const std::size_t at = static_cast<std::size_t>(it->position());
+    const std::size_t next = m.log.find("entry function", at + 1);
+    block = m.log.substr(at, next == std::string::npos ? std::string::npos : next - at);
+    break;
+  }
   std::smatch r;
-  if (std::regex_search(m.log, r, std::regex("Used ([0-9]+) registers"))) m.registers = std::stoi(r[1]);
-  if (std::regex_search(m.log, r, std::regex("([0-9]+) bytes smem"))) m.shared_bytes = std::stoi(r[1]);
+  if (std::regex_search(block, r, std::regex("Used ([0-9]+) registers"))) m.registers = std::stoi(r[1]);
+  if (std::regex_search(block, r, std::regex("([0-9]+) bytes smem"))) m.shared_bytes = std::stoi(r[1]);
 }
 
 }  // namespace
