@@ -142,10 +142,22 @@ int ff_pattern_prepare(ff_pattern* p, const ff_mesh* mesh);
 /* Gather plan statistics (built by the first gather assembly or here):
  * warp items, lock-step steps (records / 32) and incidences (row, element). */
 typedef struct ff_gather_info {
-  int64_t n_items, n_steps, n_incidences;
+  int64_t n_items, n_steps, n_incidences;  /* generic items (rows outside the classes) */
   int record_bytes;
   double build_ms;
+  int n_classes;                            /* row classes with a specialised kernel */
+  int64_t n_class_rows, n_class_items;
 } ff_gather_info;
+/* Row classes of the gather plan: rows with identical incidence sequences
+ * get an NVRTC kernel specialised to the class (slots as compile-time
+ * register indices). Classes need >= min_rows rows (default 128); 0 turns
+ * the specialisation off (every row takes the generic gather). */
+int ff_ctx_set_gather_classes(ff_ctx* ctx, int64_t min_rows);
+/* The class-specialised source for caller-given classes (tests / inspection):
+ * n classes with len[c] entries and steps[c] incidences; local and slots are
+ * the concatenated per-step local indices and [steps][n_local] slot bytes. */
+int ff_class_source(const ff_form* form, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
+                    const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
 int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* mesh, ff_gather_info* out);
 /* Which scatter the next assembly of (form, pattern) runs: FF_SCATTER_*_MODE. */
 int ff_scatter_selected(const ff_form* form, const ff_pattern* p, unsigned flags, int* mode);

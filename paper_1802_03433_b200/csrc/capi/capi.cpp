@@ -200,15 +200,54 @@ void ensure_tile_plan(ff_pattern* p, const ff_mesh* m, const codegen::RowTilePar
   p->tile_chunk = tp.chunk;
 }
 
+void free_class_module(ff_pattern* p) {
+  if (p->class_lib) cudaLibraryUnload(p->class_lib);
+  p->class_lib = nullptr;
+  p->class_kernel[0] = p->class_kernel[1] = nullptr;
+  p->class_key.clear();
+}
+
 void free_gather(ff_pattern* p) {
   ffb::kernels::free_gather_plan(&p->gather);
   p->gather_generation = ~0ull;
   p->gather_mesh = nullptr;
+  free_class_module(p);
+}
+
+// NVRTC-compiles the class-specialised gather kernels of (form, plan).
+void ensure_class_module(ff_form* f, ff_pattern* p) {
+  if (p->gather.classes.empty()) return;
+  const std::string key = f->source[1] + "#" + std::to_string(p->gather_generation) + "#" +
+                          std::to_string(reinterpret_cast<std::uintptr_t>(p->gather.crec));
+  if (p->class_key == key && p->class_lib) return;
+  free_class_module(p);
+  std::vector<codegen::RowClass> rc;
+  for (const auto& c : p->gather.classes) {
+    codegen::RowClass r;
+    r.len = c.len;
+    r.steps = c.steps;
+    r.local = c.local;
+    r.slots = c.slots;
+    rc.push_back(std::move(r));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::string src = codegen::emit_class_source(f->plan, f->n_local, rc);
+  const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
+  bind(p->ctx);
+  ffb::cuda_check(cudaLibraryLoadData(&p->class_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+                  "cudaLibraryLoadData (classes)");
+  ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[0], p->class_lib, "ff_gather_classes_s"), "class kernel");
+  ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[1], p->class_lib, "ff_gather_classes_l"), "class kernel");
+  p->class_compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  p->class_key = key;
 }
 
 void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
   ensure_plan(p, m);
-  if (p->gather_mesh == m && p->gather_generation == m->generation && p->gather.rec) return;
+  const int64_t cmin = p->ctx->class_min_rows;
+  if (p->gather_mesh == m && p->gather_generation == m->generation && p->gather_class_min == cmin &&
+      (p->gather.rec || p->gather.crec))
+    return;
   require(p->slot_bytes == 1, "row gather needs rows of <= 256 entries");
   free_gather(p);
   ff_ctx* ctx = p->ctx;
@@ -232,7 +271,10 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
   }
   const cudaError_t e = ffb::kernels::build_gather_plan(m->coords, m->vconn, m->dim, bbox, m->dconn, m->ne, m->k, p->rb,
                                                         p->re - p->rb, p->row_ptr, static_cast<const uint8_t*>(p->slots),
-                                                        4096, ctx->sm_count, ctx->stream, &p->gather);
+                                                        4096, ctx->sm_count, ctx->stream, &p->gather,
+                                                        cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
+                                                                 : (1 << 30),
+                                                        cmin > 0 ? 64 : 0);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
@@ -240,6 +282,7 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
   p->gather_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   p->gather_mesh = m;
   p->gather_generation = m->generation;
+  p->gather_class_min = cmin;
 }
 
 // The scatter a (form, pattern, flags) assembly runs (FF_SCATTER_*_MODE).
@@ -285,8 +328,34 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     }
   }
   if (flags & FF_GATHER_INVARIANTS_ONLY) return;
-  // K2b in two launches: short-pitch items, then long-pitch items
   const ffb::kernels::GatherPlan& gp = p->gather;
+  // K2b for the row classes: specialised kernels (rows in registers)
+  if (gp.n_citems > 0) {
+    ensure_class_module(f, p);
+    const int64_t cr[2][2] = {{0, gp.n_citems_short}, {gp.n_citems_short, gp.n_citems}};
+    for (int c = 0; c < 2; ++c) {
+      long long i0 = cr[c][0], i1 = cr[c][1];
+      if (i1 <= i0) continue;
+      int per_sm = 0;
+      ffb::cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                          &per_sm, reinterpret_cast<const void*>(p->class_kernel[c]), 128, 0),
+                      "class gather occupancy");
+      const int64_t want = (i1 - i0 + 3) / 4;
+      const unsigned grid = static_cast<unsigned>(
+          std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(per_sm, 1)) * ctx->sm_count)));
+      const double* ginv = p->ginv;
+      const int64_t* row_ptr = p->row_ptr;
+      const int32_t* icls = gp.citem_class;
+      const int32_t* irows = gp.citem_rows;
+      const int64_t* irec = gp.citem_rec;
+      const int32_t* crec = gp.crec;
+      void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
+      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(128), args,
+                                       0, s),
+                      "K2b (class row gather) launch");
+    }
+  }
+  // K2b for the remaining rows in two launches: short-pitch items, then long-pitch items
   const int64_t ranges[2][2] = {{0, gp.n_short}, {gp.n_short, gp.n_items}};
   const int pitches[2] = {gp.pitch_short, gp.pitch_long};
   for (int c = 0; c < 2; ++c) {
@@ -442,6 +511,39 @@ int ff_ctx_set_scatter(ff_ctx* ctx, int mode) {
     require(mode == FF_SCATTER_ROWTILE || mode == FF_SCATTER_ATOMIC_MODE || mode == FF_SCATTER_GATHER_MODE,
             "unknown scatter mode");
     ctx->scatter = mode;
+  });
+}
+
+int ff_ctx_set_gather_classes(ff_ctx* ctx, int64_t min_rows) {
+  return guarded([&] {
+    require(ctx && min_rows >= 0, "invalid argument");
+    ctx->class_min_rows = min_rows;
+  });
+}
+
+int ff_class_source(const ff_form* f, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
+                    const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {
+  return guarded([&] {
+    require(f && n >= 0 && (n == 0 || (len && steps && local && slots)), "null argument");
+    require(f->plan.n_kinv > 0, "form has no reference-tensor plan (no row gather)");
+    std::vector<codegen::RowClass> rc(n);
+    int64_t at = 0;
+    for (int c = 0; c < n; ++c) {
+      rc[c].len = len[c];
+      rc[c].steps = steps[c];
+      for (int q = 0; q < steps[c]; ++q) {
+        rc[c].local.push_back(local[at + q]);
+        for (int j = 0; j < f->n_local; ++j) rc[c].slots.push_back(slots[(at + q) * f->n_local + j]);
+      }
+      at += steps[c];
+    }
+    const std::string src = codegen::emit_class_source(f->plan, f->n_local, rc);
+    if (out_len) *out_len = src.size();
+    if (buf && cap) {
+      const std::size_t k = std::min(cap - 1, src.size());
+      std::memcpy(buf, src.data(), k);
+      buf[k] = '\0';
+    }
   });
 }
 
@@ -709,6 +811,9 @@ int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* m, ff_gather_info* out)
     out->n_incidences = p->gather.n_incidences;
     out->record_bytes = p->gather.rec_bytes;
     out->build_ms = p->gather_ms;
+    out->n_classes = static_cast<int>(p->gather.classes.size());
+    out->n_class_rows = p->gather.n_class_rows;
+    out->n_class_items = p->gather.n_citems;
   });
 }
 

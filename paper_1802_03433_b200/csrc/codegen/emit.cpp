@@ -1,6 +1,8 @@
 // Source emission: the hand-written assembly template with the generated
 // element body spliced in (the reference's template route, kernel.cpp:
 // 290-449, made executable: the output is what NVRTC compiles).
+#include <algorithm>
+#include <sstream>
 #include <string>
 
 #include "femforge/codegen.hpp"
@@ -86,6 +88,100 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   if (text.find("{{") != std::string::npos) throw CodegenError("unresolved placeholder");
   if (plan_out) *plan_out = std::move(plan);
   return text;
+}
+
+
+std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes) {
+  if (plan.n_kinv <= 0) throw CodegenError("row classes need a reference-tensor plan");
+  std::ostringstream os;
+  const int nkp = plan.n_kinv + (plan.n_kinv & 1);
+  const int erec = (plan.n_kinv + n_local + 1) & ~1;
+  os << "// femforge-b200 class-specialised row gather (generated per (form, gather plan));\n"
+        "// every class row stays in registers, indexed by compile-time slots.\n"
+        "typedef long long ff_i64;\ntypedef int ff_i32;\n"
+     << "#define FF_NLOC " << n_local << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
+     << "\n#define FF_EREC " << erec << "\n"
+     << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
+     << plan.row_code
+     << R"(
+__device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, double (&g)[FF_NKP],
+                                         double& b) {
+  if (e >= 0) {
+    const double* base = einv + (ff_i64)e * FF_EREC;
+    const double2* g2 = (const double2*)base;
+#pragma unroll
+    for (int q = 0; q < FF_NKP / 2; ++q) {
+      const double2 t = __ldg(g2 + q);
+      g[2 * q] = t.x;
+      g[2 * q + 1] = t.y;
+    }
+    b = __ldg(base + FF_NKINV + i);
+  } else {
+#pragma unroll
+    for (int q = 0; q < FF_NKP; ++q) g[q] = 0.0;
+    b = 0.0;
+  }
+}
+#define FF_SP 33  // staging pitch (odd: conflict-free lane-row stores)
+)";
+  auto class_fn = [&](int c) {
+    const RowClass& k = classes[c];
+    const int depth = k.len > 33 ? 4 : 8;
+    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
+       << "__device__ __forceinline__ void ff_cls_" << c
+       << "(const ff_i32* __restrict__ rec, const double* __restrict__ einv, double* __restrict__ st, int lane,\n"
+          "    ff_i64 rbeg, int row, double* __restrict__ values, double* __restrict__ rhs) {\n";
+    for (int p = 0; p < k.len; ++p) os << "  double a" << p << " = 0.0;\n";
+    os << "  double bs = 0.0;\n";
+    for (int s0 = 0; s0 < k.steps; s0 += depth) {
+      const int s1 = std::min(k.steps, s0 + depth);
+      os << "  {\n";
+      for (int s = s0; s < s1; ++s) os << "    const int e" << s << " = __ldcs(rec + " << s * 32 << ");\n";
+      for (int s = s0; s < s1; ++s)
+        os << "    double g" << s << "[FF_NKP], b" << s << "; ff_cload(e" << s << ", " << k.local[s] << ", einv, g" << s
+           << ", b" << s << ");\n";
+      for (int s = s0; s < s1; ++s) {
+        os << "    { double v[FF_NLOC]; ff_row<" << k.local[s] << ">(g" << s << ", v);";
+        for (int j = 0; j < n_local; ++j) os << " a" << int(k.slots[s * n_local + j]) << " += v[" << j << "];";
+        os << " bs += b" << s << "; }\n";
+      }
+      os << "  }\n";
+    }
+    for (int q0 = 0; q0 < k.len; q0 += 32) {
+      const int cnt = std::min(32, k.len - q0);
+      for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
+      os << "  __syncwarp();\n"
+            "  for (int m = 0; m < 32; ++m) {\n"
+            "    const ff_i64 rb = __shfl_sync(0xffffffffu, rbeg, m);\n"
+            "    const int rm = __shfl_sync(0xffffffffu, row, m);\n"
+         << "    if (rm >= 0 && lane < " << cnt << ") __stcs(values + rb + " << q0 << " + lane, st[m * FF_SP + lane]);\n"
+         << "  }\n  __syncwarp();\n";
+    }
+    os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
+  };
+  for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
+  auto kernel = [&](const char* name, bool longrows) {
+    os << "extern \"C\" __global__ void __launch_bounds__(128)\n" << name
+       << "(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr, double* __restrict__ values,\n"
+          "    double* __restrict__ rhs, const ff_i32* __restrict__ citem_class, const ff_i32* __restrict__ citem_rows,\n"
+          "    const ff_i64* __restrict__ citem_rec, const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
+          "  __shared__ double stage[4][32 * FF_SP];\n"
+          "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
+          "  double* st = stage[wid];\n"
+          "  for (ff_i64 w = i0 + (ff_i64)blockIdx.x * 4 + wid; w < i1; w += (ff_i64)gridDim.x * 4) {\n"
+          "    const int c = __ldg(citem_class + w);\n"
+          "    const int row = __ldg(citem_rows + w * 32 + lane);\n"
+          "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
+          "    const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
+          "    switch (c) {\n";
+    for (int c = 0; c < static_cast<int>(classes.size()); ++c)
+      if ((classes[c].len > 33) == longrows)
+        os << "      case " << c << ": ff_cls_" << c << "(rec, einv, st, lane, rbeg, row, values, rhs); break;\n";
+    os << "      default: break;\n    }\n  }\n}\n";
+  };
+  kernel("ff_gather_classes_s", false);
+  kernel("ff_gather_classes_l", true);
+  return os.str();
 }
 
 }  // namespace femforge::codegen

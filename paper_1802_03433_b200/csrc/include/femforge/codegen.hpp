@@ -148,6 +148,21 @@ RowTileParams rowtile_params(int n_local, int block_size);
 std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg);
 std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg, ElementPlan* plan_out);
 
+// Row classes of a gather plan (rows with identical incidence sequences):
+// the specialised gather kernels keep a class's row in registers, indexed by
+// the compile-time slots.
+struct RowClass {
+  int len = 0;                       // row length (CSR entries)
+  int steps = 0;                     // incidences
+  std::vector<int> local;            // [steps] local index i of each incidence
+  std::vector<std::uint8_t> slots;   // [steps][n_local] slot of column dof[j] in the row
+};
+
+// NVRTC translation unit with ff_gather_classes_s (classes of rows <= 33
+// entries) and ff_gather_classes_l (longer rows). Needs a gather-capable
+// plan (plan.n_kinv > 0). Byte-deterministic.
+std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes);
+
 // Shortest round-trip double literal valid in C/CUDA source.
 std::string double_literal(double v);
 

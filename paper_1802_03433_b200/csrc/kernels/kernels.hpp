@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include <cstdint>
 
 namespace ffb::kernels {
@@ -38,12 +40,28 @@ struct GatherPlan {
   int32_t* item_order = nullptr;     // [n_items]: the n_short short-pitch items, then the long ones
   int64_t n_short = 0;
   int pitch_short = 1, pitch_long = 1;  // odd accumulator pitches (longest row of the class, | 1)
+  // Row classes: rows whose sorted incidence sequence (local index + slot
+  // bytes of every incidence) and length are identical. Frequent classes
+  // get a specialised NVRTC kernel with the slots as compile-time register
+  // indices; the rows above (the generic items) are the others.
+  struct Class {
+    int len = 0, steps = 0;
+    std::vector<int> local;         // [steps] local index i of each step
+    std::vector<uint8_t> slots;     // [steps][k]
+    int64_t rows = 0;
+  };
+  std::vector<Class> classes;
+  int64_t n_citems = 0, n_citems_short = 0, n_crec = 0, n_class_rows = 0;
+  int32_t* citem_class = nullptr;   // [n_citems]
+  int32_t* citem_rows = nullptr;    // [n_citems][32] local row or -1
+  int64_t* citem_rec = nullptr;     // [n_citems] first record of the item ([steps][32] element ids)
+  int32_t* crec = nullptr;          // [n_crec] element ids (-1: idle lane)
 };
 // bbox: {min x, min y, min z, max x, max y, max z} of the mesh coordinates.
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
-                              cudaStream_t s, GatherPlan* out);
+                              cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64);
 void free_gather_plan(GatherPlan* p);
 
 // Order-independent 64-bit content hash of n int32 values (sum of mixed

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <unordered_map>
 #include <vector>
 
 #include "kernels.hpp"
@@ -378,6 +379,67 @@ __global__ void item_steps(const int32_t* __restrict__ order, int64_t n_rows, in
   }
 }
 
+// class templates of the representative rows: [c][2 + kMaxSteps*(1+k)] ints:
+// len, steps, then per step the local index and the k slot bytes
+constexpr int kMaxClassSteps = 64;
+__global__ void class_templates(const int32_t* __restrict__ reps, int n_cls, const int64_t* __restrict__ inc_ptr,
+                                const int32_t* __restrict__ inc, const uint8_t* __restrict__ slots, int k,
+                                const int64_t* __restrict__ row_ptr, int32_t* __restrict__ out) {
+  const int stride = 2 + kMaxClassSteps * (1 + k);
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_cls; c += gridDim.x * blockDim.x) {
+    const int32_t r = reps[c];
+    int32_t* o = out + static_cast<int64_t>(c) * stride;
+    const int64_t b = inc_ptr[r];
+    const int n = static_cast<int>(inc_ptr[r + 1] - b);
+    o[0] = static_cast<int32_t>(row_ptr[r + 1] - row_ptr[r]);
+    o[1] = n;
+    for (int q = 0; q < n && q < kMaxClassSteps; ++q) {
+      const int32_t t = inc[b + q];
+      o[2 + q * (1 + k)] = t % k;
+      for (int j = 0; j < k; ++j) o[3 + q * (1 + k) + j] = slots[static_cast<int64_t>(t) * k + j];
+    }
+  }
+}
+
+// demotes rows whose incidences differ from their class template (hash collisions)
+__global__ void class_verify(int32_t* __restrict__ cls, int64_t n_rows, const int32_t* __restrict__ tmpl, int k,
+                             const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
+                             const uint8_t* __restrict__ slots, const int64_t* __restrict__ row_ptr) {
+  const int stride = 2 + kMaxClassSteps * (1 + k);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = cls[r];
+    if (c < 0) continue;
+    const int32_t* o = tmpl + static_cast<int64_t>(c) * stride;
+    const int64_t b = inc_ptr[r];
+    const int n = static_cast<int>(inc_ptr[r + 1] - b);
+    bool ok = o[0] == static_cast<int32_t>(row_ptr[r + 1] - row_ptr[r]) && o[1] == n && n <= kMaxClassSteps;
+    for (int q = 0; ok && q < n; ++q) {
+      const int32_t t = inc[b + q];
+      ok = o[2 + q * (1 + k)] == t % k;
+      for (int j = 0; ok && j < k; ++j) ok = o[3 + q * (1 + k) + j] == slots[static_cast<int64_t>(t) * k + j];
+    }
+    if (!ok) cls[r] = -1;
+  }
+}
+
+// class item records: [steps][32] element ids of each item (incidence order)
+__global__ void fill_class_records(const int32_t* __restrict__ citem_class, const int32_t* __restrict__ citem_rows,
+                                   const int64_t* __restrict__ citem_rec, int64_t n_citems,
+                                   const int32_t* __restrict__ cls_steps, const int64_t* __restrict__ inc_ptr,
+                                   const int32_t* __restrict__ inc, int k, int32_t* __restrict__ crec) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_citems * 32;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = t / 32;
+    const int lane = static_cast<int>(t % 32);
+    const int32_t row = citem_rows[t];
+    const int n = cls_steps[citem_class[w]];
+    const int64_t base = citem_rec[w] * 32 + lane;
+    const int64_t p = row >= 0 ? inc_ptr[row] : 0;
+    for (int q = 0; q < n; ++q) crec[base + q * 32] = row >= 0 ? inc[p + q] / k : -1;
+  }
+}
+
 template <int K>
 __global__ void fill_records(const int32_t* __restrict__ warp_rows, const int32_t* __restrict__ warp_steps,
                              const int64_t* __restrict__ warp_rec, int64_t n_items, const int64_t* __restrict__ inc_ptr,
@@ -552,7 +614,7 @@ cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
-                              cudaStream_t s, GatherPlan* out) {
+                              cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   const int cap = sm_count * 16;
@@ -627,10 +689,165 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
   if ((err = need_temp(tb)) != cudaSuccess) return done(err);
   if ((err = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, rows, order, n_rows, 0, 64, s)) != cudaSuccess)
     return done(err);
+  // ---- row classes (signature counts on the host, verified on the device)
+  std::vector<int32_t> morton(n_rows), cls_h(n_rows, -1);
+  {
+    std::vector<uint64_t> sig_h(n_rows);
+    if (n_rows > 0) {
+      cudaMemcpyAsync(morton.data(), order, n_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(sig_h.data(), sig, n_rows * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    }
+    if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+    std::unordered_map<uint64_t, std::pair<int64_t, int32_t>> count;  // sig -> (rows, first row in Morton order)
+    count.reserve(1024);
+    for (int64_t pos = 0; pos < n_rows; ++pos) {
+      const int32_t r = morton[pos];
+      auto [it, fresh] = count.emplace(sig_h[r], std::make_pair(int64_t(0), r));
+      ++it->second.first;
+    }
+    std::vector<std::pair<int64_t, uint64_t>> big;
+    for (const auto& [h, v] : count)
+      if (v.first >= min_class_rows) big.push_back({v.first, h});
+    std::sort(big.begin(), big.end(), [&](const auto& a, const auto& b) {
+      return a.first != b.first ? a.first > b.first : count[a.second].second < count[b.second].second;
+    });
+    if (static_cast<int>(big.size()) > max_classes) big.resize(max_classes);
+    std::unordered_map<uint64_t, int> cid;
+    std::vector<int32_t> reps;
+    for (const auto& [n, h] : big) {
+      cid[h] = static_cast<int>(reps.size());
+      reps.push_back(count[h].second);
+    }
+    const int n_cls = static_cast<int>(reps.size());
+    out->classes.clear();
+    if (n_cls > 0) {
+      for (int64_t r = 0; r < n_rows; ++r) {
+        auto it = cid.find(sig_h[r]);
+        if (it != cid.end()) cls_h[r] = it->second;
+      }
+      const int stride = 2 + kMaxClassSteps * (1 + k);
+      int32_t *d_reps = nullptr, *d_tmpl = nullptr, *d_cls = nullptr;
+      auto cleanup = [&]() {
+        cudaFree(d_reps);
+        cudaFree(d_tmpl);
+        cudaFree(d_cls);
+      };
+      if ((err = cudaMalloc(&d_reps, n_cls * sizeof(int32_t))) != cudaSuccess) return cleanup(), done(err);
+      if ((err = cudaMalloc(&d_tmpl, static_cast<size_t>(n_cls) * stride * sizeof(int32_t))) != cudaSuccess)
+        return cleanup(), done(err);
+      if ((err = cudaMalloc(&d_cls, n_rows * sizeof(int32_t))) != cudaSuccess) return cleanup(), done(err);
+      cudaMemcpyAsync(d_reps, reps.data(), n_cls * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      cudaMemsetAsync(d_tmpl, 0, static_cast<size_t>(n_cls) * stride * sizeof(int32_t), s);
+      class_templates<<<1, 64, 0, s>>>(d_reps, n_cls, inc_ptr, inc, d_slots, k, d_row_ptr, d_tmpl);
+      cudaMemcpyAsync(d_cls, cls_h.data(), n_rows * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      class_verify<<<grid_for(n_rows, cap), kThreads, 0, s>>>(d_cls, n_rows, d_tmpl, k, inc_ptr, inc, d_slots,
+                                                             d_row_ptr);
+      std::vector<int32_t> tmpl(static_cast<size_t>(n_cls) * stride);
+      cudaMemcpyAsync(tmpl.data(), d_tmpl, tmpl.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(cls_h.data(), d_cls, n_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return cleanup(), done(err);
+      cleanup();
+      for (int c = 0; c < n_cls; ++c) {
+        const int32_t* o = tmpl.data() + static_cast<size_t>(c) * stride;
+        GatherPlan::Class cl;
+        cl.len = o[0];
+        cl.steps = o[1];
+        if (cl.steps > kMaxClassSteps) cl.steps = -1;  // never matches: rows stay generic
+        for (int q = 0; q < std::max(cl.steps, 0); ++q) {
+          cl.local.push_back(o[2 + q * (1 + k)]);
+          for (int j = 0; j < k; ++j) cl.slots.push_back(static_cast<uint8_t>(o[3 + q * (1 + k) + j]));
+        }
+        out->classes.push_back(std::move(cl));
+      }
+    }
+    // class items: each class's rows in Morton order, 32 per item; items
+    // interleaved by the Morton position of their first row
+    std::vector<std::vector<int32_t>> members(n_cls);
+    std::vector<std::vector<int64_t>> first_pos(n_cls);
+    for (int64_t pos = 0; pos < n_rows; ++pos) {
+      const int32_t r = morton[pos];
+      const int c = cls_h[r];
+      if (c < 0) continue;
+      if (members[c].size() % 32 == 0) first_pos[c].push_back(pos);
+      members[c].push_back(r);
+    }
+    struct Item {
+      int64_t key;
+      int c;
+      int64_t idx;
+    };
+    std::vector<Item> items;
+    for (int c = 0; c < n_cls; ++c) {
+      out->classes[c].rows = static_cast<int64_t>(members[c].size());
+      for (size_t q = 0; q < first_pos[c].size(); ++q) items.push_back({first_pos[c][q], c, static_cast<int64_t>(q)});
+    }
+    // short-row classes (<= 33 entries) first, then long-row ones: two
+    // specialised kernels with their own register budgets
+    auto longrows = [&](const Item& it) { return out->classes[it.c].len > 33 ? 1 : 0; };
+    std::sort(items.begin(), items.end(), [&](const Item& a, const Item& b) {
+      return longrows(a) != longrows(b) ? longrows(a) < longrows(b) : a.key < b.key;
+    });
+    out->n_citems_short = 0;
+    for (const Item& it : items) out->n_citems_short += longrows(it) ? 0 : 1;
+    const int64_t nci = static_cast<int64_t>(items.size());
+    std::vector<int32_t> ic(nci), ir(nci * 32, -1), cls_steps(std::max(n_cls, 1), 0);
+    std::vector<int64_t> irec(nci + 1, 0);
+    for (int c = 0; c < n_cls; ++c) cls_steps[c] = out->classes[c].steps;
+    int64_t nrec = 0, ncr = 0;
+    for (int64_t w = 0; w < nci; ++w) {
+      const Item& it = items[w];
+      ic[w] = it.c;
+      const auto& m = members[it.c];
+      for (int l = 0; l < 32; ++l) {
+        const size_t q = static_cast<size_t>(it.idx) * 32 + l;
+        if (q < m.size()) {
+          ir[w * 32 + l] = m[q];
+          ++ncr;
+        }
+      }
+      irec[w] = nrec;
+      nrec += cls_steps[it.c];
+    }
+    irec[nci] = nrec;
+    out->n_citems = nci;
+    out->n_crec = nrec * 32;
+    out->n_class_rows = ncr;
+    if (nci > 0) {
+      int32_t* d_steps = nullptr;
+      if ((err = cudaMalloc(&out->citem_class, nci * sizeof(int32_t))) != cudaSuccess) return done(err);
+      if ((err = cudaMalloc(&out->citem_rows, nci * 32 * sizeof(int32_t))) != cudaSuccess) return done(err);
+      if ((err = cudaMalloc(&out->citem_rec, (nci + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
+      if ((err = cudaMalloc(&out->crec, std::max<int64_t>(out->n_crec, 1) * sizeof(int32_t))) != cudaSuccess)
+        return done(err);
+      if ((err = cudaMalloc(&d_steps, cls_steps.size() * sizeof(int32_t))) != cudaSuccess) return done(err);
+      cudaMemcpyAsync(out->citem_class, ic.data(), nci * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(out->citem_rows, ir.data(), nci * 32 * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(out->citem_rec, irec.data(), (nci + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(d_steps, cls_steps.data(), cls_steps.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      fill_class_records<<<grid_for(nci * 32, cap), kThreads, 0, s>>>(out->citem_class, out->citem_rows,
+                                                                      out->citem_rec, nci, d_steps, inc_ptr, inc, k,
+                                                                      out->crec);
+      err = cudaStreamSynchronize(s);
+      cudaFree(d_steps);
+      if (err != cudaSuccess) return done(err);
+    }
+  }
+  // ---- generic rows: the rest, ordered by (Morton window, signature)
   if (n_rows > 0) row_order_keys<<<grid_for(n_rows, cap), kThreads, 0, s>>>(sig, order, n_rows, window, keys, rows);
   if ((err = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, rows, order, n_rows, 0, 64, s)) != cudaSuccess)
     return done(err);
-  const int64_t n_items = (n_rows + 31) / 32;
+  int64_t n_gen = n_rows;
+  if (out->n_class_rows > 0) {
+    std::vector<int32_t> ord(n_rows);
+    cudaMemcpyAsync(ord.data(), order, n_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+    n_gen = 0;
+    for (int64_t pos = 0; pos < n_rows; ++pos)
+      if (cls_h[ord[pos]] < 0) ord[n_gen++] = ord[pos];
+    if (n_gen > 0) cudaMemcpyAsync(order, ord.data(), n_gen * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
+  }
+  const int64_t n_items = (n_gen + 31) / 32;
   out->n_items = n_items;
   if ((err = cudaMalloc(&out->warp_rows, (n_items > 0 ? n_items : 1) * 32 * sizeof(int32_t))) != cudaSuccess)
     return done(err);
@@ -643,7 +860,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
   int32_t* item_len = cnt;  // reuse: n_items <= n_rows + 1
   cudaMemsetAsync(item_total, 0, (n_items + 1) * sizeof(int64_t), s);
   if (n_items > 0)
-    item_steps<<<grid_for(n_items, cap), kThreads, 0, s>>>(order, n_rows, n_items, k, inc_ptr, inc, d_row_ptr,
+    item_steps<<<grid_for(n_items, cap), kThreads, 0, s>>>(order, n_gen, n_items, k, inc_ptr, inc, d_row_ptr,
                                                            out->warp_rows, out->warp_steps, item_total, item_len);
   // item order: items whose rows fit the short accumulator pitch first, then
   // the long ones (two launches, each at the occupancy its pitch allows)
@@ -700,6 +917,10 @@ cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_ou
 }
 
 void free_gather_plan(GatherPlan* p) {
+  cudaFree(p->citem_class);
+  cudaFree(p->citem_rows);
+  cudaFree(p->citem_rec);
+  cudaFree(p->crec);
   cudaFree(p->item_order);
   cudaFree(p->warp_rows);
   cudaFree(p->warp_steps);

@@ -43,6 +43,7 @@ struct ff_ctx {
   unsigned long long* d_status = nullptr;  // [bad_elem, bad_row]
   unsigned long long* h_status = nullptr;  // pinned mirror
   int scatter = 2;                          // FF_SCATTER_*_MODE (default: row gather)
+  int64_t class_min_rows = 128;             // gather row classes (0: off)
 };
 
 struct ff_form {
@@ -101,9 +102,15 @@ struct ff_pattern {
   int tile_acc = 0, tile_rows = 0, tile_stage = 0, tile_chunk = 0;
   // row-gather plan for plan_mesh, and the per-element invariant buffers
   std::uint64_t gather_generation = ~0ull;
+  int64_t gather_class_min = -1;            // class_min_rows the plan was built with
   const ff_mesh* gather_mesh = nullptr;
   ffb::kernels::GatherPlan gather;
   double gather_ms = 0.0;
+  // class-specialised gather kernels for (form source, plan)
+  std::string class_key;
+  cudaLibrary_t class_lib = nullptr;
+  cudaKernel_t class_kernel[2] = {nullptr, nullptr};  // short rows, long rows
+  double class_compile_ms = 0.0;
   double* ginv = nullptr;   // [ne][nkp]
   double* bvec = nullptr;   // [ne][k]
   std::size_t ginv_cap = 0, bvec_cap = 0;

@@ -129,3 +129,40 @@ def test_cpp_host_suites():
         pytest.skip("C++ test binary not built")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+def _row_classes(dconn, n_dofs, row_ptr, col_idx, min_rows):
+    """Row classes as the gather plan defines them: rows whose incidences,
+    sorted by (local index, slot bytes, element), and lengths coincide."""
+    import collections
+    k = dconn.shape[1]
+    inc = collections.defaultdict(list)
+    for e in range(dconn.shape[0]):
+        for i in range(k):
+            r = dconn[e, i]
+            cols = col_idx[row_ptr[r]:row_ptr[r + 1]]
+            inc[r].append((i, tuple(int(np.searchsorted(cols, dconn[e, j])) for j in range(k)), e))
+    sig = collections.Counter()
+    for r in range(n_dofs):
+        seq = tuple((i, sl) for i, sl, e in sorted(inc[r]))
+        sig[(int(row_ptr[r + 1] - row_ptr[r]), seq)] += 1
+    return [(ln, [i for i, _ in seq], [list(sl) for _, sl in seq])
+            for (ln, seq), c in sig.most_common() if c >= min_rows]
+
+
+def test_class_specialised_source_compiles(ff):
+    """The per-class gather kernels (rows in registers, compile-time slots) of
+    a 3D P2 Kuhn mesh compile for sm_100a through NVRTC."""
+    import pyoracle as po
+    c, v = po.kuhn_mesh(4)
+    d, nd = po.p2_dofs_kuhn(4, v)
+    rp, ci = po.build_pattern(d, nd)
+    classes = _row_classes(d, nd, rp, ci, 8)
+    assert len(classes) >= 8 and max(c[0] for c in classes) == 65
+    bil, lin = ff.named_form("poisson", 3)
+    f = ff.Form(None, 3, 2, bil, lin, quad_rule=4)
+    src = f.class_source(classes)
+    assert "ff_gather_classes_s" in src and "ff_gather_classes_l" in src
+    assert f.class_source(classes) == src  # byte-deterministic
+    g = ff.Form.from_source(None, src, 3, 2)
+    assert g.cubin[:4] == b"\x7fELF"

@@ -290,3 +290,32 @@ def test_north_star_size_properties(ff, ctx):
     ctx.check()
     assert float((va - vals).abs().max() / amax) <= 1e-12
     assert float((ra - rhs).abs().max() / rhs.abs().max()) <= 1e-12
+
+
+@pytest.mark.parametrize("dim,deg,n,form", [(3, 2, 10, "poisson"), (3, 1, 12, "helmholtz"), (2, 1, 64, "demo2d"),
+                                            (2, 2, 24, "helmholtz")])
+def test_class_specialised_gather_equals_generic_bitwise(ff, ctx, dim, deg, n, form):
+    """Row classes (slots as compile-time register indices) sum every CSR slot
+    in the same incidence order as the generic gather: identical bits."""
+    c, v, d, nd = _mesh(ff, dim, deg, n)
+    ctx.set_scatter("gather")
+    quad = 4 if dim == 3 else 3
+    b, l = ff.named_form(form, dim)
+    f = ff.Form(ctx, dim, deg, b, l, quad_rule=quad)
+    m = ff.Mesh(ctx, dim, c, v, None if deg == 1 else d, nd)
+    p = ff.Pattern(ctx, m)
+    try:
+        ctx.set_gather_classes(16)
+        gi = p.gather_info(m)
+        assert gi["n_classes"] > 0 and gi["n_class_rows"] > nd // 2
+        assert gi["n_class_rows"] + gi["n_items"] * 32 >= nd
+        v1, b1 = ff.assemble(f, m, p)
+        ctx.set_gather_classes(0)
+        assert p.gather_info(m)["n_classes"] == 0
+        v0, b0 = ff.assemble(f, m, p)
+    finally:
+        ctx.set_gather_classes(128)
+    assert v1.tobytes() == v0.tobytes() and b1.tobytes() == b0.tobytes()
+    orp, oci = po.build_pattern(d, nd)
+    ov, ob = po.assemble(form, dim, deg, quad, c, v, d, orp, oci, workers=8)
+    assert normwise(v1, ov) <= TOL and normwise(b1, ob) <= TOL
