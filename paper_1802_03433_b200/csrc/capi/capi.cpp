@@ -336,13 +336,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     for (int c = 0; c < 2; ++c) {
       long long i0 = cr[c][0], i1 = cr[c][1];
       if (i1 <= i0) continue;
-      int per_sm = 0;
-      ffb::cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                          &per_sm, reinterpret_cast<const void*>(p->class_kernel[c]), 128, 0),
-                      "class gather occupancy");
-      const int64_t want = (i1 - i0 + 3) / 4;
-      const unsigned grid = static_cast<unsigned>(
-          std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(per_sm, 1)) * ctx->sm_count)));
+      const unsigned grid = static_cast<unsigned>((i1 - i0 + 3) / 4);  // one item per warp
       const double* ginv = p->ginv;
       const int64_t* row_ptr = p->row_ptr;
       const int32_t* icls = gp.citem_class;
@@ -364,13 +358,10 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     int pitch = pitches[c];
     const int smem = gather_smem(pitch);
     require(smem <= kGatherSmemMax, "row gather: rows too long for the shared-memory accumulators");
-    int per_sm = 0;
-    ffb::cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                        &per_sm, reinterpret_cast<const void*>(f->kernel_grows[w]), kGatherWarps * 32, smem),
-                    "row-gather occupancy");
-    const int64_t want = (i1 - i0 + kGatherWarps - 1) / kGatherWarps;
-    const unsigned grid =
-        static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(std::max(per_sm, 1)) * ctx->sm_count)));
+    // a few items per warp (grid-stride): CTAs run in item order, so the items
+    // in flight stay contiguous and their element data stays in L2
+    const int64_t per_cta = int64_t(kGatherWarps) * 4;
+    const unsigned grid = static_cast<unsigned>((i1 - i0 + per_cta - 1) / per_cta);
     const double* ginv = p->ginv;
     const int64_t* row_ptr = p->row_ptr;
     const int32_t* order = gp.item_order;

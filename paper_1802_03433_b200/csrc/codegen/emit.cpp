@@ -168,7 +168,9 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
           "  __shared__ double stage[4][32 * FF_SP];\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
           "  double* st = stage[wid];\n"
-          "  for (ff_i64 w = i0 + (ff_i64)blockIdx.x * 4 + wid; w < i1; w += (ff_i64)gridDim.x * 4) {\n"
+          "  // one item per warp, CTAs in item order: the hardware keeps the items in\n"
+          "  // flight contiguous (Morton-local), so element data stays hot in L2\n"
+          "  {\n    const ff_i64 w = i0 + (ff_i64)blockIdx.x * 4 + wid;\n    if (w >= i1) return;\n"
           "    const int c = __ldg(citem_class + w);\n"
           "    const int row = __ldg(citem_rows + w * 32 + lane);\n"
           "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"

@@ -214,8 +214,9 @@ def test_gather_plan_covers_every_incidence(ff, ctx, dim, deg, n):
     gi = p.gather_info(m)
     k = d.shape[1]
     assert gi["n_incidences"] == d.shape[0] * k           # every (element, local row) once
-    assert gi["n_items"] == -(-nd // 32)
-    assert gi["n_steps"] * 32 >= gi["n_incidences"]
+    # every row is either in a specialised row class or in a generic item
+    assert gi["n_items"] == -(-(nd - gi["n_class_rows"]) // 32)
+    assert gi["n_class_items"] * 32 >= gi["n_class_rows"]
     assert gi["record_bytes"] == (8 if k <= 4 else 16)
     assert f.info["n_kinv"] > 0
 

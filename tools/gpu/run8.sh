@@ -2,6 +2,6 @@
 set -x
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -x 2>&1 | tail -4 > gpurun_out/pytest_gpu.txt
 timeout 400 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_ns.json 2> gpurun_out/bench_ns.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:ff_gather -s 3 -c 3 -o gpurun_out/prof_gather_ns6 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ff_gather_classes -s 2 -c 2 -o gpurun_out/prof_gather_ns7 \
   python bench.py --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full.txt 2>&1
 tail -4 gpurun_out/pytest_gpu.txt; cat gpurun_out/bench_ns.json; tail -3 gpurun_out/bench_ns.err; tail -2 gpurun_out/ncu_full.txt
