@@ -123,66 +123,85 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   }
 }
 #define FF_SP 33  // staging pitch (odd: conflict-free lane-row stores)
+#ifndef FF_CLASS_MINB
+#define FF_CLASS_MINB 4   // CTAs per SM the register budget is sized for
+#endif
 )";
+  // Rows longer than kPass entries are accumulated in passes over slot
+  // ranges of <= kPass entries (each pass reloads the element data and
+  // computes only its own entries), so every class fits one register budget.
+  constexpr int kPass = 33;
   auto class_fn = [&](int c) {
     const RowClass& k = classes[c];
-    const int depth = k.len > 33 ? 4 : 8;
-    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
+    const int n_pass = std::max(1, (k.len + kPass - 1) / kPass);
+    const int per = (k.len + n_pass - 1) / n_pass;
+    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences, " << n_pass << " pass(es)\n"
        << "__device__ __forceinline__ void ff_cls_" << c
        << "(const ff_i32* __restrict__ rec, const double* __restrict__ einv, double* __restrict__ st, int lane,\n"
-          "    ff_i64 rbeg, int row, double* __restrict__ values, double* __restrict__ rhs) {\n";
-    for (int p = 0; p < k.len; ++p) os << "  double a" << p << " = 0.0;\n";
+          "    ff_i64 rbeg, int row, double* __restrict__ values, double* __restrict__ rhs) {\n"
+          "  int e[" << std::max(k.steps, 1) << "];\n";
+    for (int q = 0; q < k.steps; ++q) os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
     os << "  double bs = 0.0;\n";
-    for (int s0 = 0; s0 < k.steps; s0 += depth) {
-      const int s1 = std::min(k.steps, s0 + depth);
-      os << "  {\n";
-      for (int s = s0; s < s1; ++s) os << "    const int e" << s << " = __ldcs(rec + " << s * 32 << ");\n";
-      for (int s = s0; s < s1; ++s)
-        os << "    double g" << s << "[FF_NKP], b" << s << "; ff_cload(e" << s << ", " << k.local[s] << ", einv, g" << s
-           << ", b" << s << ");\n";
-      for (int s = s0; s < s1; ++s) {
-        os << "    { double v[FF_NLOC]; ff_row<" << k.local[s] << ">(g" << s << ", v);";
-        for (int j = 0; j < n_local; ++j) os << " a" << int(k.slots[s * n_local + j]) << " += v[" << j << "];";
-        os << " bs += b" << s << "; }\n";
+    for (int ps = 0; ps < n_pass; ++ps) {
+      const int lo = ps * per, hi = std::min(k.len, lo + per);
+      os << "  {  // slots [" << lo << ", " << hi << ")\n";
+      for (int p = lo; p < hi; ++p) os << "    double a" << p << " = 0.0;\n";
+      constexpr int kDepth = 4;
+      for (int s0 = 0; s0 < k.steps; s0 += kDepth) {
+        const int s1 = std::min(k.steps, s0 + kDepth);
+        os << "    {\n";
+        for (int q = s0; q < s1; ++q)
+          os << "      double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] << ", einv, g" << q
+             << ", b" << q << ");\n";
+        for (int q = s0; q < s1; ++q) {
+          std::string adds;
+          for (int j = 0; j < n_local; ++j) {
+            const int sl = k.slots[q * n_local + j];
+            if (sl >= lo && sl < hi) adds += " a" + std::to_string(sl) + " += v[" + std::to_string(j) + "];";
+          }
+          if (!adds.empty())
+            os << "      { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);" << adds << " }\n";
+          if (ps == 0) os << "      bs += b" << q << ";\n";
+        }
+        os << "    }\n";
+      }
+      for (int q0 = lo; q0 < hi; q0 += 32) {
+        const int cnt = std::min(32, hi - q0);
+        for (int j = 0; j < cnt; ++j) os << "    st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
+        os << "    __syncwarp();\n"
+              "    for (int m = 0; m < 32; ++m) {\n"
+              "      const ff_i64 rb = __shfl_sync(0xffffffffu, rbeg, m);\n"
+              "      const int rm = __shfl_sync(0xffffffffu, row, m);\n"
+           << "      if (rm >= 0 && lane < " << cnt << ") __stcs(values + rb + " << q0
+           << " + lane, st[m * FF_SP + lane]);\n"
+           << "    }\n    __syncwarp();\n";
       }
       os << "  }\n";
-    }
-    for (int q0 = 0; q0 < k.len; q0 += 32) {
-      const int cnt = std::min(32, k.len - q0);
-      for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
-      os << "  __syncwarp();\n"
-            "  for (int m = 0; m < 32; ++m) {\n"
-            "    const ff_i64 rb = __shfl_sync(0xffffffffu, rbeg, m);\n"
-            "    const int rm = __shfl_sync(0xffffffffu, row, m);\n"
-         << "    if (rm >= 0 && lane < " << cnt << ") __stcs(values + rb + " << q0 << " + lane, st[m * FF_SP + lane]);\n"
-         << "  }\n  __syncwarp();\n";
     }
     os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
   };
   for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
-  auto kernel = [&](const char* name, bool longrows) {
-    os << "extern \"C\" __global__ void __launch_bounds__(128)\n" << name
-       << "(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr, double* __restrict__ values,\n"
-          "    double* __restrict__ rhs, const ff_i32* __restrict__ citem_class, const ff_i32* __restrict__ citem_rows,\n"
-          "    const ff_i64* __restrict__ citem_rec, const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
-          "  __shared__ double stage[4][32 * FF_SP];\n"
-          "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
-          "  double* st = stage[wid];\n"
-          "  // one item per warp, CTAs in item order: the hardware keeps the items in\n"
-          "  // flight contiguous (Morton-local), so element data stays hot in L2\n"
-          "  {\n    const ff_i64 w = i0 + (ff_i64)blockIdx.x * 4 + wid;\n    if (w >= i1) return;\n"
-          "    const int c = __ldg(citem_class + w);\n"
-          "    const int row = __ldg(citem_rows + w * 32 + lane);\n"
-          "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
-          "    const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
-          "    switch (c) {\n";
-    for (int c = 0; c < static_cast<int>(classes.size()); ++c)
-      if ((classes[c].len > 33) == longrows)
-        os << "      case " << c << ": ff_cls_" << c << "(rec, einv, st, lane, rbeg, row, values, rhs); break;\n";
-    os << "      default: break;\n    }\n  }\n}\n";
-  };
-  kernel("ff_gather_classes_s", false);
-  kernel("ff_gather_classes_l", true);
+  os << "// 4 consecutive (Morton-ordered) items per warp, CTAs in item order: the\n"
+        "// items in flight stay spatially compact, so element data is reused in L1/L2\n"
+        "extern \"C\" __global__ void __launch_bounds__(128, FF_CLASS_MINB)\n"
+        "ff_gather_classes(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr,\n"
+        "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
+        "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec, const ff_i32* __restrict__ crec,\n"
+        "    ff_i64 i0, ff_i64 i1) {\n"
+        "  __shared__ double stage[4][32 * FF_SP];\n"
+        "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
+        "  double* st = stage[wid];\n"
+        "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * 4;\n"
+        "  const ff_i64 last = first + 4 < i1 ? first + 4 : i1;\n"
+        "  for (ff_i64 w = first; w < last; ++w) {\n"
+        "    const int c = __ldg(citem_class + w);\n"
+        "    const int row = __ldg(citem_rows + w * 32 + lane);\n"
+        "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
+        "    const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
+        "    switch (c) {\n";
+  for (int c = 0; c < static_cast<int>(classes.size()); ++c)
+    os << "      case " << c << ": ff_cls_" << c << "(rec, einv, st, lane, rbeg, row, values, rhs); break;\n";
+  os << "      default: break;\n    }\n  }\n}\n";
   return os.str();
 }
 
