@@ -204,7 +204,7 @@ void ensure_tile_plan(ff_pattern* p, const ff_mesh* m, const codegen::RowTilePar
 void free_class_module(ff_pattern* p) {
   if (p->class_lib) cudaLibraryUnload(p->class_lib);
   p->class_lib = nullptr;
-  p->class_kernel = nullptr;
+  p->class_kernel[0] = p->class_kernel[1] = nullptr;
   p->class_key.clear();
 }
 
@@ -233,13 +233,12 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   }
   const auto t0 = std::chrono::steady_clock::now();
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc);
-  if (const char* mb = std::getenv("FF_CLASS_MINB"))  // tuning knob: register budget of the class kernel
-    src = "#define FF_CLASS_MINB " + std::to_string(std::max(1, std::atoi(mb))) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
   bind(p->ctx);
   ffb::cuda_check(cudaLibraryLoadData(&p->class_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
                   "cudaLibraryLoadData (classes)");
-  ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel, p->class_lib, "ff_gather_classes"), "class kernel");
+  ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[0], p->class_lib, "ff_gather_classes_s"), "class kernel");
+  ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[1], p->class_lib, "ff_gather_classes_l"), "class kernel");
   p->class_compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   p->class_key = key;
 }
@@ -334,17 +333,22 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   // K2b for the row classes: specialised kernels (rows in registers)
   if (gp.n_citems > 0) {
     ensure_class_module(f, p);
-    long long i0 = 0, i1 = gp.n_citems;
-    const unsigned grid = static_cast<unsigned>((i1 - i0 + 15) / 16);  // 4 warps x 4 items
-    const double* ginv = p->ginv;
-    const int64_t* row_ptr = p->row_ptr;
-    const int32_t* icls = gp.citem_class;
-    const int32_t* irows = gp.citem_rows;
-    const int64_t* irec = gp.citem_rec;
-    const int32_t* crec = gp.crec;
-    void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
-    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel), dim3(grid), dim3(128), args, 0, s),
-                    "K2b (class row gather) launch");
+    const int64_t cr[2][2] = {{0, gp.n_citems_short}, {gp.n_citems_short, gp.n_citems}};
+    for (int c = 0; c < 2; ++c) {
+      long long i0 = cr[c][0], i1 = cr[c][1];
+      if (i1 <= i0) continue;
+      const unsigned grid = static_cast<unsigned>((i1 - i0 + 15) / 16);  // 4 warps x 4 items
+      const double* ginv = p->ginv;
+      const int64_t* row_ptr = p->row_ptr;
+      const int32_t* icls = gp.citem_class;
+      const int32_t* irows = gp.citem_rows;
+      const int64_t* irec = gp.citem_rec;
+      const int32_t* crec = gp.crec;
+      void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
+      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(128), args,
+                                       0, s),
+                      "K2b (class row gather) launch");
+    }
   }
   // K2b for the remaining rows in two launches: short-pitch items, then long-pitch items
   const int64_t ranges[2][2] = {{0, gp.n_short}, {gp.n_short, gp.n_items}};
@@ -526,8 +530,6 @@ int ff_class_source(const ff_form* f, int n, const int32_t* len, const int32_t* 
       at += steps[c];
     }
     std::string src = codegen::emit_class_source(f->plan, f->n_local, rc);
-  if (const char* mb = std::getenv("FF_CLASS_MINB"))  // tuning knob: register budget of the class kernel
-    src = "#define FF_CLASS_MINB " + std::to_string(std::max(1, std::atoi(mb))) + "\n" + src;
     if (out_len) *out_len = src.size();
     if (buf && cap) {
       const std::size_t k = std::min(cap - 1, src.size());

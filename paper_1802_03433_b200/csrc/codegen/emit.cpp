@@ -123,85 +123,102 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   }
 }
 #define FF_SP 33  // staging pitch (odd: conflict-free lane-row stores)
-#ifndef FF_CLASS_MINB
-#define FF_CLASS_MINB 4   // CTAs per SM the register budget is sized for
-#endif
+#define FF_PRE 8  // records of the next item prefetched while this item computes
 )";
-  // Rows longer than kPass entries are accumulated in passes over slot
-  // ranges of <= kPass entries (each pass reloads the element data and
-  // computes only its own entries), so every class fits one register budget.
-  constexpr int kPass = 33;
+  // class c with rows of <= 33 entries -> ff_gather_classes_s, else _l
+  auto is_long = [&](int c) { return classes[c].len > 33; };
   auto class_fn = [&](int c) {
     const RowClass& k = classes[c];
-    const int n_pass = std::max(1, (k.len + kPass - 1) / kPass);
-    const int per = (k.len + n_pass - 1) / n_pass;
-    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences, " << n_pass << " pass(es)\n"
+    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
        << "__device__ __forceinline__ void ff_cls_" << c
-       << "(const ff_i32* __restrict__ rec, const double* __restrict__ einv, double* __restrict__ st, int lane,\n"
-          "    ff_i64 rbeg, int row, double* __restrict__ values, double* __restrict__ rhs) {\n"
+       << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv,\n"
+          "    double* __restrict__ st, int lane, ff_i64 rbeg, int row, double* __restrict__ values,\n"
+          "    double* __restrict__ rhs) {\n"
           "  int e[" << std::max(k.steps, 1) << "];\n";
-    for (int q = 0; q < k.steps; ++q) os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
+    for (int q = 0; q < k.steps; ++q) {
+      if (q < 8)
+        os << "  e[" << q << "] = ep[" << q << "];\n";
+      else
+        os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
+    }
+    for (int p = 0; p < k.len; ++p) os << "  double a" << p << " = 0.0;\n";
     os << "  double bs = 0.0;\n";
-    for (int ps = 0; ps < n_pass; ++ps) {
-      const int lo = ps * per, hi = std::min(k.len, lo + per);
-      os << "  {  // slots [" << lo << ", " << hi << ")\n";
-      for (int p = lo; p < hi; ++p) os << "    double a" << p << " = 0.0;\n";
-      constexpr int kDepth = 4;
-      for (int s0 = 0; s0 < k.steps; s0 += kDepth) {
-        const int s1 = std::min(k.steps, s0 + kDepth);
-        os << "    {\n";
-        for (int q = s0; q < s1; ++q)
-          os << "      double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] << ", einv, g" << q
-             << ", b" << q << ");\n";
-        for (int q = s0; q < s1; ++q) {
-          std::string adds;
-          for (int j = 0; j < n_local; ++j) {
-            const int sl = k.slots[q * n_local + j];
-            if (sl >= lo && sl < hi) adds += " a" + std::to_string(sl) + " += v[" + std::to_string(j) + "];";
-          }
-          if (!adds.empty())
-            os << "      { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);" << adds << " }\n";
-          if (ps == 0) os << "      bs += b" << q << ";\n";
-        }
-        os << "    }\n";
-      }
-      for (int q0 = lo; q0 < hi; q0 += 32) {
-        const int cnt = std::min(32, hi - q0);
-        for (int j = 0; j < cnt; ++j) os << "    st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
-        os << "    __syncwarp();\n"
-              "    for (int m = 0; m < 32; ++m) {\n"
-              "      const ff_i64 rb = __shfl_sync(0xffffffffu, rbeg, m);\n"
-              "      const int rm = __shfl_sync(0xffffffffu, row, m);\n"
-           << "      if (rm >= 0 && lane < " << cnt << ") __stcs(values + rb + " << q0
-           << " + lane, st[m * FF_SP + lane]);\n"
-           << "    }\n    __syncwarp();\n";
+    const int depth = is_long(c) ? 4 : 8;
+    for (int s0 = 0; s0 < k.steps; s0 += depth) {
+      const int s1 = std::min(k.steps, s0 + depth);
+      os << "  {\n";
+      for (int q = s0; q < s1; ++q)
+        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] << ", einv, g" << q
+           << ", b" << q << ");\n";
+      for (int q = s0; q < s1; ++q) {
+        os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);";
+        for (int j = 0; j < n_local; ++j) os << " a" << int(k.slots[q * n_local + j]) << " += v[" << j << "];";
+        os << " bs += b" << q << "; }\n";
       }
       os << "  }\n";
+    }
+    for (int q0 = 0; q0 < k.len; q0 += 32) {
+      const int cnt = std::min(32, k.len - q0);
+      for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
+      os << "  __syncwarp();\n"
+            "  for (int m = 0; m < 32; ++m) {\n"
+            "    const ff_i64 rb = __shfl_sync(0xffffffffu, rbeg, m);\n"
+            "    const int rm = __shfl_sync(0xffffffffu, row, m);\n"
+         << "    if (rm >= 0 && lane < " << cnt << ") __stcs(values + rb + " << q0 << " + lane, st[m * FF_SP + lane]);\n"
+         << "  }\n  __syncwarp();\n";
     }
     os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
   };
   for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
-  os << "// 4 consecutive (Morton-ordered) items per warp, CTAs in item order: the\n"
-        "// items in flight stay spatially compact, so element data is reused in L1/L2\n"
-        "extern \"C\" __global__ void __launch_bounds__(128, FF_CLASS_MINB)\n"
-        "ff_gather_classes(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr,\n"
-        "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
-        "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec, const ff_i32* __restrict__ crec,\n"
-        "    ff_i64 i0, ff_i64 i1) {\n"
-        "  __shared__ double stage[4][32 * FF_SP];\n"
-        "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
-        "  double* st = stage[wid];\n"
-        "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * 4;\n"
-        "  const ff_i64 last = first + 4 < i1 ? first + 4 : i1;\n"
-        "  for (ff_i64 w = first; w < last; ++w) {\n"
-        "    const int c = __ldg(citem_class + w);\n"
-        "    const int row = __ldg(citem_rows + w * 32 + lane);\n"
-        "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
-        "    const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
-        "    switch (c) {\n";
-  for (int c = 0; c < static_cast<int>(classes.size()); ++c)
-    os << "      case " << c << ": ff_cls_" << c << "(rec, einv, st, lane, rbeg, row, values, rhs); break;\n";
-  os << "      default: break;\n    }\n  }\n}\n";
+  os << "__constant__ int ff_csteps[" << std::max<std::size_t>(classes.size(), 1) << "] = {";
+  for (std::size_t c = 0; c < classes.size(); ++c) os << (c ? ", " : "") << classes[c].steps;
+  if (classes.empty()) os << "0";
+  os << "};\n";
+  auto kernel = [&](const char* name, bool longrows, int minb) {
+    os << "// items of one launch: 4 consecutive (Morton-ordered) items per warp, CTAs in\n"
+          "// item order (items in flight stay spatially compact: element data reused in\n"
+          "// L1/L2); the next item's class, row and first records load during this one\n"
+          "extern \"C\" __global__ void __launch_bounds__(128, "
+       << minb << ")\n" << name
+       << "(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr,\n"
+          "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
+          "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
+          "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
+          "  __shared__ double stage[4][32 * FF_SP];\n"
+          "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
+          "  double* st = stage[wid];\n"
+          "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * 4;\n"
+          "  const ff_i64 last = first + 4 < i1 ? first + 4 : i1;\n"
+          "  if (first >= last) return;\n"
+          "  int c, row, ep[FF_PRE];\n"
+          "  ff_i64 rbeg;\n"
+          "  const ff_i32* rec;\n"
+          "  auto fetch = [&](ff_i64 w, int& cc, int& rr, ff_i64& rb, const ff_i32*& rc, int (&ee)[FF_PRE]) {\n"
+          "    cc = __ldg(citem_class + w);\n"
+          "    rr = __ldg(citem_rows + w * 32 + lane);\n"
+          "    rc = crec + __ldg(citem_rec + w) * 32 + lane;\n"
+          "    const int ns = ff_csteps[cc];\n"
+          "#pragma unroll\n"
+          "    for (int u = 0; u < FF_PRE; ++u) ee[u] = u < ns ? __ldcs(rc + u * 32) : -1;\n"
+          "    rb = rr >= 0 ? __ldg(row_ptr + rr) : 0;\n"
+          "  };\n"
+          "  fetch(first, c, row, rbeg, rec, ep);\n"
+          "  for (ff_i64 w = first; w < last; ++w) {\n"
+          "    int cn = 0, rown = -1, epn[FF_PRE];\n"
+          "    ff_i64 rbn = 0;\n"
+          "    const ff_i32* recn = rec;\n"
+          "    if (w + 1 < last) fetch(w + 1, cn, rown, rbn, recn, epn);\n"
+          "    switch (c) {\n";
+    for (int c = 0; c < static_cast<int>(classes.size()); ++c)
+      if (is_long(c) == longrows)
+        os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, st, lane, rbeg, row, values, rhs); break;\n";
+    os << "      default: break;\n    }\n"
+          "    c = cn;\n    row = rown;\n    rbeg = rbn;\n    rec = recn;\n"
+          "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
+          "  }\n}\n";
+  };
+  kernel("ff_gather_classes_s", false, 4);
+  kernel("ff_gather_classes_l", true, 2);
   return os.str();
 }
 

@@ -158,9 +158,9 @@ struct RowClass {
   std::vector<std::uint8_t> slots;   // [steps][n_local] slot of column dof[j] in the row
 };
 
-// NVRTC translation unit with ff_gather_classes (rows longer than 33 entries
-// are accumulated in slot-range passes). Needs a gather-capable plan
-// (plan.n_kinv > 0). Byte-deterministic.
+// NVRTC translation unit with ff_gather_classes_s (classes of rows <= 33
+// entries) and ff_gather_classes_l (longer rows). Needs a gather-capable
+// plan (plan.n_kinv > 0). Byte-deterministic.
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes);
 
 // Shortest round-trip double literal valid in C/CUDA source.

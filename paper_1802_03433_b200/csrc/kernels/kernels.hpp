@@ -51,7 +51,7 @@ struct GatherPlan {
     int64_t rows = 0;
   };
   std::vector<Class> classes;
-  int64_t n_citems = 0, n_crec = 0, n_class_rows = 0;
+  int64_t n_citems = 0, n_citems_short = 0, n_crec = 0, n_class_rows = 0;
   int32_t* citem_class = nullptr;   // [n_citems]
   int32_t* citem_rows = nullptr;    // [n_citems][32] local row or -1
   int64_t* citem_rec = nullptr;     // [n_citems] first record of the item ([steps][32] element ids)

@@ -706,8 +706,12 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       ++it->second.first;
     }
     std::vector<std::pair<int64_t, uint64_t>> big;
+    // classes worth a specialised kernel: >= min_class_rows rows and >= 0.5 %
+    // of the block (boundary classes stay generic: smaller code, fewer
+    // instruction-cache misses)
+    const int64_t min_rows = std::max<int64_t>(min_class_rows, n_rows / 200);
     for (const auto& [h, v] : count)
-      if (v.first >= min_class_rows) big.push_back({v.first, h});
+      if (v.first >= min_rows) big.push_back({v.first, h});
     std::sort(big.begin(), big.end(), [&](const auto& a, const auto& b) {
       return a.first != b.first ? a.first > b.first : count[a.second].second < count[b.second].second;
     });
@@ -781,7 +785,14 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       out->classes[c].rows = static_cast<int64_t>(members[c].size());
       for (size_t q = 0; q < first_pos[c].size(); ++q) items.push_back({first_pos[c][q], c, static_cast<int64_t>(q)});
     }
-    std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) { return a.key < b.key; });
+    // short-row classes (<= 33 entries) first, then long-row ones: two
+    // specialised kernels with their own register budgets
+    auto longrows = [&](const Item& it) { return out->classes[it.c].len > 33 ? 1 : 0; };
+    std::sort(items.begin(), items.end(), [&](const Item& a, const Item& b) {
+      return longrows(a) != longrows(b) ? longrows(a) < longrows(b) : a.key < b.key;
+    });
+    out->n_citems_short = 0;
+    for (const Item& it : items) out->n_citems_short += longrows(it) ? 0 : 1;
     const int64_t nci = static_cast<int64_t>(items.size());
     std::vector<int32_t> ic(nci), ir(nci * 32, -1), cls_steps(std::max(n_cls, 1), 0);
     std::vector<int64_t> irec(nci + 1, 0);

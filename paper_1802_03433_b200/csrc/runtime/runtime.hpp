@@ -109,7 +109,7 @@ struct ff_pattern {
   // class-specialised gather kernels for (form source, plan)
   std::string class_key;
   cudaLibrary_t class_lib = nullptr;
-  cudaKernel_t class_kernel = nullptr;
+  cudaKernel_t class_kernel[2] = {nullptr, nullptr};  // short rows, long rows
   double class_compile_ms = 0.0;
   double* ginv = nullptr;   // [ne][nkp]
   double* bvec = nullptr;   // [ne][k]
