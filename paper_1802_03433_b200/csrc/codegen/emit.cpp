@@ -124,6 +124,15 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
 }
 #define FF_SP 33  // staging pitch (odd: conflict-free lane-row stores)
 #define FF_PRE 8  // records of the next item prefetched while this item computes
+#ifndef FF_IPW
+#define FF_IPW 4  // consecutive items per warp
+#endif
+#ifndef FF_MINB_S
+#define FF_MINB_S 4  // CTAs per SM the register budgets are sized for
+#endif
+#ifndef FF_MINB_L
+#define FF_MINB_L 2
+#endif
 )";
   // class c with rows of <= 33 entries -> ff_gather_classes_s, else _l
   auto is_long = [&](int c) { return classes[c].len > 33; };
@@ -132,8 +141,8 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
     os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
        << "__device__ __forceinline__ void ff_cls_" << c
        << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv,\n"
-          "    double* __restrict__ st, int lane, ff_i64 rbeg, int row, double* __restrict__ values,\n"
-          "    double* __restrict__ rhs) {\n"
+          "    double* __restrict__ st, ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row,\n"
+          "    double* __restrict__ values, double* __restrict__ rhs) {\n"
           "  int e[" << std::max(k.steps, 1) << "];\n";
     for (int q = 0; q < k.steps; ++q) {
       if (q < 8)
@@ -157,14 +166,17 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
       }
       os << "  }\n";
     }
+    // write-out through the staging rows: flat index f over the 32 rows x cnt
+    // slots (consecutive lanes = consecutive CSR values of one row)
+    os << "  sr[lane] = row >= 0 ? rbeg : -1;\n";
     for (int q0 = 0; q0 < k.len; q0 += 32) {
       const int cnt = std::min(32, k.len - q0);
       for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
       os << "  __syncwarp();\n"
-            "  for (int m = 0; m < 32; ++m) {\n"
-            "    const ff_i64 rb = __shfl_sync(0xffffffffu, rbeg, m);\n"
-            "    const int rm = __shfl_sync(0xffffffffu, row, m);\n"
-         << "    if (rm >= 0 && lane < " << cnt << ") __stcs(values + rb + " << q0 << " + lane, st[m * FF_SP + lane]);\n"
+         << "#pragma unroll\n  for (int u = 0; u < " << cnt << "; ++u) {\n"
+         << "    const int f = u * 32 + lane, m = f / " << cnt << ", j = f - m * " << cnt << ";\n"
+         << "    const ff_i64 rb = sr[m];\n"
+         << "    if (rb >= 0) __stcs(values + rb + " << q0 << " + j, st[m * FF_SP + j]);\n"
          << "  }\n  __syncwarp();\n";
     }
     os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
@@ -174,21 +186,23 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   for (std::size_t c = 0; c < classes.size(); ++c) os << (c ? ", " : "") << classes[c].steps;
   if (classes.empty()) os << "0";
   os << "};\n";
-  auto kernel = [&](const char* name, bool longrows, int minb) {
+  auto kernel = [&](const char* name, bool longrows) {
     os << "// items of one launch: 4 consecutive (Morton-ordered) items per warp, CTAs in\n"
           "// item order (items in flight stay spatially compact: element data reused in\n"
           "// L1/L2); the next item's class, row and first records load during this one\n"
           "extern \"C\" __global__ void __launch_bounds__(128, "
-       << minb << ")\n" << name
+       << (longrows ? "FF_MINB_L" : "FF_MINB_S") << ")\n" << name
        << "(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr,\n"
           "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
           "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
           "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
           "  __shared__ double stage[4][32 * FF_SP];\n"
+          "  __shared__ ff_i64 srow[4][32];\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
           "  double* st = stage[wid];\n"
-          "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * 4;\n"
-          "  const ff_i64 last = first + 4 < i1 ? first + 4 : i1;\n"
+          "  ff_i64* sr = srow[wid];\n"
+          "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * FF_IPW;\n"
+          "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
           "  int c, row, ep[FF_PRE];\n"
           "  ff_i64 rbeg;\n"
@@ -211,14 +225,14 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
           "    switch (c) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
-        os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, st, lane, rbeg, row, values, rhs); break;\n";
+        os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, st, sr, lane, rbeg, row, values, rhs); break;\n";
     os << "      default: break;\n    }\n"
           "    c = cn;\n    row = rown;\n    rbeg = rbn;\n    rec = recn;\n"
           "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
           "  }\n}\n";
   };
-  kernel("ff_gather_classes_s", false, 4);
-  kernel("ff_gather_classes_l", true, 2);
+  kernel("ff_gather_classes_s", false);
+  kernel("ff_gather_classes_l", true);
   return os.str();
 }
 
