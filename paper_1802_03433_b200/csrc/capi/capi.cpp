@@ -233,6 +233,10 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   }
   const auto t0 = std::chrono::steady_clock::now();
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc);
+  // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
+  for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L"})
+    if (const char* v = std::getenv(knob))
+      src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
   bind(p->ctx);
   ffb::cuda_check(cudaLibraryLoadData(&p->class_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
@@ -337,7 +341,9 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     for (int c = 0; c < 2; ++c) {
       long long i0 = cr[c][0], i1 = cr[c][1];
       if (i1 <= i0) continue;
-      const unsigned grid = static_cast<unsigned>((i1 - i0 + 15) / 16);  // 4 warps x 4 items
+      const char* ipw_env = std::getenv("FF_IPW");
+      const int64_t ipw = ipw_env ? std::max(1, std::atoi(ipw_env)) : 4;
+      const unsigned grid = static_cast<unsigned>((i1 - i0 + 4 * ipw - 1) / (4 * ipw));  // 4 warps x FF_IPW items
       const double* ginv = p->ginv;
       const int64_t* row_ptr = p->row_ptr;
       const int32_t* icls = gp.citem_class;
