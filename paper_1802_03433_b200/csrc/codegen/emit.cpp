@@ -124,6 +124,20 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
 }
 #define FF_SP 33  // staging pitch (odd: conflict-free lane-row stores)
 #define FF_PRE 8  // records of the next item prefetched while this item computes
+// staged rows -> CSR values: flat index f over 32 rows x cnt slots, so
+// consecutive lanes write consecutive values of one row. Shared by every
+// class (one copy, not unrolled: keeps the instruction footprint small).
+__device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
+                                         int cnt, int q0, double* __restrict__ values) {
+  __syncwarp();
+#pragma unroll 1
+  for (int f = lane; f < 32 * cnt; f += 32) {
+    const int m = f / cnt, j = f - m * cnt;
+    const ff_i64 rb = sr[m];
+    if (rb >= 0) __stcs(values + rb + q0 + j, st[m * FF_SP + j]);
+  }
+  __syncwarp();
+}
 #ifndef FF_IPW
 #define FF_IPW 4  // consecutive items per warp
 #endif
@@ -172,12 +186,7 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
     for (int q0 = 0; q0 < k.len; q0 += 32) {
       const int cnt = std::min(32, k.len - q0);
       for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
-      os << "  __syncwarp();\n"
-         << "#pragma unroll\n  for (int u = 0; u < " << cnt << "; ++u) {\n"
-         << "    const int f = u * 32 + lane, m = f / " << cnt << ", j = f - m * " << cnt << ";\n"
-         << "    const ff_i64 rb = sr[m];\n"
-         << "    if (rb >= 0) __stcs(values + rb + " << q0 << " + j, st[m * FF_SP + j]);\n"
-         << "  }\n  __syncwarp();\n";
+      os << "  ff_writeout(st, sr, lane, " << cnt << ", " << q0 << ", values);\n";
     }
     os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
   };
@@ -187,9 +196,10 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   if (classes.empty()) os << "0";
   os << "};\n";
   auto kernel = [&](const char* name, bool longrows) {
-    os << "// items of one launch: 4 consecutive (Morton-ordered) items per warp, CTAs in\n"
-          "// item order (items in flight stay spatially compact: element data reused in\n"
-          "// L1/L2); the next item's class, row and first records load during this one\n"
+    os << "// items of one launch: FF_IPW consecutive items per warp, CTAs in item order;\n"
+          "// items are sorted by (Morton window, class): a CTA runs one class (small\n"
+          "// instruction footprint per SM) and the items in flight stay spatially\n"
+          "// compact (element data reused in L1/L2)\n"
           "extern \"C\" __global__ void __launch_bounds__(128, "
        << (longrows ? "FF_MINB_L" : "FF_MINB_S") << ")\n" << name
        << "(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr,\n"
@@ -204,32 +214,20 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
           "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * FF_IPW;\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
-          "  int c, row, ep[FF_PRE];\n"
-          "  ff_i64 rbeg;\n"
-          "  const ff_i32* rec;\n"
-          "  auto fetch = [&](ff_i64 w, int& cc, int& rr, ff_i64& rb, const ff_i32*& rc, int (&ee)[FF_PRE]) {\n"
-          "    cc = __ldg(citem_class + w);\n"
-          "    rr = __ldg(citem_rows + w * 32 + lane);\n"
-          "    rc = crec + __ldg(citem_rec + w) * 32 + lane;\n"
-          "    const int ns = ff_csteps[cc];\n"
-          "#pragma unroll\n"
-          "    for (int u = 0; u < FF_PRE; ++u) ee[u] = u < ns ? __ldcs(rc + u * 32) : -1;\n"
-          "    rb = rr >= 0 ? __ldg(row_ptr + rr) : 0;\n"
-          "  };\n"
-          "  fetch(first, c, row, rbeg, rec, ep);\n"
           "  for (ff_i64 w = first; w < last; ++w) {\n"
-          "    int cn = 0, rown = -1, epn[FF_PRE];\n"
-          "    ff_i64 rbn = 0;\n"
-          "    const ff_i32* recn = rec;\n"
-          "    if (w + 1 < last) fetch(w + 1, cn, rown, rbn, recn, epn);\n"
+          "    const int c = __ldg(citem_class + w);\n"
+          "    const int row = __ldg(citem_rows + w * 32 + lane);\n"
+          "    const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
+          "    int ep[FF_PRE];\n"
+          "    const int ns = ff_csteps[c];\n"
+          "#pragma unroll\n"
+          "    for (int u = 0; u < FF_PRE; ++u) ep[u] = u < ns ? __ldcs(rec + u * 32) : -1;\n"
+          "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
           "    switch (c) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
         os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, st, sr, lane, rbeg, row, values, rhs); break;\n";
-    os << "      default: break;\n    }\n"
-          "    c = cn;\n    row = rown;\n    rbeg = rbn;\n    rec = recn;\n"
-          "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
-          "  }\n}\n";
+    os << "      default: break;\n    }\n  }\n}\n";
   };
   kernel("ff_gather_classes_s", false);
   kernel("ff_gather_classes_l", true);

@@ -788,8 +788,13 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     // short-row classes (<= 33 entries) first, then long-row ones: two
     // specialised kernels with their own register budgets
     auto longrows = [&](const Item& it) { return out->classes[it.c].len > 33 ? 1 : 0; };
+    // within each, by (Morton window of 4096 rows, class, position): the 16
+    // items a CTA takes are of one class (one instruction footprint per CTA)
+    auto win = [&](const Item& it) { return it.key / 4096; };
     std::sort(items.begin(), items.end(), [&](const Item& a, const Item& b) {
-      return longrows(a) != longrows(b) ? longrows(a) < longrows(b) : a.key < b.key;
+      if (longrows(a) != longrows(b)) return longrows(a) < longrows(b);
+      if (win(a) != win(b)) return win(a) < win(b);
+      return a.c != b.c ? a.c < b.c : a.key < b.key;
     });
     out->n_citems_short = 0;
     for (const Item& it : items) out->n_citems_short += longrows(it) ? 0 : 1;
