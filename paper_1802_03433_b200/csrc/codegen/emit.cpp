@@ -130,11 +130,12 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
 __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
                                          int cnt, int q0, double* __restrict__ values) {
   __syncwarp();
-#pragma unroll 1
-  for (int f = lane; f < 32 * cnt; f += 32) {
-    const int m = f / cnt, j = f - m * cnt;
-    const ff_i64 rb = sr[m];
-    if (rb >= 0) __stcs(values + rb + q0 + j, st[m * FF_SP + j]);
+  if (lane < cnt) {
+#pragma unroll 4
+    for (int m = 0; m < 32; ++m) {
+      const ff_i64 rb = sr[m];
+      if (rb >= 0) __stcs(values + rb + q0 + lane, st[m * FF_SP + lane]);
+    }
   }
   __syncwarp();
 }
