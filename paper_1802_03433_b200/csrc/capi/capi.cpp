@@ -279,7 +279,7 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         4096, ctx->sm_count, ctx->stream, &p->gather,
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
-                                                        cmin > 0 ? 64 : 0);
+                                                        cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"));
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
@@ -325,7 +325,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       const int32_t* dconn = m->dconn;
       long long ne = m->ne;
       double* ginv = p->ginv;
-      void* args[] = {&coords, &vconn, &dconn, &ne, &ginv, &status};
+      const int32_t* eorder = p->gather.eorder;
+      void* args[] = {&coords, &vconn, &dconn, &eorder, &ne, &ginv, &status};
       const unsigned grid = static_cast<unsigned>((m->ne + f->block - 1) / f->block);
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_ginv[w]), dim3(grid), dim3(f->block),
                                        args, 0, s),

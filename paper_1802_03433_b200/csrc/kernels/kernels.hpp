@@ -55,13 +55,18 @@ struct GatherPlan {
   int32_t* citem_class = nullptr;   // [n_citems]
   int32_t* citem_rows = nullptr;    // [n_citems][32] local row or -1
   int64_t* citem_rec = nullptr;     // [n_citems] first record of the item ([steps][32] element ids)
-  int32_t* crec = nullptr;          // [n_crec] element ids (-1: idle lane)
+  int32_t* crec = nullptr;          // [n_crec] element records (-1: idle lane)
+  // element order of the per-element records: record t belongs to element
+  // eorder[t]; records (rec, crec) hold erank[e]
+  int32_t* eorder = nullptr;
+  int32_t* erank = nullptr;
 };
 // bbox: {min x, min y, min z, max x, max y, max z} of the mesh coordinates.
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
-                              cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64);
+                              cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64,
+                              bool use_eorder = true);
 void free_gather_plan(GatherPlan* p);
 
 // Order-independent 64-bit content hash of n int32 values (sum of mixed

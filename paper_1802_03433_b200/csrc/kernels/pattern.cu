@@ -325,6 +325,35 @@ __global__ void dof_morton(const double* __restrict__ coords, const int32_t* __r
   }
 }
 
+// Morton code of every element's vertex centroid (element data order of the
+// gather: elements used by the same rows are neighbours in memory)
+__global__ void elem_morton(const double* __restrict__ coords, const int32_t* __restrict__ vconn, int64_t ne, int dim,
+                            double lx, double ly, double lz, double sx, double sy, double sz,
+                            uint64_t* __restrict__ code, int32_t* __restrict__ ids) {
+  const int nv = dim + 1;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double p[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < nv; ++a) {
+      const int64_t v = vconn[e * nv + a];
+      for (int c = 0; c < dim; ++c) p[c] += coords[v * dim + c];
+    }
+    const double lo[3] = {lx, ly, lz}, sc[3] = {sx, sy, sz};
+    uint64_t qv[3] = {0, 0, 0};
+    const double qmax = dim == 3 ? 2097151.0 : 2147483647.0;
+    for (int c = 0; c < dim; ++c) qv[c] = static_cast<uint64_t>(fmin(fmax((p[c] / nv - lo[c]) * sc[c], 0.0), qmax));
+    code[e] = dim == 3 ? (spread3(qv[0]) | spread3(qv[1]) << 1 | spread3(qv[2]) << 2)
+                       : (spread2(qv[0]) | spread2(qv[1]) << 1);
+    ids[e] = static_cast<int32_t>(e);
+  }
+}
+
+__global__ void invert_perm(const int32_t* __restrict__ order, int64_t n, int32_t* __restrict__ rank) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    rank[order[t]] = static_cast<int32_t>(t);
+}
+
 __global__ void iota_rows(int64_t n_rows, int32_t* __restrict__ rows) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -424,7 +453,8 @@ __global__ void class_verify(int32_t* __restrict__ cls, int64_t n_rows, const in
 }
 
 // class item records: [steps][32] element ids of each item (incidence order)
-__global__ void fill_class_records(const int32_t* __restrict__ citem_class, const int32_t* __restrict__ citem_rows,
+__global__ void fill_class_records(const int32_t* __restrict__ erank, const int32_t* __restrict__ citem_class,
+                                   const int32_t* __restrict__ citem_rows,
                                    const int64_t* __restrict__ citem_rec, int64_t n_citems,
                                    const int32_t* __restrict__ cls_steps, const int64_t* __restrict__ inc_ptr,
                                    const int32_t* __restrict__ inc, int k, int32_t* __restrict__ crec) {
@@ -436,12 +466,13 @@ __global__ void fill_class_records(const int32_t* __restrict__ citem_class, cons
     const int n = cls_steps[citem_class[w]];
     const int64_t base = citem_rec[w] * 32 + lane;
     const int64_t p = row >= 0 ? inc_ptr[row] : 0;
-    for (int q = 0; q < n; ++q) crec[base + q * 32] = row >= 0 ? inc[p + q] / k : -1;
+    for (int q = 0; q < n; ++q) crec[base + q * 32] = row >= 0 ? erank[inc[p + q] / k] : -1;
   }
 }
 
 template <int K>
-__global__ void fill_records(const int32_t* __restrict__ warp_rows, const int32_t* __restrict__ warp_steps,
+__global__ void fill_records(const int32_t* __restrict__ erank, const int32_t* __restrict__ warp_rows,
+                             const int32_t* __restrict__ warp_steps,
                              const int64_t* __restrict__ warp_rec, int64_t n_items, const int64_t* __restrict__ inc_ptr,
                              const int32_t* __restrict__ inc, const uint8_t* __restrict__ slots, void* __restrict__ rec) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_items * 32;
@@ -458,7 +489,7 @@ __global__ void fill_records(const int32_t* __restrict__ warp_rows, const int32_
         uint32_t word[4] = {0xffffffffu, 0u, 0u, 0u};
         if (p < pe && inc[p] % K == i) {
           const int32_t x = inc[p++];
-          word[0] = static_cast<uint32_t>(x / K);
+          word[0] = static_cast<uint32_t>(erank[x / K]);
           const uint8_t* sl = slots + static_cast<int64_t>(x) * K;
           for (int j = 0; j < K; ++j) word[1 + j / 4] |= static_cast<uint32_t>(sl[j]) << (8 * (j & 3));
         }
@@ -614,7 +645,8 @@ cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
-                              cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes) {
+                              cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes,
+                              bool use_eorder) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   const int cap = sm_count * 16;
@@ -683,6 +715,37 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     dof_morton<<<grid_for(nk, cap), kThreads, 0, s>>>(d_coords, d_vconn, d_dconn, ne, k, dim, rb, n_rows, bbox[0],
                                                      bbox[1], bbox[2], sc[0], sc[1], sc[2], keys);
     iota_rows<<<grid_for(n_rows, cap), kThreads, 0, s>>>(n_rows, rows);
+  }
+  // element order of the gather's per-element records (K2a writes record t
+  // for element eorder[t]): Morton order of the element centroids, or the
+  // identity when use_eorder is false
+  if ((err = cudaMalloc(&out->eorder, std::max<int64_t>(ne, 1) * sizeof(int32_t))) != cudaSuccess) return done(err);
+  if ((err = cudaMalloc(&out->erank, std::max<int64_t>(ne, 1) * sizeof(int32_t))) != cudaSuccess) return done(err);
+  if (ne > 0) {
+    uint64_t *ek = nullptr, *ek2 = nullptr;
+    int32_t* eid = nullptr;
+    if ((err = cudaMalloc(&ek, ne * sizeof(uint64_t))) != cudaSuccess) return done(err);
+    if ((err = cudaMalloc(&ek2, ne * sizeof(uint64_t))) != cudaSuccess) return cudaFree(ek), done(err);
+    if ((err = cudaMalloc(&eid, ne * sizeof(int32_t))) != cudaSuccess) return cudaFree(ek), cudaFree(ek2), done(err);
+    double sc[3] = {0.0, 0.0, 0.0};
+    const double qmax = dim == 3 ? 2097151.0 : 2147483647.0;
+    for (int c = 0; c < dim; ++c) {
+      const double ext = bbox[3 + c] - bbox[c];
+      sc[c] = ext > 0 ? qmax / ext : 0.0;
+    }
+    elem_morton<<<grid_for(ne, cap), kThreads, 0, s>>>(d_coords, d_vconn, ne, dim, bbox[0], bbox[1], bbox[2], sc[0],
+                                                      sc[1], sc[2], ek, eid);
+    if (!use_eorder) cudaMemsetAsync(ek, 0, ne * sizeof(uint64_t), s);  // stable sort of equal keys: identity
+    size_t te = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, te, ek, ek2, eid, out->eorder, ne, 0, 64, s);
+    if ((err = need_temp(te)) != cudaSuccess) return cudaFree(ek), cudaFree(ek2), cudaFree(eid), done(err);
+    err = cub::DeviceRadixSort::SortPairs(temp, te, ek, ek2, eid, out->eorder, ne, 0, 64, s);
+    if (err == cudaSuccess) invert_perm<<<grid_for(ne, cap), kThreads, 0, s>>>(out->eorder, ne, out->erank);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+    cudaFree(ek);
+    cudaFree(ek2);
+    cudaFree(eid);
+    if (err != cudaSuccess) return done(err);
   }
   tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, order, n_rows, 0, 64, s);
@@ -833,7 +896,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       cudaMemcpyAsync(out->citem_rows, ir.data(), nci * 32 * sizeof(int32_t), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(out->citem_rec, irec.data(), (nci + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(d_steps, cls_steps.data(), cls_steps.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-      fill_class_records<<<grid_for(nci * 32, cap), kThreads, 0, s>>>(out->citem_class, out->citem_rows,
+      fill_class_records<<<grid_for(nci * 32, cap), kThreads, 0, s>>>(out->erank, out->citem_class, out->citem_rows,
                                                                       out->citem_rec, nci, d_steps, inc_ptr, inc, k,
                                                                       out->crec);
       err = cudaStreamSynchronize(s);
@@ -908,7 +971,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     const int g = grid_for(n_items * 32, cap);
     switch (k) {
 #define FF_FILL(K) \
-  case K: fill_records<K><<<g, kThreads, 0, s>>>(out->warp_rows, out->warp_steps, out->warp_rec, n_items, inc_ptr, inc, d_slots, out->rec); break;
+  case K: fill_records<K><<<g, kThreads, 0, s>>>(out->erank, out->warp_rows, out->warp_steps, out->warp_rec, n_items, inc_ptr, inc, d_slots, out->rec); break;
       FF_FILL(1) FF_FILL(2) FF_FILL(3) FF_FILL(4) FF_FILL(5) FF_FILL(6) FF_FILL(7) FF_FILL(8) FF_FILL(9) FF_FILL(10)
       FF_FILL(11) FF_FILL(12)
 #undef FF_FILL
@@ -926,6 +989,8 @@ cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_ou
 }
 
 void free_gather_plan(GatherPlan* p) {
+  cudaFree(p->eorder);
+  cudaFree(p->erank);
   cudaFree(p->citem_class);
   cudaFree(p->citem_rows);
   cudaFree(p->citem_rec);
