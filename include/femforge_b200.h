@@ -147,6 +147,9 @@ typedef struct ff_gather_info {
   double build_ms;
   int n_classes;                            /* row classes with a specialised kernel */
   int64_t n_class_rows, n_class_items;
+  int64_t n_windows;                        /* window plan (0: none): windows of window_rows rows, */
+  int window_rows;                          /* each with <= window_max_elems elements in shared memory */
+  int64_t window_max_elems, n_window_items;
 } ff_gather_info;
 /* Row classes of the gather plan: rows with identical incidence sequences
  * get an NVRTC kernel specialised to the class (slots as compile-time
@@ -158,6 +161,10 @@ int ff_ctx_set_gather_classes(ff_ctx* ctx, int64_t min_rows);
  * the concatenated per-step local indices and [steps][n_local] slot bytes. */
 int ff_class_source(const ff_form* form, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
+/* Same classes -> the window row-gather translation unit (form source +
+ * ff_gather_windows). */
+int ff_window_source(const ff_form* form, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
+                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
 int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* mesh, ff_gather_info* out);
 /* Which scatter the next assembly of (form, pattern) runs: FF_SCATTER_*_MODE. */
 int ff_scatter_selected(const ff_form* form, const ff_pattern* p, unsigned flags, int* mode);

@@ -208,11 +208,52 @@ void free_class_module(ff_pattern* p) {
   p->class_key.clear();
 }
 
+void free_window_module(ff_pattern* p) {
+  if (p->window_lib) cudaLibraryUnload(p->window_lib);
+  p->window_lib = nullptr;
+  p->window_kernel = nullptr;
+  p->window_key.clear();
+}
+
+// shared-memory budget of the window kernel: 2 CTAs per SM
+constexpr int kWindowMaxElems = 540;
+int window_es(const ff_form* f) { return ((f->plan.n_kinv + f->n_local + 1) & ~1) + 2; }  // FF_ES
+
 void free_gather(ff_pattern* p) {
   ffb::kernels::free_gather_plan(&p->gather);
   p->gather_generation = ~0ull;
   p->gather_mesh = nullptr;
   free_class_module(p);
+  free_window_module(p);
+}
+
+// NVRTC-compiles the window row-gather kernel of (form, plan).
+void ensure_window_module(ff_form* f, ff_pattern* p) {
+  const std::string key = f->source[1] + "#w" + std::to_string(p->gather_generation) + "#" +
+                          std::to_string(reinterpret_cast<std::uintptr_t>(p->gather.wrec16));
+  if (p->window_key == key && p->window_lib) return;
+  free_window_module(p);
+  std::vector<codegen::RowClass> rc;
+  for (const auto& c : p->gather.classes) {
+    codegen::RowClass r;
+    r.len = c.len;
+    r.steps = c.steps;
+    r.local = c.local;
+    r.slots = c.slots;
+    rc.push_back(std::move(r));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::string src = codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc);
+  const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_windows.cu");
+  bind(p->ctx);
+  ffb::cuda_check(cudaLibraryLoadData(&p->window_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
+                  "cudaLibraryLoadData (windows)");
+  ffb::cuda_check(cudaLibraryGetKernel(&p->window_kernel, p->window_lib, "ff_gather_windows"), "window kernel");
+  ffb::cuda_check(cudaKernelSetAttributeForDevice(p->window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kWindowMaxElems * window_es(f) * 8, p->ctx->device),
+                  "window kernel shared memory attribute");
+  p->class_compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  p->window_key = key;
 }
 
 // NVRTC-compiles the class-specialised gather kernels of (form, plan).
@@ -279,7 +320,8 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         4096, ctx->sm_count, ctx->stream, &p->gather,
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
-                                                        cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"));
+                                                        cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
+                                                        std::getenv("FF_NO_WINDOWS") ? 0 : kWindowMaxElems);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
@@ -308,6 +350,39 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
                    unsigned flags, int w) {
   ff_ctx* ctx = f->ctx;
   ensure_gather_plan(p, m);
+  unsigned long long* wstatus = ctx->d_status;
+  if (p->gather.n_win > 0 && window_es(f) * 8 * p->gather.win_max_elems <= kWindowMaxElems * window_es(f) * 8) {
+    // window row gather: element records computed in shared memory per window
+    if (flags & FF_GATHER_INVARIANTS_ONLY) {
+      ffb::cuda_check(cudaMemsetAsync(wstatus, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
+      return;
+    }
+    if (!(flags & FF_GATHER_ROWS_ONLY))
+      ffb::cuda_check(cudaMemsetAsync(wstatus, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
+    ensure_window_module(f, p);
+    const ffb::kernels::GatherPlan& gp = p->gather;
+    const double* coords = m->coords;
+    const int32_t* vconn = m->vconn;
+    const int32_t* dconn = m->dconn;
+    const int64_t* weptr = gp.win_eptr;
+    const int32_t* welem = gp.win_elem;
+    const int32_t* wiptr = gp.win_iptr;
+    const int32_t* irows = gp.witem_rows;
+    const int32_t* icls = gp.witem_class;
+    const int32_t* isteps = gp.witem_steps;
+    const int64_t* irec = gp.witem_rec;
+    const int64_t* igoff = gp.witem_goff;
+    const uint16_t* rec16 = gp.wrec16;
+    const uint8_t* gsl = gp.gslot;
+    const int64_t* row_ptr = p->row_ptr;
+    void* args[] = {&coords, &vconn, &dconn, &weptr, &welem, &wiptr, &irows, &icls, &isteps, &irec, &igoff,
+                    &rec16, &gsl, &row_ptr, &d_values, &d_rhs, &wstatus};
+    const int smem = static_cast<int>(gp.win_max_elems) * window_es(f) * 8;
+    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->window_kernel), dim3(static_cast<unsigned>(gp.n_win)),
+                                     dim3(128), args, smem, s),
+                    "K2 (window row gather) launch");
+    return;
+  }
   const int erec = (f->plan.n_kinv + m->k + 1) & ~1;  // FF_EREC
   const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * erec;
   if (p->ginv_cap < ng) {
@@ -520,8 +595,21 @@ int ff_ctx_set_gather_classes(ff_ctx* ctx, int64_t min_rows) {
   });
 }
 
+int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* len, const int32_t* steps,
+                           const int32_t* local, const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
+
 int ff_class_source(const ff_form* f, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {
+  return class_or_window_source(false, f, n, len, steps, local, slots, buf, cap, out_len);
+}
+
+int ff_window_source(const ff_form* f, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
+                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {
+  return class_or_window_source(true, f, n, len, steps, local, slots, buf, cap, out_len);
+}
+
+int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* len, const int32_t* steps,
+                           const int32_t* local, const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {
   return guarded([&] {
     require(f && n >= 0 && (n == 0 || (len && steps && local && slots)), "null argument");
     require(f->plan.n_kinv > 0, "form has no reference-tensor plan (no row gather)");
@@ -536,7 +624,8 @@ int ff_class_source(const ff_form* f, int n, const int32_t* len, const int32_t* 
       }
       at += steps[c];
     }
-    std::string src = codegen::emit_class_source(f->plan, f->n_local, rc);
+    const std::string src = window ? codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc)
+                                   : codegen::emit_class_source(f->plan, f->n_local, rc);
     if (out_len) *out_len = src.size();
     if (buf && cap) {
       const std::size_t k = std::min(cap - 1, src.size());
@@ -813,6 +902,10 @@ int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* m, ff_gather_info* out)
     out->n_classes = static_cast<int>(p->gather.classes.size());
     out->n_class_rows = p->gather.n_class_rows;
     out->n_class_items = p->gather.n_citems;
+    out->n_windows = p->gather.n_win;
+    out->window_rows = p->gather.win_rows;
+    out->window_max_elems = p->gather.win_max_elems;
+    out->n_window_items = p->gather.n_witems;
   });
 }
 

@@ -163,6 +163,11 @@ struct RowClass {
 // plan (plan.n_kinv > 0). Byte-deterministic.
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes);
 
+// The window row-gather kernel (ff_gather_windows) appended to the form's own
+// translation unit (it reuses the form's geometry and element body).
+std::string emit_window_source(const std::string& form_source, const ElementPlan& plan, int n_local,
+                               const std::vector<RowClass>& classes);
+
 // Shortest round-trip double literal valid in C/CUDA source.
 std::string double_literal(double v);
 

@@ -110,6 +110,10 @@ struct ff_pattern {
   std::string class_key;
   cudaLibrary_t class_lib = nullptr;
   cudaKernel_t class_kernel[2] = {nullptr, nullptr};  // short rows, long rows
+  // window row-gather kernel for (form source, plan)
+  std::string window_key;
+  cudaLibrary_t window_lib = nullptr;
+  cudaKernel_t window_kernel = nullptr;
   double class_compile_ms = 0.0;
   double* ginv = nullptr;   // [ne][nkp]
   double* bvec = nullptr;   // [ne][k]

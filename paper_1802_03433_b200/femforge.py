@@ -74,7 +74,8 @@ class FormInfo(C.Structure):
 class GatherInfo(C.Structure):
     _fields_ = [("n_items", C.c_int64), ("n_steps", C.c_int64), ("n_incidences", C.c_int64),
                 ("record_bytes", C.c_int), ("build_ms", C.c_double), ("n_classes", C.c_int),
-                ("n_class_rows", C.c_int64), ("n_class_items", C.c_int64)]
+                ("n_class_rows", C.c_int64), ("n_class_items", C.c_int64), ("n_windows", C.c_int64),
+                ("window_rows", C.c_int), ("window_max_elems", C.c_int64), ("n_window_items", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -102,6 +103,7 @@ SIGNATURES = [
     ("ff_ctx_set_scatter", C.c_int, [_P, C.c_int]),
     ("ff_ctx_set_gather_classes", C.c_int, [_P, _i64]),
     ("ff_class_source", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("ff_window_source", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_form_create", C.c_int, [_P, C.POINTER(_FormDesc), C.POINTER(_P)]),
     ("ff_compile", C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P), C.c_char_p, C.c_size_t]),
     ("ff_form_source", C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
@@ -248,17 +250,19 @@ class Form:
         _ok(lib().ff_form_info_get(self.h, C.byref(i)))
         return i.as_dict()
 
-    def class_source(self, classes):
-        """Specialised gather source for classes [(len, [local i], [[slot bytes]])]."""
+    def class_source(self, classes, window=False):
+        """Specialised gather source for classes [(len, [local i], [[slot bytes]])]
+        (window=True: the window row-gather translation unit)."""
         n = len(classes)
         ln = np.array([c[0] for c in classes], np.int32)
         st = np.array([len(c[1]) for c in classes], np.int32)
         lo = np.ascontiguousarray(np.concatenate([np.asarray(c[1], np.int32) for c in classes]) if n else np.zeros(1, np.int32))
         sl = np.ascontiguousarray(np.concatenate([np.asarray(c[2], np.uint8).ravel() for c in classes]) if n else np.zeros(1, np.uint8))
         m = C.c_size_t(0)
-        _ok(lib().ff_class_source(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), None, 0, C.byref(m)))
+        fn = lib().ff_window_source if window else lib().ff_class_source
+        _ok(fn(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), None, 0, C.byref(m)))
         buf = C.create_string_buffer(m.value + 1)
-        _ok(lib().ff_class_source(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), buf, m.value + 1, C.byref(m)))
+        _ok(fn(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), buf, m.value + 1, C.byref(m)))
         return buf.value.decode()
 
     def close(self):
