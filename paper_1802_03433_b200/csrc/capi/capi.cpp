@@ -215,8 +215,13 @@ void free_window_module(ff_pattern* p) {
   p->window_key.clear();
 }
 
-// shared-memory budget of the window kernel: 2 CTAs per SM
-constexpr int kWindowMaxElems = 540;
+// shared-memory budget of the window kernel (element records of one window);
+// FF_WIN_ELEMS overrides (smaller windows, more CTAs per SM)
+int window_max_elems() {
+  const char* v = std::getenv("FF_WIN_ELEMS");
+  return v ? std::max(64, std::atoi(v)) : 280;
+}
+const int kWindowMaxElems = window_max_elems();
 int window_es(const ff_form* f) { return ((f->plan.n_kinv + f->n_local + 1) & ~1) + 2; }  // FF_ES
 
 void free_gather(ff_pattern* p) {
@@ -243,7 +248,9 @@ void ensure_window_module(ff_form* f, ff_pattern* p) {
     rc.push_back(std::move(r));
   }
   const auto t0 = std::chrono::steady_clock::now();
-  const std::string src = codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc);
+  std::string src = codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc);
+  if (const char* v = std::getenv("FF_WMINB"))  // tuning knob: register budget (CTAs per SM)
+    src = "#define FF_WMINB " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_windows.cu");
   bind(p->ctx);
   ffb::cuda_check(cudaLibraryLoadData(&p->window_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),

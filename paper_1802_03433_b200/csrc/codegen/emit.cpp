@@ -238,6 +238,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
 std::string emit_window_source(const std::string& form_source, const ElementPlan& plan, int n_local,
                                const std::vector<RowClass>& classes) {
   if (plan.n_kinv <= 0) throw CodegenError("windows need a reference-tensor plan");
+  constexpr int FF_WDEPTH_GEN = 3;  // element records in flight per step batch
   std::ostringstream os;
   os << form_source << R"(
 // ===========================================================================
@@ -249,8 +250,11 @@ std::string emit_window_source(const std::string& form_source, const ElementPlan
 // (zeroed) CSR row through their slot bytes. No atomics; each value written by
 // its row's lane.
 #define FF_ES (FF_EREC + 2)  // shared-memory stride of an element record (bank spread)
-#define FF_SP 33             // staging pitch (odd: conflict-free lane-row stores)
+#define FF_SP 17             // staging pitch (odd: conflict-free lane-row stores; 16-slot chunks)
 #define FF_WWARPS 4
+#ifndef FF_WMINB
+#define FF_WMINB 4           // CTAs per SM the register budget is sized for
+#endif
 
 __device__ __forceinline__ void ff_wload(int le, int i, const double* __restrict__ es, double (&g)[FF_NKP],
                                          double& b) {
@@ -271,15 +275,17 @@ __device__ __forceinline__ void ff_wload(int le, int i, const double* __restrict
   }
 }
 
-// staged rows -> CSR values (consecutive lanes = consecutive values of a row)
+// staged rows (<= 16 slots each) -> CSR values: half-warps take one row each,
+// consecutive lanes = consecutive values of a row
 __device__ __noinline__ void ff_wout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane, int cnt,
                                      int q0, double* __restrict__ values) {
   __syncwarp();
-  if (lane < cnt) {
+  const int h = lane >> 4, j = lane & 15;
+  if (j < cnt) {
 #pragma unroll 4
-    for (int m = 0; m < 32; ++m) {
+    for (int m = h; m < 32; m += 2) {
       const ff_i64 rb = sr[m];
-      if (rb >= 0) __stcs(values + rb + q0 + lane, st[m * FF_SP + lane]);
+      if (rb >= 0) __stcs(values + rb + q0 + j, st[m * FF_SP + j]);
     }
   }
   __syncwarp();
@@ -323,42 +329,55 @@ __device__ __noinline__ void ff_wgen(const unsigned short* __restrict__ rec, con
   if (row >= 0) __stcs(rhs + row, bs);
 }
 )";
+  // class rows live in registers; rows longer than FF_WPASS entries are
+  // accumulated in slot-range passes (each pass re-reads the element records
+  // from shared memory and computes only its entries) to bound registers
+  constexpr int kPass = 33;
   auto class_fn = [&](int c) {
     const RowClass& k = classes[c];
-    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
+    const int n_pass = std::max(1, (k.len + kPass - 1) / kPass);
+    const int per = (k.len + n_pass - 1) / n_pass;
+    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences, " << n_pass << " pass(es)\n"
        << "__device__ __forceinline__ void ff_wcls_" << c
        << "(const unsigned short* __restrict__ rec, const double* __restrict__ es, double* __restrict__ st,\n"
           "    ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row, double* __restrict__ values,\n"
           "    double* __restrict__ rhs) {\n"
-          "  int e[" << std::max(k.steps, 1) << "];\n";
-    for (int q = 0; q < k.steps; ++q) os << "  e[" << q << "] = rec[" << q * 32 << "];\n";
-    for (int p = 0; p < k.len; ++p) os << "  double a" << p << " = 0.0;\n";
-    os << "  double bs = 0.0;\n";
-    constexpr int depth = 4;
-    for (int s0 = 0; s0 < k.steps; s0 += depth) {
-      const int s1 = std::min(k.steps, s0 + depth);
-      os << "  {\n";
-      for (int q = s0; q < s1; ++q)
-        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_wload(e[" << q << "], " << k.local[q] << ", es, g" << q
-           << ", b" << q << ");\n";
-      for (int q = s0; q < s1; ++q) {
-        os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);";
-        for (int j = 0; j < n_local; ++j) os << " a" << int(k.slots[q * n_local + j]) << " += v[" << j << "];";
-        os << " bs += b" << q << "; }\n";
+          "  double bs = 0.0;\n"
+          "  sr[lane] = row >= 0 ? rbeg : -1;\n";
+    for (int ps = 0; ps < n_pass; ++ps) {
+      const int lo = ps * per, hi = std::min(k.len, lo + per);
+      os << "  {  // slots [" << lo << ", " << hi << ")\n";
+      for (int p = lo; p < hi; ++p) os << "    double a" << p << " = 0.0;\n";
+      for (int s0 = 0; s0 < k.steps; s0 += FF_WDEPTH_GEN) {
+        const int s1 = std::min(k.steps, s0 + FF_WDEPTH_GEN);
+        os << "    {\n";
+        for (int q = s0; q < s1; ++q)
+          os << "      double g" << q << "[FF_NKP], b" << q << "; ff_wload(rec[" << q * 32 << "], " << k.local[q]
+             << ", es, g" << q << ", b" << q << ");\n";
+        for (int q = s0; q < s1; ++q) {
+          std::string adds;
+          for (int j = 0; j < n_local; ++j) {
+            const int sl = k.slots[q * n_local + j];
+            if (sl >= lo && sl < hi) adds += " a" + std::to_string(sl) + " += v[" + std::to_string(j) + "];";
+          }
+          if (!adds.empty())
+            os << "      { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);" << adds << " }\n";
+          if (ps == 0) os << "      bs += b" << q << ";\n";
+        }
+        os << "    }\n";
+      }
+      for (int q0 = lo; q0 < hi; q0 += 16) {
+        const int cnt = std::min(16, hi - q0);
+        for (int j = 0; j < cnt; ++j) os << "    st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
+        os << "    ff_wout(st, sr, lane, " << cnt << ", " << q0 << ", values);\n";
       }
       os << "  }\n";
-    }
-    os << "  sr[lane] = row >= 0 ? rbeg : -1;\n";
-    for (int q0 = 0; q0 < k.len; q0 += 32) {
-      const int cnt = std::min(32, k.len - q0);
-      for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
-      os << "  ff_wout(st, sr, lane, " << cnt << ", " << q0 << ", values);\n";
     }
     os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
   };
   for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
   os << R"(
-extern "C" __global__ void __launch_bounds__(FF_WWARPS * 32, 2)
+extern "C" __global__ void __launch_bounds__(FF_WWARPS * 32, FF_WMINB)
 ff_gather_windows(const double* __restrict__ coords, const ff_i32* __restrict__ vconn, const ff_i32* __restrict__ dconn,
                   const ff_i64* __restrict__ win_eptr, const ff_i32* __restrict__ win_elem,
                   const ff_i32* __restrict__ win_iptr, const ff_i32* __restrict__ witem_rows,
@@ -370,7 +389,9 @@ ff_gather_windows(const double* __restrict__ coords, const ff_i32* __restrict__ 
   extern __shared__ __align__(16) double ff_es[];
   __shared__ double stage[FF_WWARPS][32 * FF_SP];
   __shared__ ff_i64 srow[FF_WWARPS][32];
+  __shared__ int next_item;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) next_item = win_iptr[blockIdx.x] + FF_WWARPS;
   const ff_i64 eb = win_eptr[blockIdx.x];
   const int nwe = (int)(win_eptr[blockIdx.x + 1] - eb);
   // ---- phase 1: element records of the window (halo elements included)
@@ -415,7 +436,9 @@ ff_gather_windows(const double* __restrict__ coords, const ff_i32* __restrict__ 
   // ---- phase 2: the window's items, one warp per item
   double* st = stage[wid];
   ff_i64* sr = srow[wid];
-  for (int it = win_iptr[blockIdx.x] + wid; it < win_iptr[blockIdx.x + 1]; it += FF_WWARPS) {
+  // items are taken dynamically (their costs differ by class)
+  const int it_end = win_iptr[blockIdx.x + 1];
+  for (int it = win_iptr[blockIdx.x] + wid; it < it_end;) {
     const int c = __ldg(witem_class + it);
     const int row = __ldg(witem_rows + (ff_i64)it * 32 + lane);
     ff_i64 rbeg = 0;
@@ -434,6 +457,9 @@ ff_gather_windows(const double* __restrict__ coords, const ff_i32* __restrict__ 
                 lane, rbeg, len, row, values, rhs);
         break;
     }
+    int nx = 0;
+    if (lane == 0) nx = atomicAdd(&next_item, 1);
+    it = __shfl_sync(0xffffffffu, nx, 0);
   }
 }
 )";
