@@ -328,7 +328,7 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
-                                                        std::getenv("FF_NO_WINDOWS") ? 0 : kWindowMaxElems);
+                                                        std::getenv("FF_WINDOWS") ? kWindowMaxElems : 0);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
@@ -421,7 +421,16 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   if (gp.n_citems > 0) {
     ensure_class_module(f, p);
     const int64_t cr[2][2] = {{0, gp.n_citems_short}, {gp.n_citems_short, gp.n_citems}};
-    for (int c = 0; c < 2; ++c) {
+    // the long-row kernel runs on the context's side stream, concurrently with
+    // the short-row one (disjoint rows): the two register budgets share the SMs
+    // and the element records they both read stay in L2
+    const bool both = gp.n_citems_short > 0 && gp.n_citems > gp.n_citems_short && !std::getenv("FF_SERIAL_CLASSES");
+    if (both) {
+      ffb::cuda_check(cudaEventRecord(ctx->fork, s), "fork");
+      ffb::cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
+    }
+    for (int c = 1; c >= 0; --c) {
+      cudaStream_t sc = (both && c == 1) ? ctx->side : s;
       long long i0 = cr[c][0], i1 = cr[c][1];
       if (i1 <= i0) continue;
       const char* ipw_env = std::getenv("FF_IPW");
@@ -435,8 +444,12 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       const int32_t* crec = gp.crec;
       void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(128), args,
-                                       0, s),
+                                       0, sc),
                       "K2b (class row gather) launch");
+    }
+    if (both) {
+      ffb::cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
+      ffb::cuda_check(cudaStreamWaitEvent(s, ctx->join, 0), "join");
     }
   }
   // K2b for the remaining rows in two launches: short-pitch items, then long-pitch items
@@ -557,6 +570,9 @@ int ff_init(int device, ff_ctx** out) {
     ffb::cuda_check(cudaSetDevice(device), "cudaSetDevice");
     ffb::cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attribute");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ffb::cuda_check(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    ffb::cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
+    ffb::cuda_check(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming), "cudaEventCreate");
     c->d_status = device_alloc<unsigned long long>(3, "status");  // [bad_elem, bad_row, scratch]
     ffb::cuda_check(cudaMallocHost(&c->h_status, 2 * sizeof(unsigned long long)), "cudaMallocHost");
     ffb::cuda_check(cudaMemset(c->d_status, 0xff, 2 * sizeof(unsigned long long)), "memset");
@@ -571,6 +587,10 @@ int ff_ctx_destroy(ff_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
+    cudaStreamSynchronize(ctx->side);
+    cudaEventDestroy(ctx->fork);
+    cudaEventDestroy(ctx->join);
+    cudaStreamDestroy(ctx->side);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });

@@ -324,3 +324,27 @@ def test_class_specialised_gather_equals_generic(ff, ctx, dim, deg, n, form):
     orp, oci = po.build_pattern(d, nd)
     ov, ob = po.assemble(form, dim, deg, quad, c, v, d, orp, oci, workers=8)
     assert normwise(v1, ov) <= TOL and normwise(b1, ob) <= TOL
+
+
+@pytest.mark.parametrize("dim,deg,n,form", [(3, 2, 8, "poisson"), (2, 1, 48, "demo2d")])
+def test_window_gather_matches_oracle(ff, ctx, dim, deg, n, form, monkeypatch):
+    """Opt-in window row gather (FF_WINDOWS=1: element records computed per
+    window in shared memory) against the oracle."""
+    monkeypatch.setenv("FF_WINDOWS", "1")
+    c, v, d, nd = _mesh(ff, dim, deg, n)
+    ctx.set_scatter("gather")
+    quad = 4 if dim == 3 else 3
+    b, l = ff.named_form(form, dim)
+    f = ff.Form(ctx, dim, deg, b, l, quad_rule=quad)
+    m = ff.Mesh(ctx, dim, c, v, None if deg == 1 else d, nd)
+    p = ff.Pattern(ctx, m)
+    ctx.set_gather_classes(16)
+    try:
+        gi = p.gather_info(m)
+        assert gi["n_windows"] > 0 and gi["n_window_items"] * 32 >= nd
+        val, rhs = ff.assemble(f, m, p)
+    finally:
+        ctx.set_gather_classes(128)
+    orp, oci = po.build_pattern(d, nd)
+    ov, ob = po.assemble(form, dim, deg, quad, c, v, d, orp, oci, workers=8)
+    assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
