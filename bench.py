@@ -41,12 +41,13 @@ METRIC = "assembled elements/sec (3D P2 Poisson tets)"
 STEP_DESC = {
     "atomic": "K0 zero-fill + K2 element kernel with fp64-RED scatter",
     "rowtile": "K2 row-tile element kernel (atomic-free, each CSR value written once)",
-    "gather": "K2a element invariants + K2b row gather (atomic-free, each CSR value written once, no zero-fill)",
+    "gather": "K2a element invariants + K2b row gather (class-specialised + generic; atomic-free, each CSR value "
+              "written once, no zero-fill)",
 }
 KERNEL_DESC = {
     "atomic": "ff_assemble_atomic (K2)",
     "rowtile": "ff_assemble_rowtile (K2)",
-    "gather": "ff_gather_invariants + ff_gather_rows (K2a+K2b, the whole step)",
+    "gather": "ff_gather_invariants + ff_gather_classes_s/_l + ff_gather_rows (K2a + K2b, the whole step)",
 }
 UNIT = "elements/s"
 
