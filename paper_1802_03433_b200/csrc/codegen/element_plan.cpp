@@ -442,19 +442,14 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
 // Pointwise
 
 ElementPlan plan_pointwise(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
-  const Expr ref[3] = {fem::arg_xi(), fem::arg_eta(), fem::arg_zeta()};
+  // A runtime quadrature loop per block of kRows element rows: the block's
+  // integrands are lowered once with the reference coordinates as symbols
+  // (CSE inside the block), evaluated at every point in ascending order, and
+  // w_q * f_q is added to the block's accumulators (device.cpp:176-192 order).
+  // Code size and the live set stay one block of accumulators plus one
+  // point's subexpressions.
   std::vector<Expr> integrands = f.geo_bilinear;
   integrands.insert(integrands.end(), f.geo_linear.begin(), f.geo_linear.end());
-  std::vector<Expr> sums;
-  for (const Expr& e : integrands) {
-    std::vector<Expr> terms;
-    for (int q = 0; q < rule.size(); ++q) {
-      std::vector<std::pair<Expr, Expr>> b;
-      for (int c = 0; c < f.dim; ++c) b.push_back({ref[c], constant(rule.points[q][c])});
-      terms.push_back(constant(rule.weights[q]) * substitute(e, b));
-    }
-    sums.push_back(add(terms));
-  }
   SymbolTable args;
   const fem::GeometrySymbols& g = fem::geometry_symbols();
   for (int r = 0; r < 3; ++r)
@@ -464,37 +459,70 @@ ElementPlan plan_pointwise(const fem::InstantiatedForm& f, const fem::Quadrature
     }
   for (int r = 0; r < 3; ++r) args.add(g.X[r].name());
   args.add(g.det.name());
-  MultiProgram p = lower_many(sums, args);
+  const char* refname[3] = {"xi", "eta", "zeta"};
+  for (int c = 0; c < f.dim; ++c) args.add(refname[c]);
+  const int n = f.n_local;
+  const int nq = rule.size();
+  const int kRows = 2;
   ElementPlan plan;
   plan.strategy = Strategy::Pointwise;
+  {
+    std::ostringstream pre;
+    pre << "__constant__ double ff_qp[" << nq << "][3] = { ";
+    for (int q = 0; q < nq; ++q)
+      pre << (q ? ", " : "") << "{" << double_literal(rule.points[q][0]) << ", " << double_literal(rule.points[q][1])
+          << ", " << double_literal(f.dim == 3 ? rule.points[q][2] : 0.0) << "}";
+    pre << "};\n__constant__ double ff_qw[" << nq << "] = {";
+    for (int q = 0; q < nq; ++q) pre << (q ? ", " : "") << double_literal(rule.weights[q]);
+    pre << "};\n";
+    plan.prelude = pre.str();
+  }
   std::ostringstream os;
   std::int64_t flops = 0;
-  for (std::size_t k = 0; k < p.code.size(); ++k) {
-    const Instr& in = p.code[k];
-    auto r = [](int i) { return "ff_r" + std::to_string(i); };
-    std::string rhs;
-    switch (in.op) {
-      case Op::LoadArg: rhs = p.arg_names[in.imm]; break;
-      case Op::LoadConst: rhs = double_literal(p.consts[in.imm]); break;
-      case Op::Add: rhs = r(in.a) + " + " + r(in.b); ++flops; break;
-      case Op::Sub: rhs = r(in.a) + " - " + r(in.b); ++flops; break;
-      case Op::Mul: rhs = r(in.a) + " * " + r(in.b); ++flops; break;
-      case Op::Div: rhs = r(in.a) + " / " + r(in.b); flops += 4; break;
-      case Op::Neg: rhs = "-" + r(in.a); break;
-      case Op::PowInt: rhs = "ff_powi(" + r(in.a) + ", " + std::to_string(in.imm) + ")"; flops += 8; break;
-      case Op::Sin: rhs = "sin(" + r(in.a) + ")"; flops += 20; break;
-      case Op::Cos: rhs = "cos(" + r(in.a) + ")"; flops += 20; break;
-      case Op::Sqrt: rhs = "sqrt(" + r(in.a) + ")"; flops += 4; break;
+  const std::vector<Entry> entries = entry_list(n);
+  for (int i0 = 0; i0 < n; i0 += kRows) {
+    const int i1 = std::min(n, i0 + kRows);
+    std::vector<int> members;
+    for (int i = i0; i < i1; ++i)
+      for (int j = 0; j < n; ++j) members.push_back(i * n + j);
+    for (int i = i0; i < i1; ++i) members.push_back(n * n + i);
+    std::vector<Expr> sub;
+    for (int r : members) sub.push_back(integrands[r]);
+    MultiProgram p = lower_many(sub, args);
+    auto r = [](int k) { return "ff_r" + std::to_string(k); };
+    os << "  {  // element rows [" << i0 << ", " << i1 << ")\n";
+    for (std::size_t m = 0; m < members.size(); ++m) os << "    double ff_acc" << m << " = 0.0;\n";
+    os << "#pragma unroll 1\n    for (int ff_q = 0; ff_q < " << nq << "; ++ff_q) {\n";
+    for (int c = 0; c < f.dim; ++c) os << "      const double " << refname[c] << " = ff_qp[ff_q][" << c << "];\n";
+    os << "      const double ff_w = ff_qw[ff_q];\n";
+    std::int64_t per_q = 0;
+    for (std::size_t k = 0; k < p.code.size(); ++k) {
+      const Instr& in = p.code[k];
+      std::string rhs;
+      switch (in.op) {
+        case Op::LoadArg: rhs = p.arg_names[in.imm]; break;
+        case Op::LoadConst: rhs = double_literal(p.consts[in.imm]); break;
+        case Op::Add: rhs = r(in.a) + " + " + r(in.b); ++per_q; break;
+        case Op::Sub: rhs = r(in.a) + " - " + r(in.b); ++per_q; break;
+        case Op::Mul: rhs = r(in.a) + " * " + r(in.b); ++per_q; break;
+        case Op::Div: rhs = r(in.a) + " / " + r(in.b); per_q += 4; break;
+        case Op::Neg: rhs = "-" + r(in.a); break;
+        case Op::PowInt: rhs = "ff_powi(" + r(in.a) + ", " + std::to_string(in.imm) + ")"; per_q += 8; break;
+        case Op::Sin: rhs = "sin(" + r(in.a) + ")"; per_q += 20; break;
+        case Op::Cos: rhs = "cos(" + r(in.a) + ")"; per_q += 20; break;
+        case Op::Sqrt: rhs = "sqrt(" + r(in.a) + ")"; per_q += 4; break;
+      }
+      os << "      const double " << r(static_cast<int>(k)) << " = " << rhs << ";\n";
     }
-    os << "  const double ff_r" << k << " = " << rhs << ";\n";
+    for (std::size_t m = 0; m < members.size(); ++m) os << "      ff_acc" << m << " += ff_w * " << r(p.results[m]) << ";\n";
+    per_q += 2 * static_cast<std::int64_t>(members.size());
+    flops += per_q * nq;
+    os << "    }\n";
+    for (std::size_t m = 0; m < members.size(); ++m)
+      os << "    " << emit_call(entries[members[m]], "ff_acc" + std::to_string(m)) << "\n";
+    os << "  }\n";
   }
-  const std::vector<Entry> entries = entry_list(f.n_local);
-  std::set<int> distinct;
-  for (std::size_t r = 0; r < entries.size(); ++r) {
-    os << "  " << emit_call(entries[r], "ff_r" + std::to_string(p.results[r])) << "\n";
-    distinct.insert(p.results[r]);
-  }
-  plan.n_unique_entries = static_cast<int>(distinct.size());
+  plan.n_unique_entries = static_cast<int>(entries.size());
   plan.flops = flops;
   plan.body = os.str();
   return plan;
@@ -516,10 +544,13 @@ ElementPlan plan_element(const fem::InstantiatedForm& f, const fem::QuadratureRu
       if (strategy == Strategy::ReferenceTensor)
         throw CodegenError("integrand is not polynomial in the reference coordinates; use the pointwise strategy");
       plan = plan_pointwise(f, rule);
-    } else if (strategy == Strategy::Auto && t->flops > 4000) {
-      // large tensor expansions (e.g. high-degree coefficients): keep the cheaper
+    } else if (strategy == Strategy::Auto && (t->flops > 4000 || t->n_invariants > 48)) {
+      // large tensor expansions (e.g. variable coefficients): every invariant
+      // is live at once, so beyond ~48 of them the body spills; the pointwise
+      // quadrature loop keeps one point live. Keep the tensor form only when it
+      // is both small enough for registers and cheaper.
       ElementPlan p = plan_pointwise(f, rule);
-      plan = p.flops < t->flops ? p : *t;
+      plan = (t->n_invariants <= 48 && t->flops < p.flops) ? *t : p;
     } else {
       plan = *t;
     }

@@ -72,6 +72,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
                      " strategy, " + std::to_string(plan.n_quad) + "-point rule " + std::to_string(rule_id) + ", ~" +
                      std::to_string(plan.flops) + " flops\n" + plan.body;
   fill(text, "ELEMENT_BODY", body);
+  fill(text, "ELEMENT_PRELUDE", plan.prelude);
   // the row gather needs a reference-tensor plan and <= 12 slot bytes per record
   const bool gather = plan.n_kinv > 0 && f.n_local <= 12 && plan.n_kinv + f.n_local <= 24;
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));

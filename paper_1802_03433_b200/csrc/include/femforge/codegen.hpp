@@ -95,6 +95,7 @@ struct ElementPlan {
   int n_quad = 3;
   Strategy strategy = Strategy::ReferenceTensor;
   std::string body;        // CUDA statements; emits FF_EMIT_A(i,j,v) / FF_EMIT_B(i,v)
+  std::string prelude;     // namespace-scope declarations the body uses (quadrature tables)
   int n_invariants = 0;    // ReferenceTensor: merged geometric invariants
   int n_unique_entries = 0;
   std::int64_t flops = 0;  // fp64 operations per element after CSE (estimate)
