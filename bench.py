@@ -71,6 +71,21 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+FP64_PEAK_TFLOPS = 37.0   # nominal HGX B200 fp64
+
+
+def model_flops(cfg):
+    """SURVEY.md §8d flop model per element: geometry 60; per quadrature point
+    n_local*15 (basis gradients) + entries * (7 stiffness | +3 mass | +7
+    convection) + load 25 + 2 n_local. Reference-tensor forms (quadrature
+    summed at compile time) are quoted with their symmetric count."""
+    k = {(2, 1): 3, (2, 2): 6, (3, 1): 4, (3, 2): 10}[(cfg["dim"], cfg["degree"])]
+    nq = {1: 1, 3: 3, 4: 4, 11: 11, 14: 14}.get(cfg["quad"], cfg["quad"])
+    per_entry = {"poisson": 7, "stiffness": 7, "mass": 3, "helmholtz": 10, "demo2d": 10, "varcoef": 17}[cfg["form"]]
+    entries = k * (k + 1) // 2 if cfg["form"] != "varcoef" else k * k
+    return 60 + nq * (k * 15 + entries * per_entry + 25 + 2 * k)
+
+
 def algorithmic_bytes(cfg, n_elems, n_vertices, n_rows, nnz):
     """SURVEY.md §8d compulsory-traffic model: connectivity + coordinates +
     CSR values written and col_idx read + row_ptr + RHS."""
@@ -348,6 +363,7 @@ def main():
         return
     peak, peak_src = measured_peaks()
     B = algorithmic_bytes(cfg, vconn_l.shape[0], coords.shape[0], pat.n_rows, pat.nnz)
+    F = model_flops(cfg) * vconn_l.shape[0]   # SURVEY.md §8d flop model
     # the dominant kernel(s): the whole atomic-free step (K2a + K2b) for the
     # gather, K2 for the atomic scatter (K0 is a separate memset-like kernel)
     kern_ms = step_ms if scatter == "gather" else k2_ms
@@ -384,7 +400,13 @@ def main():
                    "nvrtc_compile_ms": compile_ms, "strategy": info["strategy"], "registers": info["registers"],
                    "flops_per_element": info["flops_per_element"],
                    "hbm_gbs_step": B / (step_ms * 1e-3) / 1e9},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "roofline": ({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak}
+                     if info["flops_per_element"] * vconn_l.shape[0] / B <= FP64_PEAK_TFLOPS * 1e3 / peak else
+                     {"bound": "fp64", "achieved": F / (kern_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                      "unit": "TFLOP/s", "frac": F / (kern_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                      "peak_note": "nominal B200 fp64 (no measured fp64 peak in MEASURED_PEAKS.json); "
+                                   "flops = SURVEY.md §8d model", "flops_per_element_model": model_flops(cfg),
+                      "hbm_gbs": achieved}) | {
                      "traffic": traffic,
                      "kernel": KERNEL_DESC[scatter],
                      "bytes_per_launch": int(B), "peak_source": peak_src},
