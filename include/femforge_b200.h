@@ -107,6 +107,15 @@ int ff_ctx_set_scatter(ff_ctx* ctx, int mode);
 /* ---- forms: weak form text -> symbolic -> CUDA source -> NVRTC (sm_100a) - */
 /* ctx may be NULL: compile-only (no device needed; ff_assemble* then fail). */
 int ff_form_create(ff_ctx* ctx, const ff_form_desc* desc, ff_form** out);
+/* Vector-valued (ncomp-component) P1/P2 forms as blocks of scalar forms:
+ * a(u,v) = sum_{c,d} a_cd(u_d, v_c) with block_bilinear[c*ncomp + d] the
+ * scalar integrand over u*, v* (trial component d, test component c), and
+ * l(v) = sum_c l_c(v_c) with block_linear[c]. Local DOF a*ncomp + c, global
+ * DOF ncomp*node + c; the mesh must carry ncomp (ff_mesh_set_components). The
+ * pattern is the ncomp x ncomp block expansion of the scalar pattern; the
+ * scatter is the fp64-RED kernel (BASELINE config 5, elasticity). */
+int ff_form_create_blocked(ff_ctx* ctx, const ff_form_desc* desc, int ncomp, const char* const* block_bilinear,
+                           const char* const* block_linear, ff_form** out);
 /* Raw template route: compile caller-provided CUDA source that defines
  * extern "C" __global__ ff_assemble_atomic with the template's signature. */
 int ff_compile(ff_ctx* ctx, const char* cuda_src, int dim, int degree, int block_size, ff_form** out,
@@ -122,6 +131,9 @@ int ff_form_destroy(ff_form* form);
 int ff_mesh_create(ff_ctx* ctx, int dim, const double* coords, int64_t n_vertices, const int32_t* vconn,
                    int64_t n_elems, const int32_t* dconn, int32_t dofs_per_elem, int64_t n_dofs,
                    ff_mesh** out);
+/* Vector space on the mesh: ncomp components per node (DOF ncomp*node + c);
+ * n_dofs of ff_mesh_create stays the node (scalar) DOF count. */
+int ff_mesh_set_components(ff_mesh* mesh, int ncomp);
 /* Re-upload coordinates/connectivity into an existing mesh (same sizes). */
 int ff_mesh_update(ff_mesh* mesh, const double* coords, const int32_t* vconn, const int32_t* dconn);
 int ff_mesh_destroy(ff_mesh* mesh);

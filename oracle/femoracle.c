@@ -471,3 +471,93 @@ int fo_assemble(int form, int dim, int degree, int quad_id, const double* coords
   if (first_miss >= 0) { if (bad) *bad = first_miss; return -2; }
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* vector P1/P2 linear elasticity (BASELINE.json config 5; no reference      */
+/* implementation -- parity rests on the rigid-body-mode and block KATs in   */
+/* the tests). Per element and quadrature point (ascending q, the device.cpp */
+/* 176-192 order) K[(a,c),(b,d)] += w det (lam d_d phi_b d_c phi_a           */
+/*   + mu d_c phi_b d_d phi_a + mu [c==d] grad phi_b . grad phi_a),          */
+/* F[(a,c)] += w det f_c phi_a; local DOF a*dim + c, global dim*node + c,    */
+/* binary-search scatter into the block-expanded CSR (device.cpp:274-288).   */
+int fo_assemble_elasticity(int dim, int degree, int quad_id, const double* coords, const int32_t* vconn,
+                           const int32_t* dconn, int64_t ne, const int64_t* row_ptr, const int32_t* col_idx,
+                           int64_t rb, int64_t re, double lam, double mu, const double* force, double* values,
+                           double* rhs, int64_t* bad) {
+  double qp[3 * 16], qw[16];
+  const int nq = fo_quad_size(dim, quad_id);
+  if (nq <= 0) return -3;
+  fo_quad_rule(dim, quad_id, qp, qw);
+  const int k = n_local(dim, degree), nv = dim + 1, n = k * dim;
+  memset(values, 0, sizeof(double) * (size_t)row_ptr[re - rb]);
+  memset(rhs, 0, sizeof(double) * (size_t)(re - rb));
+  double* ke = malloc(sizeof(double) * (size_t)(n * n));
+  double fe[30];
+  for (int64_t e = 0; e < ne; ++e) {
+    double xv[12], J[3][3] = {{0}}, C[3][3] = {{0}}, det;
+    for (int a = 0; a < nv; ++a)
+      for (int c = 0; c < dim; ++c) xv[a * dim + c] = coords[(int64_t)vconn[e * nv + a] * dim + c];
+    for (int r = 0; r < dim; ++r)
+      for (int c = 0; c < dim; ++c) J[r][c] = xv[(c + 1) * dim + r] - xv[r];
+    if (dim == 2) {
+      det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      C[0][0] = J[1][1]; C[0][1] = -J[1][0];
+      C[1][0] = -J[0][1]; C[1][1] = J[0][0];
+    } else {
+      det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          int r1 = (r + 1) % 3, r2 = (r + 2) % 3, c1 = (c + 1) % 3, c2 = (c + 2) % 3;
+          C[r][c] = J[r1][c1] * J[r2][c2] - J[r1][c2] * J[r2][c1];
+        }
+    }
+    if (fabs(det) <= 1e-14) {
+      if (bad) *bad = e;
+      free(ke);
+      return -1;
+    }
+    for (int t = 0; t < n * n; ++t) ke[t] = 0.0;
+    for (int t = 0; t < n; ++t) fe[t] = 0.0;
+    double phi[10], dref[30], g[10][3];
+    for (int q = 0; q < nq; ++q) {
+      basis(dim, degree, qp + q * dim, phi, dref);
+      for (int a = 0; a < k; ++a)
+        for (int r = 0; r < dim; ++r) {
+          double s = 0.0;
+          for (int c = 0; c < dim; ++c) s += C[r][c] * dref[a * dim + c];
+          g[a][r] = s / det;
+        }
+      for (int a = 0; a < k; ++a)
+        for (int c = 0; c < dim; ++c) {
+          for (int b = 0; b < k; ++b)
+            for (int d = 0; d < dim; ++d) {
+              double gg = 0.0;
+              for (int r = 0; r < dim; ++r) gg += g[b][r] * g[a][r];
+              double s = lam * g[b][d] * g[a][c] + mu * g[b][c] * g[a][d] + (c == d ? mu * gg : 0.0);
+              ke[(a * dim + c) * n + b * dim + d] += qw[q] * (s * det);
+            }
+          fe[a * dim + c] += qw[q] * (force[c] * phi[a] * det);
+        }
+    }
+    const int32_t* dd = dconn + e * k;
+    for (int a = 0; a < k; ++a)
+      for (int c = 0; c < dim; ++c) {
+        const int64_t gi = (int64_t)dim * dd[a] + c;
+        if (gi < rb || gi >= re) continue;
+        for (int b = 0; b < k; ++b)
+          for (int d = 0; d < dim; ++d) {
+            const int64_t s = find_slot(row_ptr, col_idx, gi - rb, dim * dd[b] + d);
+            if (s < 0) {
+              if (bad) *bad = gi;
+              free(ke);
+              return -2;
+            }
+            values[s] += ke[(a * dim + c) * n + b * dim + d];
+          }
+        rhs[gi - rb] += fe[a * dim + c];
+      }
+  }
+  free(ke);
+  return 0;
+}

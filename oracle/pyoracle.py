@@ -41,6 +41,9 @@ def lib():
         L.fo_assemble.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _f64p, _i32p, _i32p, C.c_int64,
                                   _i64p, _i32p, C.c_int64, C.c_int64, _f64p, _f64p, C.c_int,
                                   C.POINTER(C.c_int64)]
+        L.fo_assemble_elasticity.argtypes = [C.c_int, C.c_int, C.c_int, _f64p, _i32p, _i32p, C.c_int64, _i64p,
+                                             _i32p, C.c_int64, C.c_int64, C.c_double, C.c_double, _f64p, _f64p,
+                                             _f64p, C.POINTER(C.c_int64)]
         L.fo_element_matrix.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _f64p, _f64p, _f64p]
         _lib = L
     return _lib
@@ -104,6 +107,38 @@ def assemble(form, dim, degree, quad_id, coords, vconn, dconn, row_ptr, col_idx,
         raise OracleError(f"column not present in sparsity row {bad.value}")
     if rc != 0:
         raise OracleError(f"oracle error {rc}")
+    return vals, rhs
+
+
+def block_pattern(row_ptr, col_idx, bs):
+    """bs x bs block expansion of a scalar CSR (vector space DOF bs*node + c)."""
+    n = len(row_ptr) - 1
+    lens = np.diff(row_ptr)
+    rp = np.zeros(bs * n + 1, np.int64)
+    rp[1:] = np.cumsum(np.repeat(lens * bs, bs))
+    ci = np.empty(int(rp[-1]), np.int32)
+    for r in range(n):
+        cols = col_idx[row_ptr[r]:row_ptr[r + 1]].astype(np.int64)
+        blk = (bs * cols[:, None] + np.arange(bs)[None, :]).ravel()
+        for c in range(bs):
+            ci[rp[bs * r + c]:rp[bs * r + c + 1]] = blk
+    return rp, ci
+
+
+def assemble_elasticity(dim, degree, quad_id, coords, vconn, dconn, row_ptr, col_idx, lam=1.0, mu=1.0,
+                        force=(0.0, 0.0, -1.0), row_begin=0, row_end=None):
+    """Vector P2 elasticity restatement (femoracle.c) into a block-expanded CSR."""
+    row_end = row_begin + len(row_ptr) - 1 if row_end is None else row_end
+    vals = np.empty(int(row_ptr[-1])); rhs = np.empty(row_end - row_begin)
+    bad = C.c_int64(-1)
+    f = np.ascontiguousarray(list(force) + [0.0] * (3 - len(force)), np.float64)
+    rc = lib().fo_assemble_elasticity(dim, degree, quad_id, np.ascontiguousarray(coords, np.float64),
+                                      np.ascontiguousarray(vconn, np.int32), np.ascontiguousarray(dconn, np.int32),
+                                      vconn.shape[0], np.ascontiguousarray(row_ptr, np.int64),
+                                      np.ascontiguousarray(col_idx, np.int32), row_begin, row_end, lam, mu, f, vals,
+                                      rhs, C.byref(bad))
+    if rc != 0:
+        raise OracleError(f"oracle error {rc} at {bad.value}")
     return vals, rhs
 
 

@@ -346,6 +346,7 @@ int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w)
   if (flags & FF_SCATTER_TILES) mode = FF_SCATTER_ROWTILE;
   if (flags & (FF_SCATTER_GATHER | FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) mode = FF_SCATTER_GATHER_MODE;
   if (flags & (FF_ZERO_ONLY | FF_SKIP_ZERO)) mode = FF_SCATTER_ATOMIC_MODE;
+  if (f->ncomp > 1) mode = FF_SCATTER_ATOMIC_MODE;  // vector forms: block-expanded atomic scatter
   if (mode == FF_SCATTER_GATHER_MODE &&
       !(f->kernel_grows[w] && p->max_row_len <= 255 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax))
     mode = FF_SCATTER_ATOMIC_MODE;
@@ -483,7 +484,7 @@ void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_valu
                      unsigned flags = 0) {
   require(f->ctx && f->ctx == m->ctx && m->ctx == p->ctx, "form, mesh and pattern must share one context");
   require(f->dim == m->dim, "form and mesh dimensions differ");
-  require(f->n_local == m->k, "form and mesh have different DOFs per element");
+  require(f->ncomp == m->bs && f->n_local == m->k * m->bs, "form and mesh have different DOFs per element");
   ensure_plan(p, m);
   const int w = p->slot_bytes;
   build_variant(f, w);
@@ -517,7 +518,9 @@ void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_valu
     return;
   }
   if (!(flags & FF_SKIP_ZERO))
-    ffb::cuda_check(ffb::kernels::zero_fill(d_values, p->nnz, d_rhs, n_rows, ctx->d_status, ctx->sm_count, s), "K0");
+    ffb::cuda_check(ffb::kernels::zero_fill(d_values, int64_t(p->bs) * p->bs * p->nnz, d_rhs, p->bs * n_rows,
+                                            ctx->d_status, ctx->sm_count, s),
+                    "K0");
   if (m->ne == 0 || (flags & FF_ZERO_ONLY)) return;
   const double* coords = m->coords;
   const int32_t* vconn = m->vconn;
@@ -691,6 +694,55 @@ int ff_form_create(ff_ctx* ctx, const ff_form_desc* d, ff_form** out) {
   });
 }
 
+int ff_form_create_blocked(ff_ctx* ctx, const ff_form_desc* d, int ncomp, const char* const* block_bilinear,
+                           const char* const* block_linear, ff_form** out) {
+  return guarded([&] {
+    require(d && out && block_bilinear && block_linear, "ff_form_create_blocked: null argument");
+    require(d->dim == 2 || d->dim == 3, "form dimension must be 2 or 3");
+    require(d->degree == 1 || d->degree == 2, "only Lagrange degree 1 and 2 are supported");
+    require(ncomp >= 1 && ncomp <= 3, "1 to 3 components per node");
+    auto f = std::make_unique<ff_form>();
+    f->ctx = ctx;
+    f->dim = d->dim;
+    f->degree = d->degree;
+    f->block = d->block_size > 0 ? d->block_size : 128;
+    std::vector<fem::WeakForm> blocks(ncomp * ncomp), lin(ncomp);
+    for (int q = 0; q < ncomp * ncomp; ++q) {
+      require(block_bilinear[q] != nullptr, "missing bilinear block");
+      blocks[q].bilinear = symbolic::parse(block_bilinear[q]);
+      blocks[q].linear = symbolic::integer(0);
+      blocks[q].space.dim = d->dim;
+      blocks[q].space.degree = d->degree;
+    }
+    for (int c = 0; c < ncomp; ++c) {
+      require(block_linear[c] != nullptr, "missing linear component");
+      lin[c].bilinear = symbolic::integer(0);
+      lin[c].linear = symbolic::parse(block_linear[c]);
+      lin[c].space.dim = d->dim;
+      lin[c].space.degree = d->degree;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    f->inst = fem::instantiate_blocked(blocks, lin, ncomp);
+    f->n_local = f->inst.n_local;
+    f->ncomp = ncomp;
+    f->params.block_size = f->block;
+    f->params.quad_rule = d->quad_rule;
+    f->params.strategy = static_cast<codegen::Strategy>(d->strategy);
+    f->params.n_local = f->n_local;
+    f->compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    build_variant(f.get(), 1);
+    *out = f.release();
+  });
+}
+
+int ff_mesh_set_components(ff_mesh* m, int ncomp) {
+  return guarded([&] {
+    require(m && ncomp >= 1 && ncomp <= 3, "invalid argument");
+    m->bs = ncomp;
+    ++m->generation;
+  });
+}
+
 int ff_compile(ff_ctx* ctx, const char* src, int dim, int degree, int block_size, ff_form** out, char* log,
                size_t log_cap) {
   return guarded([&] {
@@ -830,13 +882,18 @@ int ff_mesh_destroy(ff_mesh* m) {
 int ff_pattern_build(ff_ctx* ctx, const ff_mesh* m, int64_t rb, int64_t re, ff_pattern** out) {
   return guarded([&] {
     require(ctx && m && out, "ff_pattern_build: null argument");
-    require(0 <= rb && rb <= re && re <= m->n_dofs, "row block outside [0, n_dofs]");
+    const int bs = m->bs;
+    require(0 <= rb && rb <= re && re <= bs * m->n_dofs, "row block outside [0, n_dofs]");
+    require(rb % bs == 0 && re % bs == 0, "row block of a vector space must cover whole nodes");
+    rb /= bs;
+    re /= bs;
     require(re - rb < (int64_t(1) << 31), "row block too large");
     bind(ctx);
     auto p = std::make_unique<ff_pattern>();
     p->ctx = ctx;
     p->rb = rb;
     p->re = re;
+    p->bs = bs;
     p->k = m->k;
     int mx = 0;
     ffb::cuda_check(ffb::kernels::build_pattern(m->dconn, m->ne, m->k, rb, re, ctx->sm_count, ctx->stream, &p->row_ptr,
@@ -850,32 +907,47 @@ int ff_pattern_build(ff_ctx* ctx, const ff_mesh* m, int64_t rb, int64_t re, ff_p
 int ff_pattern_info(const ff_pattern* p, int64_t* n_rows, int64_t* nnz, int32_t* max_row_len) {
   return guarded([&] {
     require(p, "null pattern");
-    if (n_rows) *n_rows = p->re - p->rb;
-    if (nnz) *nnz = p->nnz;
-    if (max_row_len) *max_row_len = p->max_row_len;
+    if (n_rows) *n_rows = p->bs * (p->re - p->rb);
+    if (nnz) *nnz = int64_t(p->bs) * p->bs * p->nnz;
+    if (max_row_len) *max_row_len = p->bs * p->max_row_len;
   });
+}
+
+// device CSR of the pattern as the user sees it (block-expanded for bs > 1)
+void ensure_device_csr(ff_pattern* p) {
+  if (p->bs == 1 || p->vrow_ptr) return;
+  bind(p->ctx);
+  const int64_t n = p->re - p->rb;
+  p->vrow_ptr = device_alloc<int64_t>(p->bs * n + 1, "blocked row_ptr");
+  p->vcol_idx = device_alloc<int32_t>(int64_t(p->bs) * p->bs * p->nnz, "blocked col_idx");
+  ffb::cuda_check(ffb::kernels::expand_block_pattern(p->row_ptr, p->col_idx, n, p->bs, p->vrow_ptr, p->vcol_idx,
+                                                     p->ctx->sm_count, p->ctx->stream),
+                  "block pattern expansion");
+  ffb::cuda_check(cudaStreamSynchronize(p->ctx->stream), "block pattern expansion");
 }
 
 int ff_pattern_export(const ff_pattern* p, int64_t* row_ptr, int32_t* col_idx) {
   return guarded([&] {
     require(p, "null pattern");
     bind(p->ctx);
-    if (row_ptr)
-      ffb::cuda_check(cudaMemcpy(row_ptr, p->row_ptr, (p->re - p->rb + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
-    if (col_idx) ffb::cuda_check(cudaMemcpy(col_idx, p->col_idx, p->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    ff_pattern* q = const_cast<ff_pattern*>(p);  // the expansion is a cache
+    ensure_device_csr(q);
+    const int64_t* rp = p->bs == 1 ? p->row_ptr : p->vrow_ptr;
+    const int32_t* ci = p->bs == 1 ? p->col_idx : p->vcol_idx;
+    const int64_t n = p->bs * (p->re - p->rb), nnz = int64_t(p->bs) * p->bs * p->nnz;
+    if (row_ptr) ffb::cuda_check(cudaMemcpy(row_ptr, rp, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+    if (col_idx) ffb::cuda_check(cudaMemcpy(col_idx, ci, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
   });
 }
 
 int ff_pattern_export_ell(const ff_pattern* p, int32_t max_nz, int32_t* row_len, int32_t* row_cols) {
   return guarded([&] {
     require(p && row_len && row_cols, "null argument");
-    require(max_nz >= p->max_row_len, "max_nz smaller than the longest row");
-    const int64_t n = p->re - p->rb;
+    require(max_nz >= p->bs * p->max_row_len, "max_nz smaller than the longest row");
+    const int64_t n = p->bs * (p->re - p->rb);
     std::vector<int64_t> rp(n + 1);
-    std::vector<int32_t> ci(p->nnz);
-    bind(p->ctx);
-    ffb::cuda_check(cudaMemcpy(rp.data(), p->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
-    ffb::cuda_check(cudaMemcpy(ci.data(), p->col_idx, p->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    std::vector<int32_t> ci(int64_t(p->bs) * p->bs * p->nnz);
+    if (ff_pattern_export(p, rp.data(), ci.data()) != FF_OK) throw Error(FF_E_CUDA, g_error);
     for (int64_t i = 0; i < n; ++i) {
       row_len[i] = static_cast<int32_t>(rp[i + 1] - rp[i]);
       for (int32_t c = 0; c < max_nz; ++c)
@@ -887,8 +959,10 @@ int ff_pattern_export_ell(const ff_pattern* p, int32_t max_nz, int32_t* row_len,
 int ff_pattern_device(const ff_pattern* p, const int64_t** row_ptr, const int32_t** col_idx) {
   return guarded([&] {
     require(p, "null pattern");
-    if (row_ptr) *row_ptr = p->row_ptr;
-    if (col_idx) *col_idx = p->col_idx;
+    ff_pattern* q = const_cast<ff_pattern*>(p);
+    ensure_device_csr(q);
+    if (row_ptr) *row_ptr = p->bs == 1 ? p->row_ptr : p->vrow_ptr;
+    if (col_idx) *col_idx = p->bs == 1 ? p->col_idx : p->vcol_idx;
   });
 }
 
@@ -898,6 +972,8 @@ int ff_pattern_destroy(ff_pattern* p) {
     bind(p->ctx);
     cudaFree(p->row_ptr);
     cudaFree(p->col_idx);
+    cudaFree(p->vrow_ptr);
+    cudaFree(p->vcol_idx);
     cudaFree(p->slots);
     free_tile_plan(p);
     free_gather(p);
@@ -1010,12 +1086,13 @@ int ff_assemble(ff_form* f, ff_mesh* m, ff_pattern* p, const double* coords, con
         ++m->generation;
       }
     }
-    const int64_t n_rows = p->re - p->rb;
-    if (!p->e2e_values) p->e2e_values = device_alloc<double>(p->nnz, "values");
+    const int64_t n_rows = p->bs * (p->re - p->rb);
+    const int64_t nnz = int64_t(p->bs) * p->bs * p->nnz;
+    if (!p->e2e_values) p->e2e_values = device_alloc<double>(nnz, "values");
     if (!p->e2e_rhs) p->e2e_rhs = device_alloc<double>(n_rows, "rhs");
     launch_assembly(f, m, p, p->e2e_values, p->e2e_rhs, ctx->stream);
     report_status(ctx, stats);
-    ffb::cuda_check(cudaMemcpyAsync(values_out, p->e2e_values, p->nnz * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ffb::cuda_check(cudaMemcpyAsync(values_out, p->e2e_values, nnz * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     ffb::cuda_check(cudaMemcpyAsync(rhs_out, p->e2e_rhs, n_rows * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "D2H");
     if (stats) stats->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

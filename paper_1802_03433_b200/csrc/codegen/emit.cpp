@@ -63,6 +63,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   fill(text, "DIM", std::to_string(f.dim));
   fill(text, "DEGREE", std::to_string(f.degree));
   fill(text, "NLOC", std::to_string(f.n_local));
+  fill(text, "BS", std::to_string(f.ncomp));
   fill(text, "BLOCK", std::to_string(cfg.block_size));
   const RowTileParams tp = rowtile_params(f.n_local, cfg.block_size);
   fill(text, "TILE_ACC", std::to_string(tp.acc));
@@ -74,7 +75,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   fill(text, "ELEMENT_BODY", body);
   fill(text, "ELEMENT_PRELUDE", plan.prelude);
   // the row gather needs a reference-tensor plan and <= 12 slot bytes per record
-  const bool gather = plan.n_kinv > 0 && f.n_local <= 12 && plan.n_kinv + f.n_local <= 24;
+  const bool gather = f.ncomp == 1 && plan.n_kinv > 0 && f.n_local <= 12 && plan.n_kinv + f.n_local <= 24;
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
   {

@@ -468,4 +468,74 @@ InstantiatedForm instantiate(const WeakForm& wf) {
   return out;
 }
 
+
+InstantiatedForm instantiate_blocked(const std::vector<WeakForm>& blocks, const std::vector<WeakForm>& linear,
+                                     int ncomp) {
+  if (ncomp < 1 || blocks.size() != static_cast<std::size_t>(ncomp * ncomp) ||
+      linear.size() != static_cast<std::size_t>(ncomp))
+    throw FormError("blocked form needs ncomp^2 bilinear blocks and ncomp linear forms");
+  std::vector<InstantiatedForm> bi, li;
+  for (const WeakForm& w : blocks) bi.push_back(instantiate(w));
+  for (const WeakForm& w : linear) li.push_back(instantiate(w));
+  const int k = bi[0].n_local;
+  for (const auto& f : bi)
+    if (f.n_local != k || f.dim != bi[0].dim) throw FormError("blocks of a vector form must share the scalar space");
+  InstantiatedForm out;
+  out.dim = bi[0].dim;
+  out.degree = bi[0].degree;
+  out.ncomp = ncomp;
+  out.n_local = k * ncomp;
+  const int n = out.n_local;
+  out.bilinear.resize(static_cast<std::size_t>(n) * n);
+  out.geo_bilinear.resize(static_cast<std::size_t>(n) * n);
+  out.linear.resize(n);
+  out.geo_linear.resize(n);
+  for (int a = 0; a < k; ++a)
+    for (int c = 0; c < ncomp; ++c) {
+      const int i = a * ncomp + c;
+      out.linear[i] = li[c].linear[a];
+      out.geo_linear[i] = li[c].geo_linear[a];
+      for (int b = 0; b < k; ++b)
+        for (int d = 0; d < ncomp; ++d) {
+          const int j = b * ncomp + d;
+          const InstantiatedForm& blk = bi[c * ncomp + d];
+          out.bilinear[static_cast<std::size_t>(i) * n + j] = blk.bilinear[a * k + b];
+          out.geo_bilinear[static_cast<std::size_t>(i) * n + j] = blk.geo_bilinear[a * k + b];
+        }
+    }
+  return out;
+}
+
+void elasticity_blocks(int dim, const Expr& lambda, const Expr& mu, const std::vector<Expr>& f,
+                       std::vector<WeakForm>& blocks, std::vector<WeakForm>& linear) {
+  const FormSymbols& s = form_symbols();
+  const Expr du[3] = {s.u_x, s.u_y, s.u_z}, dv[3] = {s.v_x, s.v_y, s.v_z};
+  blocks.clear();
+  linear.clear();
+  for (int c = 0; c < dim; ++c)
+    for (int d = 0; d < dim; ++d) {
+      // test component c, trial component d
+      Expr e = lambda * du[d] * dv[c] + mu * du[c] * dv[d];
+      if (c == d) {
+        std::vector<Expr> g;
+        for (int q = 0; q < dim; ++q) g.push_back(du[q] * dv[q]);
+        e = e + mu * symbolic::add(g);
+      }
+      WeakForm w;
+      w.bilinear = e;
+      w.linear = symbolic::integer(0);
+      w.space.dim = dim;
+      w.space.degree = 2;
+      blocks.push_back(w);
+    }
+  for (int c = 0; c < dim; ++c) {
+    WeakForm w;
+    w.bilinear = symbolic::integer(0);
+    w.linear = f[c] * s.v;
+    w.space.dim = dim;
+    w.space.degree = 2;
+    linear.push_back(w);
+  }
+}
+
 }  // namespace femforge::fem

@@ -143,7 +143,8 @@ AffineMap affine_map();  // 2D, fem.cpp:73-87
 struct InstantiatedForm {
   int dim = 2;
   int degree = 1;
-  int n_local = 3;
+  int n_local = 3;  // DOFs per element (ncomp x scalar DOFs for vector spaces)
+  int ncomp = 1;    // components of a vector space; local DOF index = a * ncomp + c
   std::vector<Expr> bilinear;  // n_local x n_local, row-major (test i, trial j)
   std::vector<Expr> linear;    // n_local
   std::vector<Expr> geo_bilinear;
@@ -161,6 +162,21 @@ struct GeometrySymbols {
 const GeometrySymbols& geometry_symbols();
 
 InstantiatedForm instantiate(const WeakForm& wf);
+
+// Vector-valued (ncomp-component) Lagrange forms as blocks of scalar forms:
+// a(u, v) = sum_{c,d} a_cd(u_d, v_c), l(v) = sum_c l_c(v_c), each block a
+// scalar WeakForm over the reserved symbols (u*, v* = the scalar basis of
+// the trial / test component). blocks is row-major [c][d] (ncomp^2 forms;
+// their `linear` parts are ignored), linear has ncomp forms (their `bilinear`
+// parts are ignored). The result has node-major local DOFs a * ncomp + c and
+// global DOFs ncomp * node + c (3x3 blocks for elasticity, BASELINE config 5).
+InstantiatedForm instantiate_blocked(const std::vector<WeakForm>& blocks, const std::vector<WeakForm>& linear,
+                                     int ncomp);
+
+// Isotropic linear elasticity, lambda div u div v + mu sum_cd d_d u_c (d_d v_c
+// + d_c v_d), body force f: the block forms for instantiate_blocked.
+void elasticity_blocks(int dim, const Expr& lambda, const Expr& mu, const std::vector<Expr>& f,
+                       std::vector<WeakForm>& blocks, std::vector<WeakForm>& linear);
 
 using Vec2 = std::array<Expr, 2>;
 using Mat2 = std::array<Expr, 4>;

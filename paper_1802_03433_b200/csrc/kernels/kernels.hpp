@@ -89,6 +89,11 @@ void free_gather_plan(GatherPlan* p);
 // (index, value) pairs), written to *d_out.
 cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_out, int sm_count, cudaStream_t s);
 
+// Block expansion of a scalar CSR: row bs*n + c holds columns bs*m + d of every
+// scalar column m of row n (d = 0..bs-1), sorted. rp_v [bs*n_rows + 1].
+cudaError_t expand_block_pattern(const int64_t* rp_s, const int32_t* ci_s, int64_t n_rows, int bs, int64_t* rp_v,
+                                 int32_t* ci_v, int sm_count, cudaStream_t s);
+
 // K0: values[0:na] = 0, rhs[0:nb] = 0, status[0:2] = ~0 (one launch).
 cudaError_t zero_fill(double* a, int64_t na, double* b, int64_t nb, unsigned long long* status, int sm_count,
                       cudaStream_t s);

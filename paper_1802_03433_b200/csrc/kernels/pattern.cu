@@ -1238,6 +1238,28 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
   return done(cudaGetLastError());
 }
 
+__global__ void expand_block_kernel(const int64_t* __restrict__ rp_s, const int32_t* __restrict__ ci_s, int64_t n_rows,
+                                    int bs, int64_t* __restrict__ rp_v, int32_t* __restrict__ ci_v) {
+  for (int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; n < n_rows;
+       n += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = rp_s[n], len = rp_s[n + 1] - b;
+    for (int c = 0; c < bs; ++c) {
+      const int64_t o = static_cast<int64_t>(bs) * bs * b + static_cast<int64_t>(c) * bs * len;
+      rp_v[bs * n + c] = o;
+      for (int64_t t = 0; t < len; ++t)
+        for (int d = 0; d < bs; ++d) ci_v[o + t * bs + d] = bs * ci_s[b + t] + d;
+    }
+    if (n == n_rows - 1) rp_v[bs * n_rows] = static_cast<int64_t>(bs) * bs * rp_s[n_rows];
+  }
+}
+
+cudaError_t expand_block_pattern(const int64_t* rp_s, const int32_t* ci_s, int64_t n_rows, int bs, int64_t* rp_v,
+                                 int32_t* ci_v, int sm_count, cudaStream_t s) {
+  if (n_rows == 0) return cudaMemsetAsync(rp_v, 0, sizeof(int64_t), s);
+  expand_block_kernel<<<grid_for(n_rows, sm_count * 8), kThreads, 0, s>>>(rp_s, ci_s, n_rows, bs, rp_v, ci_v);
+  return cudaGetLastError();
+}
+
 cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_out, int sm_count, cudaStream_t s) {
   cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s);
   if (n > 0) hash_kernel<<<grid_for(n, sm_count * 8), kThreads, 0, s>>>(d_a, n, d_out);

@@ -51,6 +51,7 @@ struct ff_ctx {
 struct ff_form {
   ff_ctx* ctx = nullptr;
   int dim = 2, degree = 1, n_local = 3, block = 256;
+  int ncomp = 1;                    // components of a vector (blocked) form
   femforge::codegen::ElementPlan plan;
   bool raw = false;                 // ff_compile route (caller source)
   femforge::fem::InstantiatedForm inst;
@@ -72,7 +73,8 @@ struct ff_form {
 struct ff_mesh {
   ff_ctx* ctx = nullptr;
   int dim = 2;
-  int k = 3;  // DOFs per element
+  int k = 3;  // (scalar) DOFs per element
+  int bs = 1; // components per node: global DOF bs * node + c
   int64_t nv = 0, ne = 0, n_dofs = 0;
   double* coords = nullptr;
   int32_t* vconn = nullptr;
@@ -83,7 +85,12 @@ struct ff_mesh {
 
 struct ff_pattern {
   ff_ctx* ctx = nullptr;
+  // rows [rb, re) and nnz of the SCALAR pattern; a blocked pattern (bs > 1)
+  // is its bs x bs expansion: bs*(re-rb) rows, bs^2*nnz entries
   int64_t rb = 0, re = 0, nnz = 0;
+  int bs = 1;
+  int64_t* vrow_ptr = nullptr;  // expanded CSR on the device (blocked; built on demand)
+  int32_t* vcol_idx = nullptr;
   int max_row_len = 0;
   int k = 0;
   int64_t ne = 0;

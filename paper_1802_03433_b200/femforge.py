@@ -106,6 +106,9 @@ SIGNATURES = [
     ("ff_window_source", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_form_create", C.c_int, [_P, C.POINTER(_FormDesc), C.POINTER(_P)]),
     ("ff_compile", C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P), C.c_char_p, C.c_size_t]),
+    ("ff_form_create_blocked", C.c_int, [_P, C.POINTER(_FormDesc), C.c_int, C.POINTER(C.c_char_p),
+                                         C.POINTER(C.c_char_p), C.POINTER(_P)]),
+    ("ff_mesh_set_components", C.c_int, [_P, C.c_int]),
     ("ff_form_source", C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_form_cubin", C.c_int, [_P, _P, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_form_info_get", C.c_int, [_P, C.POINTER(FormInfo)]),
@@ -219,6 +222,20 @@ class Form:
         self.h, self.ctx, self.dim, self.degree = h, ctx, dim, degree
 
     @classmethod
+    def blocked(cls, ctx, dim, degree, ncomp, block_bilinear, block_linear, quad_rule=0, strategy="auto",
+                block_size=128):
+        """Vector-valued form: block_bilinear[c*ncomp+d] (test c, trial d) and
+        block_linear[c] scalar integrands (ff_form_create_blocked)."""
+        self = cls.__new__(cls)
+        d = _FormDesc(dim, degree, quad_rule, STRATEGY.get(strategy, strategy), block_size, b"0", b"0")
+        bb = (C.c_char_p * len(block_bilinear))(*[t.encode() for t in block_bilinear])
+        bl = (C.c_char_p * len(block_linear))(*[t.encode() for t in block_linear])
+        h = _P()
+        _ok(lib().ff_form_create_blocked(ctx.h if ctx else None, C.byref(d), ncomp, bb, bl, C.byref(h)))
+        self.h, self.ctx, self.dim, self.degree, self.ncomp = h, ctx, dim, degree, ncomp
+        return self
+
+    @classmethod
     def from_source(cls, ctx, source, dim, degree, block_size=256):
         self = cls.__new__(cls)
         h = _P()
@@ -278,7 +295,7 @@ class Mesh:
     """Device copy of coordinates [nv][dim], vertex connectivity [ne][dim+1]
     and DOF connectivity [ne][k] (None for P1)."""
 
-    def __init__(self, ctx, dim, coords, vconn, dconn=None, n_dofs=None):
+    def __init__(self, ctx, dim, coords, vconn, dconn=None, n_dofs=None, ncomp=1):
         self.coords = np.ascontiguousarray(coords, np.float64)
         self.vconn = np.ascontiguousarray(vconn, np.int32)
         self.dconn = None if dconn is None else np.ascontiguousarray(dconn, np.int32)
@@ -290,6 +307,9 @@ class Mesh:
         _ok(lib().ff_mesh_create(ctx.h, dim, _ptr(self.coords), self.coords.shape[0], _ptr(self.vconn), self.n_elems,
                                  _ptr(self.dconn), self.k, self.n_dofs, C.byref(h)))
         self.h, self.ctx = h, ctx
+        self.ncomp = ncomp
+        if ncomp > 1:
+            _ok(lib().ff_mesh_set_components(h, ncomp))
 
     def update(self, coords=None, vconn=None, dconn=None):
         _ok(lib().ff_mesh_update(self.h, _ptr(coords), _ptr(vconn), _ptr(dconn)))
@@ -307,7 +327,7 @@ class Pattern:
     """K1: CSR sparsity of rows [row_begin, row_end) (build_sparsity, device.cpp:66-88)."""
 
     def __init__(self, ctx, mesh, row_begin=0, row_end=None):
-        row_end = mesh.n_dofs if row_end is None else row_end
+        row_end = mesh.n_dofs * getattr(mesh, "ncomp", 1) if row_end is None else row_end
         h = _P()
         _ok(lib().ff_pattern_build(ctx.h, mesh.h, row_begin, row_end, C.byref(h)))
         self.h, self.ctx, self.row_begin, self.row_end = h, ctx, row_begin, row_end
@@ -470,3 +490,19 @@ def named_form(name, dim):
         beta = ["1", "x", "-y"][:dim]
         return helmholtz_text(dim, sigma=sig, lam="1+x^2", f=f, beta=beta)
     raise ValueError(name)
+
+
+def elasticity_text(dim, lam="1", mu="1", f=("0", "0", "-1")):
+    """Isotropic linear elasticity as block integrands (BASELINE config 5):
+    block (c, d) = lam u_d v_c + mu u_c v_d + mu [c == d] grad u . grad v over
+    the scalar basis (u_x = d/dx of the trial basis function), l_c = f_c v."""
+    ax = ["x", "y", "z"][:dim]
+    blocks = []
+    for c in range(dim):
+        for d in range(dim):
+            t = f"({lam})*u_{ax[d]}*v_{ax[c]} + ({mu})*u_{ax[c]}*v_{ax[d]}"
+            if c == d:
+                t += f" + ({mu})*(" + " + ".join(f"u_{a}*v_{a}" for a in ax) + ")"
+            blocks.append(t)
+    return blocks, [f"({f[c]})*v" for c in range(dim)]
+

@@ -182,3 +182,13 @@ def test_window_source_compiles(ff):
     assert "ff_gather_windows" in src and "ff_assemble_atomic" in src
     g = ff.Form.from_source(None, src, 3, 2)
     assert g.cubin[:4] == b"\x7fELF"
+
+
+def test_blocked_elasticity_form_compiles(ff):
+    """Vector P2 elasticity (3x3 blocks of scalar forms, 30 DOFs per element)
+    through instantiate_blocked -> tensor plan -> NVRTC for sm_100a."""
+    b, l = ff.elasticity_text(3)
+    f = ff.Form.blocked(None, 3, 2, 3, b, l, quad_rule=4)
+    info = f.info
+    assert info["n_local"] == 30 and info["n_kinv"] == 0
+    assert f.cubin[:4] == b"\x7fELF" and "#define FF_BS 3" in f.source

@@ -348,3 +348,66 @@ def test_window_gather_matches_oracle(ff, ctx, dim, deg, n, form, monkeypatch):
     orp, oci = po.build_pattern(d, nd)
     ov, ob = po.assemble(form, dim, deg, quad, c, v, d, orp, oci, workers=8)
     assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
+
+
+def _elasticity_system(ff, ctx, n, row_begin=0, row_end=None, ids=None, lam="1", mu="1", force=("0", "0", "-1")):
+    c, v = ff.kuhn_mesh(n)
+    d, nd = ff.kuhn_p2_dofs(n, v)
+    if ids is not None:
+        v, d = np.ascontiguousarray(v[ids]), np.ascontiguousarray(d[ids])
+    b, l = ff.elasticity_text(3, lam, mu, force)
+    f = ff.Form.blocked(ctx, 3, 2, 3, b, l, quad_rule=4)
+    m = ff.Mesh(ctx, 3, c, v, d, nd, ncomp=3)
+    p = ff.Pattern(ctx, m, row_begin, row_end)
+    rp, ci = p.export()
+    val, rhs = ff.assemble(f, m, p)
+    return c, v, d, nd, rp, ci, val, rhs, f, m, p
+
+
+@pytest.mark.parametrize("n", [2, 5])
+def test_elasticity_matches_oracle(ff, ctx, n):
+    """Config 5 (vector P2 elasticity): block-expanded pattern bit-exact, values
+    and RHS <= 1e-12 normwise against the C restatement."""
+    c, v, d, nd, rp, ci, val, rhs, f, m, p = _elasticity_system(ff, ctx, n, lam="2", mu="0.5", force=("0", "1", "-1"))
+    assert p.scatter_for(f) == "atomic" and p.n_rows == 3 * nd
+    orp, oci = po.build_pattern(d, nd)
+    vrp, vci = po.block_pattern(orp, oci, 3)
+    assert np.array_equal(rp, vrp) and np.array_equal(ci, vci)
+    ov, ob = po.assemble_elasticity(3, 2, 4, c, v, d, vrp, vci, lam=2.0, mu=0.5, force=(0.0, 1.0, -1.0))
+    assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
+
+
+def test_elasticity_rigid_body_modes_and_row_blocks(ff, ctx):
+    """Size-independent properties at n=16 (24.6k tets, 107k DOFs): rigid-body
+    modes in the kernel, symmetry, sum of the load; 3 node-aligned row blocks
+    concatenate to the 1-GPU system (SURVEY §8e for config 5)."""
+    import scipy.sparse as sp
+    n = 16
+    c, v, d, nd, rp, ci, val, rhs, *_ = _elasticity_system(ff, ctx, n)
+    K = sp.csr_matrix((val, ci, rp), shape=(3 * nd, 3 * nd))
+    L = 2 * n + 1
+    idx = np.arange(nd)
+    X = np.stack([idx % L, (idx // L) % L, idx // (L * L)], 1) / (L - 1)
+    scale = np.abs(val).max()
+    for a, b in [(0, 1), (1, 2), (0, 2)]:
+        u = np.zeros(3 * nd)
+        u[a::3] = -X[:, b]
+        u[b::3] = X[:, a]
+        assert np.abs(K @ u).max() <= 1e-11 * scale
+    for t in range(3):
+        u = np.zeros(3 * nd)
+        u[t::3] = 1.0
+        assert np.abs(K @ u).max() <= 1e-11 * scale
+    assert abs(K - K.T).max() <= 1e-12 * scale
+    assert abs(rhs[2::3].sum() + 1.0) <= 1e-10
+    parts, off, pieces = 3, 0, []
+    for part in range(parts):
+        sb, se = ff.partition_rows(nd, parts, part)
+        ids = ff.select_elements(d, sb, se)
+        sub = _elasticity_system(ff, ctx, n, 3 * sb, 3 * se, ids)
+        pieces.append((sub[4][:-1] + off, sub[5], sub[6], sub[7]))
+        off += sub[4][-1]
+    rp_cat = np.concatenate([x[0] for x in pieces] + [np.array([off])])
+    assert np.array_equal(rp_cat, rp) and np.array_equal(np.concatenate([x[1] for x in pieces]), ci)
+    assert normwise(np.concatenate([x[2] for x in pieces]), val) <= TOL
+    assert normwise(np.concatenate([x[3] for x in pieces]), rhs) <= TOL

@@ -114,3 +114,35 @@ def test_oracle_vs_live_reference_2d_n32():
     # the reference's parallel mode agrees with its deterministic mode (test_device.cpp:298-311)
     vp, bp = h.assemble(workers=4)
     assert normwise(vp, v) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_elasticity_oracle_rigid_body_modes(n):
+    """Vector P2 elasticity (config 5) has no reference implementation; the
+    restatement is pinned by physics: translations and rotations are in the
+    kernel of K, K is symmetric, and sum(rhs_c) = integral of f_c."""
+    import scipy.sparse as sp
+    c, v = po.kuhn_mesh(n)
+    d, nd = po.p2_dofs_kuhn(n, v)
+    rp, ci = po.build_pattern(d, nd)
+    vrp, vci = po.block_pattern(rp, ci, 3)
+    vals, rhs = po.assemble_elasticity(3, 2, 4, c, v, d, vrp, vci, lam=2.0, mu=0.5, force=(0.0, 1.0, -1.0))
+    K = sp.csr_matrix((vals, vci, vrp), shape=(3 * nd, 3 * nd))
+    L = 2 * n + 1
+    idx = np.arange(nd)
+    X = np.stack([idx % L, (idx // L) % L, idx // (L * L)], 1) / (L - 1)
+    scale = np.abs(vals).max()
+    modes = []
+    for t in range(3):
+        u = np.zeros(3 * nd)
+        u[t::3] = 1.0
+        modes.append(u)
+    for a, b in [(0, 1), (1, 2), (0, 2)]:
+        u = np.zeros(3 * nd)
+        u[a::3] = -X[:, b]
+        u[b::3] = X[:, a]
+        modes.append(u)
+    for u in modes:
+        assert np.abs(K @ u).max() <= 1e-12 * scale
+    assert abs(K - K.T).max() <= 1e-14 * scale
+    assert abs(rhs[1::3].sum() - 1.0) <= 1e-12 and abs(rhs[2::3].sum() + 1.0) <= 1e-12 and abs(rhs[0::3].sum()) <= 1e-14
