@@ -36,6 +36,8 @@ CONFIGS = {
                workload="3D P2 Poisson tets, Kuhn 96^3 cube, stiffness + load (BASELINE.json config 3)"),
     "c4": dict(dim=3, degree=2, n=96, form="varcoef", quad=14,
                workload="3D P2 var-coef mass+stiffness+convection, Kuhn 96^3, 14-point rule (config 4)"),
+    "c5": dict(dim=3, degree=2, n=160, form="elasticity", quad=4, ncomp=3,
+               workload="3D vector P2 linear elasticity (lam=mu=1, f=(0,0,-1)), Kuhn 160^3, row blocks (config 5)"),
 }
 METRIC = "assembled elements/sec (3D P2 Poisson tets)"
 STEP_DESC = {
@@ -81,6 +83,9 @@ def model_flops(cfg):
     summed at compile time) are quoted with their symmetric count."""
     k = {(2, 1): 3, (2, 2): 6, (3, 1): 4, (3, 2): 10}[(cfg["dim"], cfg["degree"])]
     nq = {1: 1, 3: 3, 4: 4, 11: 11, 14: 14}.get(cfg["quad"], cfg["quad"])
+    if cfg["form"] == "elasticity":   # §8d C5: vector P2, 465 symmetric entries of the 30x30 element matrix
+        kk = 3 * k
+        return 60 + nq * (k * 15 + kk * (kk + 1) // 2 * 7 + 25 + 2 * kk)
     per_entry = {"poisson": 7, "stiffness": 7, "mass": 3, "helmholtz": 10, "demo2d": 10, "varcoef": 17}[cfg["form"]]
     entries = k * (k + 1) // 2 if cfg["form"] != "varcoef" else k * k
     return 60 + nq * (k * 15 + entries * per_entry + 25 + 2 * k)
@@ -162,7 +167,7 @@ def cpu_reference_sample(cfg, target_s=2.0):
     import pyoracle as po
 
     workers = os.cpu_count() or 1
-    n_s = 24 if cfg["dim"] == 3 else 256   # sample mesh of the same element type
+    n_s = (8 if cfg.get("ncomp", 1) > 1 else 24) if cfg["dim"] == 3 else 256   # sample mesh of the same element type
     if cfg["dim"] == 2:
         coords, vconn = po.unit_square_mesh(n_s)
         dconn, nd = vconn, coords.shape[0]
@@ -170,7 +175,16 @@ def cpu_reference_sample(cfg, target_s=2.0):
         coords, vconn = po.kuhn_mesh(n_s)
         dconn, nd = (vconn, coords.shape[0]) if cfg["degree"] == 1 else po.p2_dofs_kuhn(n_s, vconn)
     E = vconn.shape[0]
-    if po.ref_available() and not (cfg["dim"] == 2 and cfg["degree"] == 2):
+    if cfg.get("ncomp", 1) > 1:   # no reference implementation of vector forms: the C restatement
+        rp, ci = po.build_pattern(dconn, nd)
+        vrp, vci = po.block_pattern(rp, ci, cfg["ncomp"])
+        kind = "port"
+
+        def run(limit):
+            po.assemble_elasticity(cfg["dim"], cfg["degree"], cfg["quad"], coords, vconn[:limit], dconn[:limit],
+                                   vrp, vci)
+        workers = 1
+    elif po.ref_available() and not (cfg["dim"] == 2 and cfg["degree"] == 2):
         h = po.RefHarness(cfg["dim"], cfg["degree"], coords, vconn, dconn, nd, cfg["form"], cfg["quad"])
         kind = "reference"
 
@@ -269,14 +283,20 @@ def main():
         vconn_l, dconn_l = vconn, dconn
     ctx = ff.Context(local)
     ctx.set_scatter(args.scatter)
-    bil, lin = ff.named_form(cfg["form"], cfg["dim"])
+    ncomp = cfg.get("ncomp", 1)
     t = time.perf_counter()
-    form = ff.Form(ctx, cfg["dim"], cfg["degree"], bil, lin, quad_rule=cfg["quad"], strategy=args.strategy,
-                   block_size=args.block)
+    if ncomp > 1:   # vector P2 elasticity: 3x3 blocks of scalar forms
+        bb, bl = ff.elasticity_text(cfg["dim"])
+        form = ff.Form.blocked(ctx, cfg["dim"], cfg["degree"], ncomp, bb, bl, quad_rule=cfg["quad"],
+                               strategy=args.strategy)
+    else:
+        bil, lin = ff.named_form(cfg["form"], cfg["dim"])
+        form = ff.Form(ctx, cfg["dim"], cfg["degree"], bil, lin, quad_rule=cfg["quad"], strategy=args.strategy,
+                       block_size=args.block)
     compile_ms = 1e3 * (time.perf_counter() - t)
-    mesh = ff.Mesh(ctx, cfg["dim"], coords, vconn_l, None if cfg["degree"] == 1 else dconn_l, n_dofs)
+    mesh = ff.Mesh(ctx, cfg["dim"], coords, vconn_l, None if cfg["degree"] == 1 else dconn_l, n_dofs, ncomp=ncomp)
     t = time.perf_counter()
-    pat = ff.Pattern(ctx, mesh, rb, re)
+    pat = ff.Pattern(ctx, mesh, ncomp * rb, ncomp * re)
     pattern_ms = 1e3 * (time.perf_counter() - t)
     t = time.perf_counter()
     pat.prepare(mesh)
@@ -336,7 +356,10 @@ def main():
     # end to end through the public API: pinned host inputs -> H2D, pattern
     # re-validation, K0 + K2, D2H of values and rhs, every step
     e2e = None
-    if args.e2e_steps > 0:
+    e2e_note = None
+    if args.e2e_steps > 0 and pat.nnz * 8 * 2 > 120e9:   # pinned host + device copies of the values
+        e2e_note = f"e2e skipped: {pat.nnz * 8 / 1e9:.0f} GB of values per copy (run with --gpus 8: 1/8 per rank)"
+    elif args.e2e_steps > 0:
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
         hc, hv = pin(coords), pin(vconn_l)
         hd = pin(dconn_l) if cfg["degree"] > 1 else None
@@ -411,7 +434,7 @@ def main():
                      "kernel": KERNEL_DESC[scatter],
                      "bytes_per_launch": int(B), "peak_source": peak_src},
         "cpu_baseline": cpu,
-        "e2e": e2e,
+        "e2e": e2e if e2e is not None else ({"skipped": e2e_note} if e2e_note else None),
         "gpu_launches": (1 if scatter == "rowtile" else 2) * args.steps,  # ours only (flush is a torch fill)
         "clocks": clocks.summary(),
     }
