@@ -212,6 +212,29 @@ int ff_check(ff_ctx* ctx, ff_stats* stats);
 int ff_assemble(ff_form* form, ff_mesh* mesh, ff_pattern* p, const double* coords, const int32_t* vconn,
                 const int32_t* dconn, double* values_out, double* rhs_out, ff_stats* stats);
 
+/* ---- downstream consumer of the assembled system --------- */
+/* y = A x on the device, A the pattern's CSR with device values (replaces
+ * linalg::matvec(EllMatrix), linalg.cpp:35-49). */
+int ff_spmv(ff_pattern* p, const double* d_values, const double* d_x, double* d_y, void* stream);
+typedef struct ff_cg_result {
+  int iterations;
+  double residual; /* final relative residual ||r|| / ||b|| */
+  int converged;
+} ff_cg_result;
+/* Unpreconditioned CG on the device, the reference's algorithm and stopping
+ * rule (linalg.cpp:61-96): x0 = 0, stop when ||r|| <= tol ||b||. Breakdown
+ * (non-finite step / residual) fails with the reference's messages. */
+int ff_cg_solve(ff_pattern* p, const double* d_values, const double* d_b, double* d_x, double tol, int max_iter,
+                ff_cg_result* out);
+/* Host export of an assembled system in the reference's formats
+ * (linalg.cpp:148-210): MatrixMarket coordinate / CSV triplets, %.17g. */
+enum { FF_EXPORT_MATRIX_MARKET = 0, FF_EXPORT_CSV = 1 };
+int ff_export_matrix(ff_pattern* p, const double* values, const char* path, int fmt);
+int ff_export_vector(const double* b, int64_t n, const char* path, int fmt);
+/* Host-only export of caller CSR arrays (n rows) in the same formats. */
+int ff_export_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* values, const char* path,
+                  int fmt);
+
 /* ---- host helpers (CPU only; no device needed) --------------------------- */
 /* meshgen.cpp:13-33 unit square; SURVEY.md Appendix C Kuhn cube + P2 lattice. */
 int ff_unit_square_mesh(int n, double* coords, int32_t* conn);

@@ -174,6 +174,9 @@ def ref():
         L.ffref_assemble.argtypes = [C.c_void_p, C.c_int, C.c_int64, _f64p, _f64p]
         L.ffref_emit_demo_source.argtypes = [C.c_char_p, C.c_int64]
         L.ffref_max_threads.restype = C.c_int
+        L.ffref_export.argtypes = [C.c_void_p, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int]
+        L.ffref_cg.argtypes = [C.c_void_p, _f64p, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(C.c_int),
+                               C.POINTER(C.c_double)]
         _ref = L
     return _ref
 
@@ -230,6 +233,22 @@ class RefHarness:
             raise OracleError(self.L.ffref_last_error().decode())
         return vals, rhs
 
+
+    def export(self, values, rhs, mpath, vpath, fmt=0):
+        """The reference's export_matrix / export_vector of this 2D system."""
+        if ref().ffref_export(self.h, np.ascontiguousarray(values, np.float64), np.ascontiguousarray(rhs, np.float64),
+                              str(mpath).encode(), str(vpath).encode(), fmt) != 0:
+            raise OracleError(ref().ffref_last_error().decode())
+
+    def cg(self, values, rhs, tol=1e-10, max_iter=10000):
+        """The reference's cg_solve on this 2D system: (x, iterations, residual, converged)."""
+        x = np.empty(len(rhs))
+        it, res = C.c_int(0), C.c_double(0.0)
+        rc = ref().ffref_cg(self.h, np.ascontiguousarray(values, np.float64), np.ascontiguousarray(rhs, np.float64),
+                            tol, max_iter, x, C.byref(it), C.byref(res))
+        if rc < 0:
+            raise OracleError(ref().ffref_last_error().decode())
+        return x, it.value, res.value, rc == 0
     def __del__(self):
         if getattr(self, "h", None):
             self.L.ffref_destroy(self.h)

@@ -37,6 +37,7 @@
 #include "femforge/codegen/kernel.hpp"
 #include "femforge/device/device.hpp"
 #include "femforge/fem/fem.hpp"
+#include "femforge/linalg/linalg.hpp"
 #include "femforge/symbolic/expr.hpp"
 
 using namespace femforge;
@@ -417,5 +418,48 @@ int ffref_emit_demo_source(char* buf, std::int64_t cap) {
 }
 
 int ffref_max_threads() { return omp_get_max_threads(); }
+
+// The reference's own export (linalg::export_matrix(EllMatrix) / export_vector,
+// linalg.cpp:148-210) of a 2D system given as CSR values over the harness's
+// pattern. fmt 0: MatrixMarket, 1: CSV. Returns 0 / -1.
+int ffref_export(void* p, const double* values, const double* rhs, const char* mpath, const char* vpath, int fmt) {
+  auto* h = static_cast<Harness*>(p);
+  try {
+    if (h->dim != 2) throw std::runtime_error("export parity uses the 2D reference pipeline");
+    linalg::EllMatrix a(h->sp2.n, h->sp2.max_nz);
+    a.columns = h->sp2.row_cols;
+    for (int i = 0; i < h->sp2.n; ++i)
+      for (int k = 0; k < h->sp2.row_len[i]; ++k)
+        a.values[static_cast<std::size_t>(i) * h->sp2.max_nz + k] = values[h->row_ptr[i] + k];
+    const auto f = fmt == 0 ? linalg::ExportFormat::MatrixMarket : linalg::ExportFormat::Csv;
+    linalg::export_matrix(a, mpath, f);
+    linalg::export_vector(linalg::Vector(rhs, rhs + h->sp2.n), vpath, f);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1;
+  }
+}
+
+// The reference's cg_solve (linalg.cpp:61-96) on the same 2D system.
+int ffref_cg(void* p, const double* values, const double* rhs, double tol, int max_iter, double* x, int* iters,
+             double* residual) {
+  auto* h = static_cast<Harness*>(p);
+  try {
+    linalg::EllMatrix a(h->sp2.n, h->sp2.max_nz);
+    a.columns = h->sp2.row_cols;
+    for (int i = 0; i < h->sp2.n; ++i)
+      for (int k = 0; k < h->sp2.row_len[i]; ++k)
+        a.values[static_cast<std::size_t>(i) * h->sp2.max_nz + k] = values[h->row_ptr[i] + k];
+    linalg::CgResult r = linalg::cg_solve(a, linalg::Vector(rhs, rhs + h->sp2.n), tol, max_iter);
+    std::memcpy(x, r.x.data(), r.x.size() * sizeof(double));
+    *iters = r.iterations;
+    *residual = r.residual;
+    return r.converged ? 0 : 1;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1;
+  }
+}
 
 }  // extern "C"

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -1096,6 +1097,109 @@ int ff_assemble(ff_form* f, ff_mesh* m, ff_pattern* p, const double* coords, con
     ffb::cuda_check(cudaMemcpyAsync(rhs_out, p->e2e_rhs, n_rows * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "D2H");
     if (stats) stats->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// ---- downstream consumer ---------------------------------------------------
+
+int ff_spmv(ff_pattern* p, const double* d_values, const double* d_x, double* d_y, void* stream) {
+  return guarded([&] {
+    require(p && d_values && d_x && d_y, "ff_spmv: null argument");
+    bind(p->ctx);
+    ensure_device_csr(p);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->ctx->stream;
+    const int64_t n = p->bs * (p->re - p->rb);
+    ffb::cuda_check(ffb::kernels::spmv(p->bs == 1 ? p->row_ptr : p->vrow_ptr, p->bs == 1 ? p->col_idx : p->vcol_idx,
+                                       d_values, d_x, d_y, n, p->ctx->sm_count, s),
+                    "spmv");
+  });
+}
+
+int ff_cg_solve(ff_pattern* p, const double* d_values, const double* d_b, double* d_x, double tol, int max_iter,
+                ff_cg_result* out) {
+  return guarded([&] {
+    require(p && d_values && d_b && d_x, "ff_cg_solve: null argument");
+    require(p->rb == 0, "cg_solve needs the full system (row block starting at 0)");
+    bind(p->ctx);
+    ensure_device_csr(p);
+    const int64_t n = p->bs * (p->re - p->rb);
+    ffb::kernels::CgStats st;
+    ffb::cuda_check(ffb::kernels::cg_solve(p->bs == 1 ? p->row_ptr : p->vrow_ptr,
+                                           p->bs == 1 ? p->col_idx : p->vcol_idx, d_values, d_b, d_x, n, tol,
+                                           max_iter, p->ctx->sm_count, p->ctx->stream, &st),
+                    "cg_solve");
+    if (st.breakdown == 1) throw Error(FF_E_ARG, "cg_solve: breakdown (non-finite step)");
+    if (st.breakdown == 2) throw Error(FF_E_ARG, "cg_solve: breakdown (non-finite residual)");
+    if (out) {
+      out->iterations = st.iterations;
+      out->residual = st.residual;
+      out->converged = st.converged;
+    }
+  });
+}
+
+namespace {
+void write_value(std::FILE* f, double v) { std::fprintf(f, "%.17g", v); }
+struct OutFile {
+  std::FILE* f;
+  explicit OutFile(const char* path) : f(std::fopen(path, "w")) {
+    if (!f) throw Error(FF_E_ARG, std::string("cannot open '") + path + "' for writing");
+  }
+  ~OutFile() {
+    if (f) std::fclose(f);
+  }
+};
+}  // namespace
+
+int ff_export_matrix(ff_pattern* p, const double* values, const char* path, int fmt) {
+  return guarded([&] {
+    require(p && values && path, "ff_export_matrix: null argument");
+    const int64_t n = p->bs * (p->re - p->rb), nnz = int64_t(p->bs) * p->bs * p->nnz;
+    std::vector<int64_t> rp(n + 1);
+    std::vector<int32_t> ci(std::max<int64_t>(nnz, 1));
+    if (ff_pattern_export(p, rp.data(), ci.data()) != FF_OK) throw Error(FF_E_CUDA, g_error);
+    if (ff_export_csr(n, rp.data(), ci.data(), values, path, fmt) != FF_OK) throw Error(FF_E_ARG, g_error);
+  });
+}
+
+int ff_export_csr(int64_t n, const int64_t* rp, const int32_t* ci, const double* values, const char* path, int fmt) {
+  return guarded([&] {
+    require(rp && ci && values && path && n >= 0, "ff_export_csr: null argument");
+    require(fmt == FF_EXPORT_MATRIX_MARKET || fmt == FF_EXPORT_CSV, "unknown export format");
+    const int64_t nnz = rp[n];
+    OutFile fh(path);
+    // linalg.cpp:170-199: rows in order, sorted columns (the ELL order without padding)
+    if (fmt == FF_EXPORT_MATRIX_MARKET) {
+      std::fprintf(fh.f, "%%%%MatrixMarket matrix coordinate real general\n%lld %lld %lld\n",
+                   static_cast<long long>(n), static_cast<long long>(n), static_cast<long long>(nnz));
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+          std::fprintf(fh.f, "%lld %d ", static_cast<long long>(i + 1), ci[k] + 1);
+          write_value(fh.f, values[k]);
+          std::fputc('\n', fh.f);
+        }
+    } else {
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+          std::fprintf(fh.f, "%lld,%d,", static_cast<long long>(i), ci[k]);
+          write_value(fh.f, values[k]);
+          std::fputc('\n', fh.f);
+        }
+    }
+  });
+}
+
+int ff_export_vector(const double* b, int64_t n, const char* path, int fmt) {
+  return guarded([&] {
+    require(b && path && n >= 0, "ff_export_vector: null argument");
+    require(fmt == FF_EXPORT_MATRIX_MARKET || fmt == FF_EXPORT_CSV, "unknown export format");
+    OutFile fh(path);
+    if (fmt == FF_EXPORT_MATRIX_MARKET)
+      std::fprintf(fh.f, "%%%%MatrixMarket matrix array real general\n%lld 1\n", static_cast<long long>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      write_value(fh.f, b[i]);
+      std::fputc('\n', fh.f);
+    }
   });
 }
 

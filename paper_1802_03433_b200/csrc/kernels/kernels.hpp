@@ -94,6 +94,19 @@ cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_ou
 cudaError_t expand_block_pattern(const int64_t* rp_s, const int32_t* ci_s, int64_t n_rows, int bs, int64_t* rp_v,
                                  int32_t* ci_v, int sm_count, cudaStream_t s);
 
+// Downstream consumer (linalg.cu): y = A x (warp per row) and the reference's
+// unpreconditioned CG (linalg.cpp:61-96) with deterministic reductions.
+struct CgStats {
+  int iterations = 0;
+  double residual = 0.0;
+  int converged = 0;
+  int breakdown = 0;  // 1: non-finite step, 2: non-finite residual
+};
+cudaError_t spmv(const int64_t* rp, const int32_t* ci, const double* a, const double* x, double* y, int64_t n,
+                 int sm_count, cudaStream_t s);
+cudaError_t cg_solve(const int64_t* rp, const int32_t* ci, const double* a, const double* b, double* x, int64_t n,
+                     double tol, int max_iter, int sm_count, cudaStream_t s, CgStats* st);
+
 // K0: values[0:na] = 0, rhs[0:nb] = 0, status[0:2] = ~0 (one launch).
 cudaError_t zero_fill(double* a, int64_t na, double* b, int64_t nb, unsigned long long* status, int sm_count,
                       cudaStream_t s);

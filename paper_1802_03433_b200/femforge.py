@@ -81,6 +81,10 @@ class GatherInfo(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class CgResult(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("residual", C.c_double), ("converged", C.c_int)]
+
+
 class Stats(C.Structure):
     _fields_ = [("bad_element", C.c_int64), ("bad_row", C.c_int64), ("ms", C.c_double)]
 
@@ -129,6 +133,11 @@ SIGNATURES = [
     ("ff_assemble_device_ex", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint]),
     ("ff_check", C.c_int, [_P, C.POINTER(Stats)]),
     ("ff_assemble", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, C.POINTER(Stats)]),
+    ("ff_spmv", C.c_int, [_P, _P, _P, _P, _P]),
+    ("ff_cg_solve", C.c_int, [_P, _P, _P, _P, C.c_double, C.c_int, C.POINTER(CgResult)]),
+    ("ff_export_matrix", C.c_int, [_P, _f64p, C.c_char_p, C.c_int]),
+    ("ff_export_vector", C.c_int, [_f64p, _i64, C.c_char_p, C.c_int]),
+    ("ff_export_csr", C.c_int, [_i64, _i64p, _i32p, _f64p, C.c_char_p, C.c_int]),
     ("ff_unit_square_mesh", C.c_int, [C.c_int, _f64p, _i32p]),
     ("ff_kuhn_mesh", C.c_int, [C.c_int, _f64p, _i32p]),
     ("ff_kuhn_p2_dofs", C.c_int, [C.c_int, _i32p, _i64, _i32p]),
@@ -406,6 +415,41 @@ def assemble(form, mesh, pattern, coords=None, vconn=None, dconn=None, values=No
     _ok(lib().ff_assemble(form.h, mesh.h, pattern.h, _ptr(coords), _ptr(vconn), _ptr(dconn), _ptr(values), _ptr(rhs),
                           C.byref(st)))
     return values, rhs
+
+
+# ---- downstream consumer ---------------------------------
+
+EXPORT_FORMAT = {"matrix_market": 0, "csv": 1}
+
+
+def spmv(pattern, values_ptr, x_ptr, y_ptr, stream=None):
+    """y = A x on the device (linalg::matvec, linalg.cpp:35-49)."""
+    _ok(lib().ff_spmv(pattern.h, C.c_void_p(values_ptr), C.c_void_p(x_ptr), C.c_void_p(y_ptr), _stream(stream)))
+
+
+def cg_solve(pattern, values_ptr, b_ptr, x_ptr, tol=1e-10, max_iter=10000):
+    """The reference's unpreconditioned CG (linalg.cpp:61-96) on the device.
+    Returns {iterations, residual, converged}; x is written in place."""
+    r = CgResult()
+    _ok(lib().ff_cg_solve(pattern.h, C.c_void_p(values_ptr), C.c_void_p(b_ptr), C.c_void_p(x_ptr), tol, max_iter,
+                          C.byref(r)))
+    return {"iterations": r.iterations, "residual": r.residual, "converged": bool(r.converged)}
+
+
+def export_matrix(pattern, values, path, fmt="matrix_market"):
+    _ok(lib().ff_export_matrix(pattern.h, np.ascontiguousarray(values, np.float64), str(path).encode(),
+                               EXPORT_FORMAT[fmt]))
+
+
+def export_vector(b, path, fmt="matrix_market"):
+    b = np.ascontiguousarray(b, np.float64)
+    _ok(lib().ff_export_vector(b, b.size, str(path).encode(), EXPORT_FORMAT[fmt]))
+
+
+def export_csr(row_ptr, col_idx, values, path, fmt="matrix_market"):
+    _ok(lib().ff_export_csr(len(row_ptr) - 1, np.ascontiguousarray(row_ptr, np.int64),
+                            np.ascontiguousarray(col_idx, np.int32), np.ascontiguousarray(values, np.float64),
+                            str(path).encode(), EXPORT_FORMAT[fmt]))
 
 
 # ---- host helpers -----------------------------------------------------------

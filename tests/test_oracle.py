@@ -146,3 +146,23 @@ def test_elasticity_oracle_rigid_body_modes(n):
         assert np.abs(K @ u).max() <= 1e-12 * scale
     assert abs(K - K.T).max() <= 1e-14 * scale
     assert abs(rhs[1::3].sum() - 1.0) <= 1e-12 and abs(rhs[2::3].sum() + 1.0) <= 1e-12 and abs(rhs[0::3].sum()) <= 1e-14
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="needs oracle/_ref")
+@pytest.mark.parametrize("fmt", ["matrix_market", "csv"])
+def test_export_matches_reference_bytes(fmt, tmp_path):
+    """ff_export_csr / ff_export_vector write exactly what the reference's
+    linalg::export_matrix(EllMatrix) / export_vector write (linalg.cpp:148-210)."""
+    from paper_1802_03433_b200 import femforge as ff
+    xy, conn = po.unit_square_mesh(4)
+    h = po.RefHarness(2, 1, xy, conn, conn, xy.shape[0], "demo2d")
+    rp, ci = h.pattern()
+    v, b = h.assemble()
+    code = {"matrix_market": 0, "csv": 1}[fmt]
+    h.export(v, b, tmp_path / "ref.mtx", tmp_path / "ref_b.mtx", code)
+    ff.export_csr(rp, ci, v, tmp_path / "ours.mtx", fmt)
+    ff.export_vector(b, tmp_path / "ours_b.mtx", fmt)
+    assert (tmp_path / "ours.mtx").read_bytes() == (tmp_path / "ref.mtx").read_bytes()
+    assert (tmp_path / "ours_b.mtx").read_bytes() == (tmp_path / "ref_b.mtx").read_bytes()
+    if fmt == "matrix_market":
+        assert (tmp_path / "ours.mtx").read_text().splitlines()[1] == f"25 25 {len(ci)}"
