@@ -15,7 +15,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 INC      := -I$(SRC)/include -Iinclude -I$(CUDA)/include
 CXXFLAGS := -std=c++20 -O2 -g -fPIC -Wall -Wextra $(INC)
 NVFLAGS  := $(ARCH) -lineinfo -O3 -std=c++17 -Xcompiler -fPIC $(INC)
-LDLIBS   := -L$(CUDA)/lib64 -lcudart_static -lnvrtc -lrt -ldl -lpthread -Wl,-rpath,$(CUDA)/lib64
+LDLIBS   := -L$(CUDA)/lib64 -lcudart_static -lrt -ldl -lpthread -Wl,-rpath,$(CUDA)/lib64
 
 CPP_SRCS := $(SRC)/symbolic/symbolic.cpp $(SRC)/fem/fem.cpp $(SRC)/meshgen/meshgen.cpp \
             $(SRC)/codegen/lower.cpp $(SRC)/codegen/element_plan.cpp $(SRC)/codegen/emit.cpp \

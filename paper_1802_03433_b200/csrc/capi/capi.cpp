@@ -392,8 +392,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
                     "K2 (window row gather) launch");
     return;
   }
-  const int erec = (f->plan.n_kinv + m->k + 1) & ~1;  // FF_EREC
-  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * erec;
+  const int gs = ((f->plan.n_kinv + 3) / 4) * 4;  // FF_GS: invariants [E][gs] + load vectors [k][E]
+  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * (gs + m->k);
   if (p->ginv_cap < ng) {
     cudaFree(p->ginv);
     p->ginv = nullptr;
@@ -439,12 +439,13 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       const int64_t ipw = ipw_env ? std::max(1, std::atoi(ipw_env)) : 4;
       const unsigned grid = static_cast<unsigned>((i1 - i0 + 4 * ipw - 1) / (4 * ipw));  // 4 warps x FF_IPW items
       const double* ginv = p->ginv;
+      long long ne_arg = m->ne;
       const int64_t* row_ptr = p->row_ptr;
       const int32_t* icls = gp.citem_class;
       const int32_t* irows = gp.citem_rows;
       const int64_t* irec = gp.citem_rec;
       const int32_t* crec = gp.crec;
-      void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
+      void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(128), args,
                                        0, sc),
                       "K2b (class row gather) launch");
@@ -468,13 +469,15 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     const int64_t per_cta = int64_t(kGatherWarps) * 4;
     const unsigned grid = static_cast<unsigned>((i1 - i0 + per_cta - 1) / per_cta);
     const double* ginv = p->ginv;
+    long long ne_arg = m->ne;
     const int64_t* row_ptr = p->row_ptr;
     const int32_t* order = gp.item_order;
     const int32_t* wrows = gp.warp_rows;
     const int32_t* wsteps = gp.warp_steps;
     const int64_t* wrec = gp.warp_rec;
     const void* rec = gp.rec;
-    void* args[] = {&ginv, &row_ptr, &d_values, &d_rhs, &order, &i0, &i1, &wrows, &wsteps, &wrec, &rec, &pitch};
+    void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &order, &i0, &i1, &wrows, &wsteps, &wrec, &rec,
+                    &pitch};
     ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
                                      dim3(kGatherWarps * 32), args, smem, s),
                     "K2b (row gather) launch");

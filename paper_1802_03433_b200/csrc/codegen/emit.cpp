@@ -102,22 +102,24 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
         "// every class row stays in registers, indexed by compile-time slots.\n"
         "typedef long long ff_i64;\ntypedef int ff_i32;\n"
      << "#define FF_NLOC " << n_local << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
-     << "\n#define FF_EREC " << erec << "\n"
+     << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((plan.n_kinv + 3) / 4) * 4 << "\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
-__device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, double (&g)[FF_NKP],
-                                         double& b) {
+__device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+// element record: invariants [E][FF_GS] (256-bit loads), load vector [FF_NLOC][E]
+__device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, ff_i64 n_elems,
+                                         double (&g)[FF_NKP], double& b) {
   if (e >= 0) {
-    const double* base = einv + (ff_i64)e * FF_EREC;
-    const double2* g2 = (const double2*)base;
+    const double* base = einv + (ff_i64)e * FF_GS;
+    double t[FF_GS];
 #pragma unroll
-    for (int q = 0; q < FF_NKP / 2; ++q) {
-      const double2 t = __ldg(g2 + q);
-      g[2 * q] = t.x;
-      g[2 * q + 1] = t.y;
-    }
-    b = __ldg(base + FF_NKINV + i);
+    for (int q = 0; q < FF_GS / 4; ++q) ff_ld4(base + 4 * q, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+#pragma unroll
+    for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
+    b = __ldg(einv + n_elems * FF_GS + (ff_i64)i * n_elems + e);
   } else {
 #pragma unroll
     for (int q = 0; q < FF_NKP; ++q) g[q] = 0.0;
@@ -157,7 +159,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
     const RowClass& k = classes[c];
     os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
        << "__device__ __forceinline__ void ff_cls_" << c
-       << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv,\n"
+       << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv, ff_i64 n_elems,\n"
           "    double* __restrict__ st, ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row,\n"
           "    double* __restrict__ values, double* __restrict__ rhs) {\n"
           "  int e[" << std::max(k.steps, 1) << "];\n";
@@ -174,7 +176,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
       const int s1 = std::min(k.steps, s0 + depth);
       os << "  {\n";
       for (int q = s0; q < s1; ++q)
-        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] << ", einv, g" << q
+        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] << ", einv, n_elems, g" << q
            << ", b" << q << ");\n";
       for (int q = s0; q < s1; ++q) {
         os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);";
@@ -205,7 +207,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
           "// compact (element data reused in L1/L2)\n"
           "extern \"C\" __global__ void __launch_bounds__(128, "
        << (longrows ? "FF_MINB_L" : "FF_MINB_S") << ")\n" << name
-       << "(const double* __restrict__ einv, const ff_i64* __restrict__ row_ptr,\n"
+       << "(const double* __restrict__ einv, ff_i64 n_elems, const ff_i64* __restrict__ row_ptr,\n"
           "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
           "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
           "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
@@ -229,7 +231,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
           "    switch (c) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
-        os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, st, sr, lane, rbeg, row, values, rhs); break;\n";
+        os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
     os << "      default: break;\n    }\n  }\n}\n";
   };
   kernel("ff_gather_classes_s", false);
