@@ -281,7 +281,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
     rc.push_back(std::move(r));
   }
   const auto t0 = std::chrono::steady_clock::now();
-  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc);
+  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, std::getenv("FF_FUSED_CLASSES") != nullptr);
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
   for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L"})
     if (const char* v = std::getenv(knob))
@@ -329,7 +329,8 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
-                                                        std::getenv("FF_WINDOWS") ? kWindowMaxElems : 0);
+                                                        std::getenv("FF_WINDOWS") ? kWindowMaxElems : 0,
+                                                        !std::getenv("FF_FUSED_CLASSES"));
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");

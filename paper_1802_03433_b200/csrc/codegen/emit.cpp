@@ -93,7 +93,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
 }
 
 
-std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes) {
+std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes, bool fused) {
   if (plan.n_kinv <= 0) throw CodegenError("row classes need a reference-tensor plan");
   std::ostringstream os;
   const int nkp = plan.n_kinv + (plan.n_kinv & 1);
@@ -153,10 +153,13 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
 #define FF_MINB_L 2
 #endif
 )";
-  // class c with rows of <= 33 entries -> ff_gather_classes_s, else _l
-  auto is_long = [&](int c) { return classes[c].len > 33; };
+  // class c with rows of <= 33 entries -> ff_gather_classes_s, else _l; fused:
+  // every class in _s, rows longer than 33 entries in slot-range passes
+  auto is_long = [&](int c) { return !fused && classes[c].len > 33; };
   auto class_fn = [&](int c) {
     const RowClass& k = classes[c];
+    const int n_pass = fused ? std::max(1, (k.len + 32) / 33) : 1;
+    const int per = (k.len + n_pass - 1) / n_pass;
     os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
        << "__device__ __forceinline__ void ff_cls_" << c
        << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv, ff_i64 n_elems,\n"
@@ -169,29 +172,39 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
       else
         os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
     }
-    for (int p = 0; p < k.len; ++p) os << "  double a" << p << " = 0.0;\n";
     os << "  double bs = 0.0;\n";
+    os << "  sr[lane] = row >= 0 ? rbeg : -1;\n";
     const int depth = is_long(c) ? 4 : 8;
-    for (int s0 = 0; s0 < k.steps; s0 += depth) {
-      const int s1 = std::min(k.steps, s0 + depth);
-      os << "  {\n";
-      for (int q = s0; q < s1; ++q)
-        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] << ", einv, n_elems, g" << q
-           << ", b" << q << ");\n";
-      for (int q = s0; q < s1; ++q) {
-        os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);";
-        for (int j = 0; j < n_local; ++j) os << " a" << int(k.slots[q * n_local + j]) << " += v[" << j << "];";
-        os << " bs += b" << q << "; }\n";
+    for (int ps = 0; ps < n_pass; ++ps) {
+      const int lo = ps * per, hi = std::min(k.len, lo + per);
+      os << "  {  // slots [" << lo << ", " << hi << ")\n";
+      for (int p = lo; p < hi; ++p) os << "  double a" << p << " = 0.0;\n";
+      for (int s0 = 0; s0 < k.steps; s0 += depth) {
+        const int s1 = std::min(k.steps, s0 + depth);
+        os << "  {\n";
+        for (int q = s0; q < s1; ++q)
+          os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q]
+             << ", einv, n_elems, g" << q << ", b" << q << ");\n";
+        for (int q = s0; q < s1; ++q) {
+          std::string adds;
+          for (int j = 0; j < n_local; ++j) {
+            const int sl = k.slots[q * n_local + j];
+            if (sl >= lo && sl < hi) adds += " a" + std::to_string(sl) + " += v[" + std::to_string(j) + "];";
+          }
+          if (!adds.empty())
+            os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);" << adds << " }\n";
+          if (ps == 0) os << "    bs += b" << q << ";\n";
+        }
+        os << "  }\n";
+      }
+      // write-out through the staging rows (consecutive lanes = consecutive
+      // CSR values of one row)
+      for (int q0 = lo; q0 < hi; q0 += 32) {
+        const int cnt = std::min(32, hi - q0);
+        for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
+        os << "  ff_writeout(st, sr, lane, " << cnt << ", " << q0 << ", values);\n";
       }
       os << "  }\n";
-    }
-    // write-out through the staging rows: flat index f over the 32 rows x cnt
-    // slots (consecutive lanes = consecutive CSR values of one row)
-    os << "  sr[lane] = row >= 0 ? rbeg : -1;\n";
-    for (int q0 = 0; q0 < k.len; q0 += 32) {
-      const int cnt = std::min(32, k.len - q0);
-      for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
-      os << "  ff_writeout(st, sr, lane, " << cnt << ", " << q0 << ", values);\n";
     }
     os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
   };

@@ -162,7 +162,8 @@ struct RowClass {
 // NVRTC translation unit with ff_gather_classes_s (classes of rows <= 33
 // entries) and ff_gather_classes_l (longer rows). Needs a gather-capable
 // plan (plan.n_kinv > 0). Byte-deterministic.
-std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes);
+std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes,
+                              bool fused = false);
 
 // The window row-gather kernel (ff_gather_windows) appended to the form's own
 // translation unit (it reuses the form's geometry and element body).

@@ -82,7 +82,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64,
-                              bool use_eorder = true, int max_win_elems = 0);
+                              bool use_eorder = true, int max_win_elems = 0, bool split_long = true);
 void free_gather_plan(GatherPlan* p);
 
 // Order-independent 64-bit content hash of n int32 values (sum of mixed

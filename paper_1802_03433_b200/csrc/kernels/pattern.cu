@@ -751,7 +751,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes,
-                              bool use_eorder, int max_win_elems) {
+                              bool use_eorder, int max_win_elems, bool split_long) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   const int cap = sm_count * 16;
@@ -955,7 +955,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     }
     // short-row classes (<= 33 entries) first, then long-row ones: two
     // specialised kernels with their own register budgets
-    auto longrows = [&](const Item& it) { return out->classes[it.c].len > 33 ? 1 : 0; };
+    auto longrows = [&](const Item& it) { return split_long && out->classes[it.c].len > 33 ? 1 : 0; };
     // within each, by (Morton window of 4096 rows, class, position): the 16
     // items a CTA takes are of one class (one instruction footprint per CTA)
     auto win = [&](const Item& it) { return it.key / 4096; };
