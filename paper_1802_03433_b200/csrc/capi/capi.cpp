@@ -281,7 +281,11 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
     rc.push_back(std::move(r));
   }
   const auto t0 = std::chrono::steady_clock::now();
-  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, std::getenv("FF_FUSED_CLASSES") != nullptr);
+  // one fused kernel (long rows in slot-range passes) unless FF_SPLIT_CLASSES:
+  // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
+  const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
+  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused);
+  if (fused && !std::getenv("FF_MINB_S")) src = "#define FF_MINB_S 3\n" + src;
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
   for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L"})
     if (const char* v = std::getenv(knob))
@@ -330,7 +334,7 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
                                                         std::getenv("FF_WINDOWS") ? kWindowMaxElems : 0,
-                                                        !std::getenv("FF_FUSED_CLASSES"));
+                                                        std::getenv("FF_SPLIT_CLASSES") != nullptr);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
