@@ -106,9 +106,21 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
+#ifdef FF_EINV_NA  // element records streamed past L1 (no allocation)
+__device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ double ff_ld1(const double* p) {
+  double a;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(a) : "l"(p));
+  return a;
+}
+#else
 __device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, double& c, double& d) {
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
+__device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
+#endif
 // element record: invariants [E][FF_GS] (256-bit loads), load vector [FF_NLOC][E]
 __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, ff_i64 n_elems,
                                          double (&g)[FF_NKP], double& b) {
@@ -119,7 +131,7 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
     for (int q = 0; q < FF_GS / 4; ++q) ff_ld4(base + 4 * q, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
 #pragma unroll
     for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
-    b = __ldg(einv + n_elems * FF_GS + (ff_i64)i * n_elems + e);
+    b = ff_ld1(einv + n_elems * FF_GS + (ff_i64)i * n_elems + e);
   } else {
 #pragma unroll
     for (int q = 0; q < FF_NKP; ++q) g[q] = 0.0;
