@@ -443,7 +443,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       long long i0 = cr[c][0], i1 = cr[c][1];
       if (i1 <= i0) continue;
       const char* ipw_env = std::getenv("FF_IPW");
-      const int64_t ipw = ipw_env ? std::max(1, std::atoi(ipw_env)) : 4;
+      const int64_t ipw = ipw_env ? std::max(1, std::atoi(ipw_env)) : 2;
       const unsigned grid = static_cast<unsigned>((i1 - i0 + 4 * ipw - 1) / (4 * ipw));  // 4 warps x FF_IPW items
       const double* ginv = p->ginv;
       long long ne_arg = m->ne;

@@ -156,7 +156,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
   __syncwarp();
 }
 #ifndef FF_IPW
-#define FF_IPW 4  // consecutive items per warp
+#define FF_IPW 2  // consecutive items per warp
 #endif
 #ifndef FF_MINB_S
 #define FF_MINB_S 4  // CTAs per SM the register budgets are sized for
