@@ -244,20 +244,33 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
           "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * FF_IPW;\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
-          "  for (ff_i64 w = first; w < last; ++w) {\n"
-          "    const int c = __ldg(citem_class + w);\n"
-          "    const int row = __ldg(citem_rows + w * 32 + lane);\n"
-          "    const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
-          "    int ep[FF_PRE];\n"
-          "    const int ns = ff_csteps[c];\n"
+          "  // the next item's header and first records load while this item computes\n"
+          "  // (the record array is padded by FF_PRE steps, so the loads need no bound)\n"
+          "  int c = __ldg(citem_class + first);\n"
+          "  int row = __ldg(citem_rows + first * 32 + lane);\n"
+          "  const ff_i32* rec = crec + __ldg(citem_rec + first) * 32 + lane;\n"
+          "  int ep[FF_PRE];\n"
           "#pragma unroll\n"
-          "    for (int u = 0; u < FF_PRE; ++u) ep[u] = u < ns ? __ldcs(rec + u * 32) : -1;\n"
+          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(rec + u * 32);\n"
+          "  for (ff_i64 w = first; w < last; ++w) {\n"
+          "    int cn = 0, rown = -1, epn[FF_PRE];\n"
+          "    const ff_i32* recn = rec;\n"
+          "    if (w + 1 < last) {\n"
+          "      cn = __ldg(citem_class + w + 1);\n"
+          "      rown = __ldg(citem_rows + (w + 1) * 32 + lane);\n"
+          "      recn = crec + __ldg(citem_rec + w + 1) * 32 + lane;\n"
+          "#pragma unroll\n"
+          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = __ldcs(recn + u * 32);\n"
+          "    }\n"
           "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
           "    switch (c) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
         os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
-    os << "      default: break;\n    }\n  }\n}\n";
+    os << "      default: break;\n    }\n"
+          "    c = cn;\n    row = rown;\n    rec = recn;\n"
+          "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
+          "  }\n}\n";
   };
   kernel("ff_gather_classes_s", false);
   kernel("ff_gather_classes_l", true);

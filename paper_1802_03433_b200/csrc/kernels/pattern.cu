@@ -994,8 +994,9 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       if ((err = cudaMalloc(&out->citem_class, nci * sizeof(int32_t))) != cudaSuccess) return done(err);
       if ((err = cudaMalloc(&out->citem_rows, nci * 32 * sizeof(int32_t))) != cudaSuccess) return done(err);
       if ((err = cudaMalloc(&out->citem_rec, (nci + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
-      if ((err = cudaMalloc(&out->crec, std::max<int64_t>(out->n_crec, 1) * sizeof(int32_t))) != cudaSuccess)
-        return done(err);
+      // padded by 8 steps: the class kernel prefetches 8 records per item without a bound
+      if ((err = cudaMalloc(&out->crec, (out->n_crec + 8 * 32) * sizeof(int32_t))) != cudaSuccess) return done(err);
+      cudaMemsetAsync(out->crec + out->n_crec, 0xff, 8 * 32 * sizeof(int32_t), s);
       if ((err = cudaMalloc(&d_steps, cls_steps.size() * sizeof(int32_t))) != cudaSuccess) return done(err);
       cudaMemcpyAsync(out->citem_class, ic.data(), nci * sizeof(int32_t), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(out->citem_rows, ir.data(), nci * 32 * sizeof(int32_t), cudaMemcpyHostToDevice, s);
