@@ -267,9 +267,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # FF_BENCH_SHARE_GPU=1 (testing only): several ranks on one GPU over gloo,
+    # to exercise the multi-rank path where only one device is available
+    share = os.environ.get("FF_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1802_03433_b200 import femforge as ff
     from paper_1802_03433_b200 import rowblocks
 
@@ -348,7 +356,7 @@ def main():
     step_ms = float(np.mean([a.elapsed_time(c) for a, b, c in ev]))
     k0_ms = float(np.mean([a.elapsed_time(b) for a, b, c in ev]))
     k2_ms = float(np.mean([b.elapsed_time(c) for a, b, c in ev]))
-    times = torch.tensor([step_ms, k0_ms, k2_ms], dtype=torch.float64, device="cuda")
+    times = torch.tensor([step_ms, k0_ms, k2_ms], dtype=torch.float64, device="cpu" if share else "cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
     step_ms, k0_ms, k2_ms = times.tolist()
@@ -371,7 +379,8 @@ def main():
         t = time.perf_counter()
         for _ in range(args.e2e_steps):
             ff.assemble(form, mesh, pat, hc, hv, hd, hval, hrhs)
-        e2e_s = torch.tensor([(time.perf_counter() - t) / args.e2e_steps], dtype=torch.float64, device="cuda")
+        e2e_s = torch.tensor([(time.perf_counter() - t) / args.e2e_steps], dtype=torch.float64,
+                             device="cpu" if share else "cuda")
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         h2d = hc.nbytes + hv.nbytes + (hd.nbytes if hd is not None else 0)

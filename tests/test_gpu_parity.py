@@ -411,3 +411,26 @@ def test_elasticity_rigid_body_modes_and_row_blocks(ff, ctx):
     assert np.array_equal(rp_cat, rp) and np.array_equal(np.concatenate([x[1] for x in pieces]), ci)
     assert normwise(np.concatenate([x[2] for x in pieces]), val) <= TOL
     assert normwise(np.concatenate([x[3] for x in pieces]), rhs) <= TOL
+
+
+def test_bench_two_ranks_on_one_gpu(ff):
+    """The multi-rank bench path (row blocks, halo elements, global nnz, max
+    over ranks) with 2 ranks sharing the one GPU over gloo: one JSON line, the
+    whole-job nnz equal to the 1-rank pattern's."""
+    import json
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FF_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c3",
+           "--n", "16", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    n = 16
+    assert d["n_gpus"] == 2 and d["config"]["nnz"] == 230 * n ** 3 + 138 * n ** 2 + 24 * n + 1
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
