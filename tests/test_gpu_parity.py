@@ -434,3 +434,27 @@ def test_bench_two_ranks_on_one_gpu(ff):
     n = 16
     assert d["n_gpus"] == 2 and d["config"]["nnz"] == 230 * n ** 3 + 138 * n ** 2 + 24 * n + 1
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+@pytest.mark.parametrize("deg", [1, 2])
+def test_jittered_permuted_mesh(ff, ctx, deg):
+    """SURVEY §8d stress variant (seed 42, as test_device.cpp:219): interior
+    vertices jittered by <= 0.1 h (orientation kept), elements randomly
+    permuted (no element-order locality). Sparsity bit-exact, values <= 1e-12
+    against the oracle, through the default row gather."""
+    n = 10
+    c, v = ff.kuhn_mesh(n)
+    rng = np.random.default_rng(42)
+    h = 1.0 / n
+    interior = np.all((c > 1e-12) & (c < 1 - 1e-12), axis=1)
+    c = c.copy()
+    c[interior] += rng.uniform(-0.1 * h, 0.1 * h, size=(interior.sum(), 3))
+    perm = rng.permutation(v.shape[0])
+    v = np.ascontiguousarray(v[perm])
+    d, nd = (v, c.shape[0]) if deg == 1 else ff.kuhn_p2_dofs(n, v)
+    rp, ci, val, rhs, f, m, p = gpu_system(ff, ctx, 3, deg, "helmholtz", c, v, d, nd, quad=4, scatter="gather")
+    assert p.scatter_for(f) == "gather"
+    orp, oci = po.build_pattern(d, nd)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    ov, ob = po.assemble("helmholtz", 3, deg, 4, c, v, d, orp, oci, workers=8)
+    assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
