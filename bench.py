@@ -247,7 +247,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="ns", choices=sorted(CONFIGS))
-    ap.add_argument("--n", type=int, default=0, help="override mesh resolution")
+    ap.add_argument("--size", "--n", dest="n", type=int, default=0, help="override mesh resolution")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-step-s", type=float, default=2.0)

@@ -425,7 +425,7 @@ def test_bench_two_ranks_on_one_gpu(ff):
     env = dict(os.environ, FF_BENCH_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
            "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c3",
-           "--n", "16", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+           "--size", "16", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
