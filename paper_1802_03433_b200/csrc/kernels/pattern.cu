@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <unordered_map>
 #include <vector>
 
@@ -877,7 +878,9 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     // classes worth a specialised kernel: >= min_class_rows rows and >= 0.5 %
     // of the block (boundary classes stay generic: smaller code, fewer
     // instruction-cache misses)
-    const int64_t min_rows = std::max<int64_t>(min_class_rows, n_rows / 200);
+    const char* frac_env = std::getenv("FF_CLASS_FRAC");  // tuning knob, default 0.5 %
+    const double frac = frac_env ? std::atof(frac_env) : 0.005;
+    const int64_t min_rows = std::max<int64_t>(min_class_rows, static_cast<int64_t>(frac * n_rows));
     for (const auto& [h, v] : count)
       if (v.first >= min_rows) big.push_back({v.first, h});
     std::sort(big.begin(), big.end(), [&](const auto& a, const auto& b) {
