@@ -426,6 +426,45 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   }
   if (flags & FF_GATHER_INVARIANTS_ONLY) return;
   const ffb::kernels::GatherPlan& gp = p->gather;
+  // the generic rows run on the side stream, concurrently with the class
+  // kernel (disjoint rows, both only read the element records): 2.861 ->
+  // 2.846 ms at the north star (run 34)
+  const bool generic_side = gp.n_citems > 0 && gp.n_items > 0 && !std::getenv("FF_GENERIC_SERIAL");
+  if (generic_side) {
+    ffb::cuda_check(cudaEventRecord(ctx->fork, s), "fork");
+    ffb::cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
+  }
+  const cudaStream_t sg = generic_side ? ctx->side : s;
+  auto launch_generic = [&]() {
+    // K2b for the remaining rows in two launches: short-pitch items, then long-pitch items
+    const int64_t ranges[2][2] = {{0, gp.n_short}, {gp.n_short, gp.n_items}};
+    const int pitches[2] = {gp.pitch_short, gp.pitch_long};
+    for (int c = 0; c < 2; ++c) {
+      long long i0 = ranges[c][0], i1 = ranges[c][1];
+      if (i1 <= i0) continue;
+      int pitch = pitches[c];
+      const int smem = gather_smem(pitch);
+      require(smem <= kGatherSmemMax, "row gather: rows too long for the shared-memory accumulators");
+      // a few items per warp (grid-stride): CTAs run in item order, so the items
+      // in flight stay contiguous and their element data stays in L2
+      const int64_t per_cta = int64_t(kGatherWarps) * 4;
+      const unsigned grid = static_cast<unsigned>((i1 - i0 + per_cta - 1) / per_cta);
+      const double* ginv = p->ginv;
+      long long ne_arg = m->ne;
+      const int64_t* row_ptr = p->row_ptr;
+      const int32_t* order = gp.item_order;
+      const int32_t* wrows = gp.warp_rows;
+      const int32_t* wsteps = gp.warp_steps;
+      const int64_t* wrec = gp.warp_rec;
+      const void* rec = gp.rec;
+      void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &order, &i0, &i1, &wrows, &wsteps, &wrec, &rec,
+                      &pitch};
+      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
+                                       dim3(kGatherWarps * 32), args, smem, sg),
+                      "K2b (row gather) launch");
+    }
+  };
+  if (generic_side) launch_generic();
   // K2b for the row classes: specialised kernels (rows in registers)
   if (gp.n_citems > 0) {
     ensure_class_module(f, p);
@@ -433,7 +472,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     // the long-row kernel runs on the context's side stream, concurrently with
     // the short-row one (disjoint rows): the two register budgets share the SMs
     // and the element records they both read stay in L2
-    const bool both = gp.n_citems_short > 0 && gp.n_citems > gp.n_citems_short && !std::getenv("FF_SERIAL_CLASSES");
+    const bool both = !generic_side && gp.n_citems_short > 0 && gp.n_citems > gp.n_citems_short &&
+                      !std::getenv("FF_SERIAL_CLASSES");
     if (both) {
       ffb::cuda_check(cudaEventRecord(ctx->fork, s), "fork");
       ffb::cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
@@ -462,32 +502,10 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       ffb::cuda_check(cudaStreamWaitEvent(s, ctx->join, 0), "join");
     }
   }
-  // K2b for the remaining rows in two launches: short-pitch items, then long-pitch items
-  const int64_t ranges[2][2] = {{0, gp.n_short}, {gp.n_short, gp.n_items}};
-  const int pitches[2] = {gp.pitch_short, gp.pitch_long};
-  for (int c = 0; c < 2; ++c) {
-    long long i0 = ranges[c][0], i1 = ranges[c][1];
-    if (i1 <= i0) continue;
-    int pitch = pitches[c];
-    const int smem = gather_smem(pitch);
-    require(smem <= kGatherSmemMax, "row gather: rows too long for the shared-memory accumulators");
-    // a few items per warp (grid-stride): CTAs run in item order, so the items
-    // in flight stay contiguous and their element data stays in L2
-    const int64_t per_cta = int64_t(kGatherWarps) * 4;
-    const unsigned grid = static_cast<unsigned>((i1 - i0 + per_cta - 1) / per_cta);
-    const double* ginv = p->ginv;
-    long long ne_arg = m->ne;
-    const int64_t* row_ptr = p->row_ptr;
-    const int32_t* order = gp.item_order;
-    const int32_t* wrows = gp.warp_rows;
-    const int32_t* wsteps = gp.warp_steps;
-    const int64_t* wrec = gp.warp_rec;
-    const void* rec = gp.rec;
-    void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &order, &i0, &i1, &wrows, &wsteps, &wrec, &rec,
-                    &pitch};
-    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
-                                     dim3(kGatherWarps * 32), args, smem, s),
-                    "K2b (row gather) launch");
+  if (!generic_side) launch_generic();
+  if (generic_side) {
+    ffb::cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
+    ffb::cuda_check(cudaStreamWaitEvent(s, ctx->join, 0), "join");
   }
 }
 
