@@ -281,7 +281,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
     rc.push_back(std::move(r));
   }
   const auto t0 = std::chrono::steady_clock::now();
-  // one fused kernel (long rows in slot-range passes) unless FF_SPLIT_CLASSES:
+  // one fused kernel for every class unless FF_SPLIT_CLASSES:
   // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
   const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused);
@@ -298,6 +298,12 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
                   "cudaLibraryLoadData (classes)");
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[0], p->class_lib, "ff_gather_classes_s"), "class kernel");
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[1], p->class_lib, "ff_gather_classes_l"), "class kernel");
+  for (int c = 0; c < 2; ++c) {
+    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused);
+    ffb::cuda_check(cudaKernelSetAttributeForDevice(p->class_kernel[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    p->class_smem[c], p->ctx->device),
+                    "class kernel shared memory attribute");
+  }
   p->class_compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   p->class_key = key;
 }
@@ -494,7 +500,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       const int32_t* crec = gp.crec;
       void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(128), args,
-                                       0, sc),
+                                       p->class_smem[c], sc),
                       "K2b (class row gather) launch");
     }
     if (both) {
@@ -684,7 +690,8 @@ int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* 
       at += steps[c];
     }
     const std::string src = window ? codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc)
-                                   : codegen::emit_class_source(f->plan, f->n_local, rc);
+                                   : codegen::emit_class_source(f->plan, f->n_local, rc,
+                                                                std::getenv("FF_SPLIT_CLASSES") == nullptr);
     if (out_len) *out_len = src.size();
     if (buf && cap) {
       const std::size_t k = std::min(cap - 1, src.size());

@@ -93,6 +93,84 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
 }
 
 
+namespace {
+
+// Peak number of row slots "open" (first contribution added, last not yet)
+// when the class's incidences are accumulated in `order`.
+int peak_live(const RowClass& k, int n_local, const std::vector<int>& order) {
+  std::vector<int> first(k.len, -1), last(k.len, -1);
+  for (int t = 0; t < static_cast<int>(order.size()); ++t)
+    for (int j = 0; j < n_local; ++j) {
+      const int sl = k.slots[order[t] * n_local + j];
+      if (first[sl] < 0) first[sl] = t;
+      last[sl] = t;
+    }
+  int live = 0, peak = 0;
+  for (int t = 0; t < static_cast<int>(order.size()); ++t) {
+    for (int sl = 0; sl < k.len; ++sl) live += first[sl] == t;
+    peak = std::max(peak, live);
+    for (int sl = 0; sl < k.len; ++sl) live -= last[sl] == t;
+  }
+  return peak;
+}
+
+}  // namespace
+
+// Incidence order of a class that keeps few row slots open at once: a slot's
+// register is live from its first to its last contribution, then the value
+// goes to the staging row. Greedy (fewest newly opened slots) from every
+// start, then a fixed-seed swap search; deterministic, so the source is too.
+// P2 Kuhn vertex rows (65 slots, 24 incidences): 23-26 live instead of 65.
+std::vector<int> class_step_order(const RowClass& k, int n_local) {
+  const int n = k.steps;
+  std::vector<int> best(n);
+  for (int q = 0; q < n; ++q) best[q] = q;
+  if (n < 2) return best;
+  int bv = peak_live(k, n_local, best);
+  for (int start = 0; start < n; ++start) {
+    std::vector<int> order{start};
+    std::vector<char> used(n, 0), seen(k.len, 0);
+    used[start] = 1;
+    for (int j = 0; j < n_local; ++j) seen[k.slots[start * n_local + j]] = 1;
+    while (static_cast<int>(order.size()) < n) {
+      int pick = -1, pc = 1 << 30;
+      for (int q = 0; q < n; ++q) {
+        if (used[q]) continue;
+        int c = 0;
+        for (int j = 0; j < n_local; ++j) c += !seen[k.slots[q * n_local + j]];
+        if (c < pc) pc = c, pick = q;
+      }
+      used[pick] = 1;
+      order.push_back(pick);
+      for (int j = 0; j < n_local; ++j) seen[k.slots[pick * n_local + j]] = 1;
+    }
+    const int v = peak_live(k, n_local, order);
+    if (v < bv) bv = v, best = order;
+  }
+  uint64_t rng = 0x9e3779b97f4a7c15ull;
+  const int iters = n <= 8 ? 2000 : 20000;
+  for (int it = 0; it < iters; ++it) {
+    rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+    const int a = static_cast<int>((rng >> 33) % n), b = static_cast<int>((rng >> 13) % n);
+    if (a == b) continue;
+    std::swap(best[a], best[b]);
+    const int v = peak_live(k, n_local, best);
+    if (v <= bv)
+      bv = v;
+    else
+      std::swap(best[a], best[b]);
+  }
+  return best;
+}
+
+int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused) {
+  int m = 1;
+  for (const auto& c : classes)
+    if (fused || (c.len > 33) == (kernel == 1)) m = std::max(m, c.len);
+  // rows longer than 33 are staged in chunks of 32 in finalisation order
+  return std::min(m, 33) | 1;  // odd: conflict-free lane-row stores
+}
+
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes, bool fused) {
   if (plan.n_kinv <= 0) throw CodegenError("row classes need a reference-tensor plan");
   std::ostringstream os;
@@ -103,6 +181,9 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
         "typedef long long ff_i64;\ntypedef int ff_i32;\n"
      << "#define FF_NLOC " << n_local << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
      << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((plan.n_kinv + 3) / 4) * 4 << "\n"
+     << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
+     << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
+     << class_stage_pitch(classes, 1, fused) << "\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
@@ -138,19 +219,34 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
     b = 0.0;
   }
 }
-#define FF_SP 33  // staging pitch (odd: conflict-free lane-row stores)
 #define FF_PRE 8  // records of the next item prefetched while this item computes
 // staged rows -> CSR values: flat index f over 32 rows x cnt slots, so
 // consecutive lanes write consecutive values of one row. Shared by every
 // class (one copy, not unrolled: keeps the instruction footprint small).
-__device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
-                                         int cnt, int q0, double* __restrict__ values) {
+__device__ __noinline__ void ff_writeout(const double* __restrict__ st, int sp, const ff_i64* __restrict__ sr,
+                                         int lane, int cnt, int q0, double* __restrict__ values) {
   __syncwarp();
   if (lane < cnt) {
 #pragma unroll 4
     for (int m = 0; m < 32; ++m) {
       const ff_i64 rb = sr[m];
-      if (rb >= 0) __stcs(values + rb + q0 + lane, st[m * FF_SP + lane]);
+      if (rb >= 0) __stcs(values + rb + q0 + lane, st[m * sp + lane]);
+    }
+  }
+  __syncwarp();
+}
+// chunk of a long row staged in finalisation order: lane l of the chunk
+// holds the row's slot map[l]
+__device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int sp, const ff_i64* __restrict__ sr,
+                                             int lane, int cnt, const unsigned char* __restrict__ map,
+                                             double* __restrict__ values) {
+  __syncwarp();
+  if (lane < cnt) {
+    const int off = __ldg(map + lane);
+#pragma unroll 4
+    for (int m = 0; m < 32; ++m) {
+      const ff_i64 rb = sr[m];
+      if (rb >= 0) __stcs(values + rb + off, st[m * sp + lane]);
     }
   }
   __syncwarp();
@@ -166,13 +262,47 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
 #endif
 )";
   // class c with rows of <= 33 entries -> ff_gather_classes_s, else _l; fused:
-  // every class in _s, rows longer than 33 entries in slot-range passes
+  // every class in _s (rows longer than 33 entries staged in chunks)
   auto is_long = [&](int c) { return !fused && classes[c].len > 33; };
   auto class_fn = [&](int c) {
     const RowClass& k = classes[c];
-    const int n_pass = fused ? std::max(1, (k.len + 32) / 33) : 1;
-    const int per = (k.len + n_pass - 1) / n_pass;
-    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences\n"
+    const char* sp = is_long(c) ? "FF_SP_L" : "FF_SP_S";
+    // one pass over the incidences in class_step_order: each element record
+    // is loaded once; a slot's register opens at its first contribution and
+    // goes to the staging row after its last one
+    const std::vector<int> order = class_step_order(k, n_local);
+    std::vector<int> first(k.len, -1), last(k.len, -1);
+    for (int t = 0; t < k.steps; ++t)
+      for (int j = 0; j < n_local; ++j) {
+        const int sl = k.slots[order[t] * n_local + j];
+        if (first[sl] < 0) first[sl] = t;
+        last[sl] = t;
+      }
+    // staging position of every slot: the slot index when the row fits one
+    // staging row, else its finalisation rank (chunks of 32 written out as
+    // soon as they are complete, lanes in ascending slot order inside a chunk)
+    const bool chunked = k.len > 33;
+    // fin: finalisation rank (chunk = fin / 32); pos: position inside the
+    // chunk's staging row (ascending slot order)
+    std::vector<int> pos(k.len), fin(k.len), slot_at(k.len);
+    for (int sl = 0; sl < k.len; ++sl) pos[sl] = fin[sl] = sl;
+    if (chunked) {
+      std::vector<int> byfin(k.len);
+      for (int sl = 0; sl < k.len; ++sl) byfin[sl] = sl;
+      std::stable_sort(byfin.begin(), byfin.end(), [&](int a, int b) { return last[a] < last[b]; });
+      for (int r = 0; r < k.len; ++r) fin[byfin[r]] = r;
+      for (int c0 = 0; c0 < k.len; c0 += 32)
+        std::sort(byfin.begin() + c0, byfin.begin() + std::min(k.len, c0 + 32));
+      for (int r = 0; r < k.len; ++r) pos[byfin[r]] = r;
+    }
+    for (int sl = 0; sl < k.len; ++sl) slot_at[pos[sl]] = sl;
+    if (chunked) {
+      os << "__device__ const unsigned char ff_cmap_" << c << "[" << k.len << "] = {";
+      for (int r = 0; r < k.len; ++r) os << (r ? ", " : "") << slot_at[r];
+      os << "};\n";
+    }
+    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences, at most "
+       << peak_live(k, n_local, order) << " open\n"
        << "__device__ __forceinline__ void ff_cls_" << c
        << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv, ff_i64 n_elems,\n"
           "    double* __restrict__ st, ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row,\n"
@@ -185,39 +315,55 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
         os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
     }
     os << "  double bs = 0.0;\n";
+    for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
+    os << ";\n";
     os << "  sr[lane] = row >= 0 ? rbeg : -1;\n";
-    const int depth = is_long(c) ? 4 : 8;
-    for (int ps = 0; ps < n_pass; ++ps) {
-      const int lo = ps * per, hi = std::min(k.len, lo + per);
-      os << "  {  // slots [" << lo << ", " << hi << ")\n";
-      for (int p = lo; p < hi; ++p) os << "  double a" << p << " = 0.0;\n";
-      for (int s0 = 0; s0 < k.steps; s0 += depth) {
-        const int s1 = std::min(k.steps, s0 + depth);
-        os << "  {\n";
-        for (int q = s0; q < s1; ++q)
-          os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q]
-             << ", einv, n_elems, g" << q << ", b" << q << ");\n";
-        for (int q = s0; q < s1; ++q) {
-          std::string adds;
+    const int depth = 8;
+    for (int t0 = 0; t0 < k.steps; t0 += depth) {
+      const int t1 = std::min(k.steps, t0 + depth);
+      os << "  {\n";
+      for (int t = t0; t < t1; ++t) {
+        const int q = order[t];
+        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q]
+           << ", einv, n_elems, g" << q << ", b" << q << ");\n";
+      }
+      for (int t = t0; t < t1; ++t) {
+        const int q = order[t];
+        os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);";
+        for (int j = 0; j < n_local; ++j) {
+          const int sl = k.slots[q * n_local + j];
+          os << " a" << sl << (first[sl] == t ? " = v[" : " += v[") << j << "];";
+        }
+        if (!chunked) {
           for (int j = 0; j < n_local; ++j) {
             const int sl = k.slots[q * n_local + j];
-            if (sl >= lo && sl < hi) adds += " a" + std::to_string(sl) + " += v[" + std::to_string(j) + "];";
+            if (last[sl] == t) os << " st[lane * " << sp << " + " << sl << "] = a" << sl << ";";
           }
-          if (!adds.empty())
-            os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);" << adds << " }\n";
-          if (ps == 0) os << "    bs += b" << q << ";\n";
+        } else {
+          std::vector<int> closing;  // finalisation ranks closing at step t
+          for (int j = 0; j < n_local; ++j)
+            if (last[k.slots[q * n_local + j]] == t) closing.push_back(fin[k.slots[q * n_local + j]]);
+          std::sort(closing.begin(), closing.end());
+          std::vector<int> slot_of_fin(k.len);
+          for (int sl = 0; sl < k.len; ++sl) slot_of_fin[fin[sl]] = sl;
+          for (int f : closing) {
+            const int sl = slot_of_fin[f];
+            os << " st[lane * " << sp << " + " << pos[sl] % 32 << "] = a" << sl << ";";
+            if (f % 32 == 31 || f == k.len - 1)  // chunk f / 32 complete
+              os << "\n      ff_writeout_map(st, " << sp << ", sr, lane, " << f % 32 + 1 << ", ff_cmap_" << c << " + "
+                 << f - f % 32 << ", values);";
+          }
         }
-        os << "  }\n";
-      }
-      // write-out through the staging rows (consecutive lanes = consecutive
-      // CSR values of one row)
-      for (int q0 = lo; q0 < hi; q0 += 32) {
-        const int cnt = std::min(32, hi - q0);
-        for (int j = 0; j < cnt; ++j) os << "  st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
-        os << "  ff_writeout(st, sr, lane, " << cnt << ", " << q0 << ", values);\n";
+        os << " }\n    bs += b" << q << ";\n";
       }
       os << "  }\n";
     }
+    // write-out through the staging rows (consecutive lanes = consecutive CSR
+    // values of one row)
+    if (!chunked)
+      for (int q0 = 0; q0 < k.len; q0 += 32)
+        os << "  ff_writeout(st + " << q0 << ", " << sp << ", sr, lane, " << std::min(32, k.len - q0) << ", " << q0
+           << ", values);\n";
     os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
   };
   for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
@@ -236,11 +382,11 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, const ff
           "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
           "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
           "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
-          "  __shared__ double stage[4][32 * FF_SP];\n"
-          "  __shared__ ff_i64 srow[4][32];\n"
+          "  // dynamic shared memory: 4 staging tiles [32][FF_SP] + 4 x 32 row offsets\n"
+          "  extern __shared__ double ff_dsm[];\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
-          "  double* st = stage[wid];\n"
-          "  ff_i64* sr = srow[wid];\n"
+          "  double* st = ff_dsm + wid * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ";\n"
+          "  ff_i64* sr = (ff_i64*)(ff_dsm + 4 * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ") + wid * 32;\n"
           "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * FF_IPW;\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"

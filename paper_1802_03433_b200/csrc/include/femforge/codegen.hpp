@@ -159,6 +159,17 @@ struct RowClass {
   std::vector<std::uint8_t> slots;   // [steps][n_local] slot of column dof[j] in the row
 };
 
+// Incidence order of a row class that minimises the number of row slots whose
+// register accumulators are open at once (deterministic).
+std::vector<int> class_step_order(const RowClass& k, int n_local);
+// Staging-row pitch of class kernel `kernel` (0: _s, 1: _l; odd, >= its
+// longest class row).
+int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused);
+// Dynamic shared memory of class kernel `kernel` (4 warps).
+inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused) {
+  return 4 * 32 * class_stage_pitch(classes, kernel, fused) * 8 + 4 * 32 * 8;
+}
+
 // NVRTC translation unit with ff_gather_classes_s (classes of rows <= 33
 // entries) and ff_gather_classes_l (longer rows). Needs a gather-capable
 // plan (plan.n_kinv > 0). Byte-deterministic.

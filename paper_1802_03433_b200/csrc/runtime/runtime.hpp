@@ -119,6 +119,7 @@ struct ff_pattern {
   std::string class_key;
   cudaLibrary_t class_lib = nullptr;
   cudaKernel_t class_kernel[2] = {nullptr, nullptr};  // short rows, long rows
+  int class_smem[2] = {0, 0};                           // their dynamic shared memory
   // window row-gather kernel for (form source, plan)
   std::string window_key;
   cudaLibrary_t window_lib = nullptr;
