@@ -104,6 +104,10 @@ void load_module(ff_form* f, int w) {
     ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_grows[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     kGatherSmemMax, f->ctx->device),
                     "row-gather shared memory attribute");
+    ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_ginv[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    codegen::gather_invariants_smem(f->plan, f->block),
+                                                    f->ctx->device),
+                    "K2a shared memory attribute");
   } else {
     cudaGetLastError();
     f->kernel_ginv[w] = f->kernel_grows[w] = nullptr;
@@ -264,6 +268,12 @@ void ensure_window_module(ff_form* f, ff_pattern* p) {
   p->window_key = key;
 }
 
+// Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
+int class_ipw(const ff_form* f) {
+  const char* v = std::getenv("FF_IPW");
+  return v ? std::max(1, std::atoi(v)) : (f->ncomp > 1 ? 1 : 2);
+}
+
 // NVRTC-compiles the class-specialised gather kernels of (form, plan).
 void ensure_class_module(ff_form* f, ff_pattern* p) {
   if (p->gather.classes.empty()) return;
@@ -284,11 +294,15 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // one fused kernel for every class unless FF_SPLIT_CLASSES:
   // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
   const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
-  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused);
+  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp);
   if (fused && !std::getenv("FF_MINB_S")) src = "#define FF_MINB_S 3\n" + src;
+  // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
+  // 82.6 ms at config 5, run 43)
+  if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
   // element records bypass L1 allocation (streamed once per lane; -6 %, run 27)
-  if (!std::getenv("FF_EINV_L1")) src = "#define FF_EINV_NA 1\n" + src;
+  // (vector forms read each record once per component pair: keep L1)
+  if (!std::getenv("FF_EINV_L1") && f->ncomp == 1) src = "#define FF_EINV_NA 1\n" + src;
   for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
@@ -360,7 +374,6 @@ int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w)
   if (flags & FF_SCATTER_TILES) mode = FF_SCATTER_ROWTILE;
   if (flags & (FF_SCATTER_GATHER | FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) mode = FF_SCATTER_GATHER_MODE;
   if (flags & (FF_ZERO_ONLY | FF_SKIP_ZERO)) mode = FF_SCATTER_ATOMIC_MODE;
-  if (f->ncomp > 1) mode = FF_SCATTER_ATOMIC_MODE;  // vector forms: block-expanded atomic scatter
   if (mode == FF_SCATTER_GATHER_MODE &&
       !(f->kernel_grows[w] && p->max_row_len <= 255 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax))
     mode = FF_SCATTER_ATOMIC_MODE;
@@ -373,7 +386,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   ff_ctx* ctx = f->ctx;
   ensure_gather_plan(p, m);
   unsigned long long* wstatus = ctx->d_status;
-  if (p->gather.n_win > 0 && window_es(f) * 8 * p->gather.win_max_elems <= kWindowMaxElems * window_es(f) * 8) {
+  if (p->gather.n_win > 0 && f->ncomp == 1 && window_es(f) * 8 * p->gather.win_max_elems <= kWindowMaxElems * window_es(f) * 8) {
     // window row gather: element records computed in shared memory per window
     if (flags & FF_GATHER_INVARIANTS_ONLY) {
       ffb::cuda_check(cudaMemsetAsync(wstatus, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
@@ -406,7 +419,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     return;
   }
   const int gs = ((f->plan.n_kinv + 3) / 4) * 4;  // FF_GS: invariants [E][gs] + load vectors [k][E]
-  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * (gs + m->k);
+  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * (gs + f->n_local);
   if (p->ginv_cap < ng) {
     cudaFree(p->ginv);
     p->ginv = nullptr;
@@ -426,7 +439,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       void* args[] = {&coords, &vconn, &dconn, &eorder, &ne, &ginv, &status};
       const unsigned grid = static_cast<unsigned>((m->ne + f->block - 1) / f->block);
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_ginv[w]), dim3(grid), dim3(f->block),
-                                       args, 0, s),
+                                       args, codegen::gather_invariants_smem(f->plan, f->block), s),
                       "K2a (element invariants) launch");
     }
   }
@@ -443,7 +456,9 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   const cudaStream_t sg = generic_side ? ctx->side : s;
   auto launch_generic = [&]() {
     // K2b for the remaining rows in two launches: short-pitch items, then long-pitch items
-    const int64_t ranges[2][2] = {{0, gp.n_short}, {gp.n_short, gp.n_items}};
+    // vector forms: FF_BS^2 sub-items (component pairs) per item
+    const int64_t nb = static_cast<int64_t>(f->ncomp) * f->ncomp;
+    const int64_t ranges[2][2] = {{0, gp.n_short * nb}, {gp.n_short * nb, gp.n_items * nb}};
     const int pitches[2] = {gp.pitch_short, gp.pitch_long};
     for (int c = 0; c < 2; ++c) {
       long long i0 = ranges[c][0], i1 = ranges[c][1];
@@ -488,9 +503,9 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       cudaStream_t sc = (both && c == 1) ? ctx->side : s;
       long long i0 = cr[c][0], i1 = cr[c][1];
       if (i1 <= i0) continue;
-      const char* ipw_env = std::getenv("FF_IPW");
-      const int64_t ipw = ipw_env ? std::max(1, std::atoi(ipw_env)) : 2;
-      const unsigned grid = static_cast<unsigned>((i1 - i0 + 4 * ipw - 1) / (4 * ipw));  // 4 warps x FF_IPW items
+      const int64_t ipw = class_ipw(f);
+      // 4 warps x FF_IPW items per CTA; vector forms: one CTA per component pair
+      const unsigned grid = static_cast<unsigned>((i1 - i0 + 4 * ipw - 1) / (4 * ipw) * f->ncomp * f->ncomp);
       const double* ginv = p->ginv;
       long long ne_arg = m->ne;
       const int64_t* row_ptr = p->row_ptr;
@@ -678,6 +693,8 @@ int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* 
   return guarded([&] {
     require(f && n >= 0 && (n == 0 || (len && steps && local && slots)), "null argument");
     require(f->plan.n_kinv > 0, "form has no reference-tensor plan (no row gather)");
+    require(!window || f->ncomp == 1, "window gather: scalar forms only");
+    const int nsc = f->n_local / f->ncomp;  // slots per incidence (node rows of vector forms)
     std::vector<codegen::RowClass> rc(n);
     int64_t at = 0;
     for (int c = 0; c < n; ++c) {
@@ -685,13 +702,13 @@ int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* 
       rc[c].steps = steps[c];
       for (int q = 0; q < steps[c]; ++q) {
         rc[c].local.push_back(local[at + q]);
-        for (int j = 0; j < f->n_local; ++j) rc[c].slots.push_back(slots[(at + q) * f->n_local + j]);
+        for (int j = 0; j < nsc; ++j) rc[c].slots.push_back(slots[(at + q) * nsc + j]);
       }
       at += steps[c];
     }
     const std::string src = window ? codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc)
                                    : codegen::emit_class_source(f->plan, f->n_local, rc,
-                                                                std::getenv("FF_SPLIT_CLASSES") == nullptr);
+                                                                std::getenv("FF_SPLIT_CLASSES") == nullptr, f->ncomp);
     if (out_len) *out_len = src.size();
     if (buf && cap) {
       const std::size_t k = std::min(cap - 1, src.size());
@@ -846,8 +863,7 @@ int ff_form_info_get(const ff_form* f, ff_form_info* o) {
     o->registers = f->module[1].registers;
     o->shared_bytes = f->module[1].shared_bytes;
     o->compile_ms = f->compile_ms;
-    o->n_kinv = (!f->raw && f->plan.n_kinv > 0 && f->n_local <= 12 && f->plan.n_kinv + f->n_local <= 24)
-                    ? f->plan.n_kinv : 0;
+    o->n_kinv = (!f->raw && codegen::gather_capable(f->plan, f->n_local, f->ncomp, f->block)) ? f->plan.n_kinv : 0;
     o->row_flops = f->plan.row_flops;
   });
 }

@@ -360,11 +360,31 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
   for (int r = 0; r < nn; ++r)
     for (const auto& [t, c] : row_sig[r]) kq.emplace(t, 0);
   {
+    // vector forms: invariants ordered by the first (test, trial) component
+    // block that reads them, so the row gather of one block loads a few
+    // contiguous 32-byte groups of the element record
+    const int bs = std::max(1, f.ncomp);
+    std::map<int, int> first_block;
+    for (int r = 0; r < nn; ++r) {
+      const int blk = ((r / f.n_local) % bs) * bs + (r % f.n_local) % bs;
+      for (const auto& [t, c] : row_sig[r]) {
+        auto it = first_block.find(t);
+        if (it == first_block.end() || blk < it->second) first_block[t] = blk;
+      }
+    }
+    std::vector<std::pair<int, int>> keyed;
+    for (const auto& [t, slot] : kq) keyed.push_back({first_block[t], t});
+    std::sort(keyed.begin(), keyed.end());
     int q = 0;
-    for (auto& [t, slot] : kq) slot = q++;
+    for (const auto& [blk, t] : keyed) kq[t] = q++;
   }
   plan.n_kinv = static_cast<int>(kq.size());
-  for (const auto& [t, q] : kq) os << "  FF_KINV(" << q << ", ff_t" << t << ");\n";
+  {
+    std::vector<std::pair<int, int>> by_q;
+    for (const auto& [t, q] : kq) by_q.push_back({q, t});
+    std::sort(by_q.begin(), by_q.end());
+    for (const auto& [q, t] : by_q) os << "  FF_KINV(" << q << ", ff_t" << t << ");\n";
+  }
   {
     // ff_row<i>: v[j] = K_ij with the same expression (term order, literals)
     // as the element body, so both scatters compute bit-identical entries

@@ -1,6 +1,7 @@
 // Source emission: the hand-written assembly template with the generated
 // element body spliced in (the reference's template route, kernel.cpp:
 // 290-449, made executable: the output is what NVRTC compiles).
+#include <cstdlib>
 #include <algorithm>
 #include <sstream>
 #include <string>
@@ -74,16 +75,15 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
                      std::to_string(plan.flops) + " flops\n" + plan.body;
   fill(text, "ELEMENT_BODY", body);
   fill(text, "ELEMENT_PRELUDE", plan.prelude);
-  // the row gather needs a reference-tensor plan and <= 12 slot bytes per record
-  const bool gather = f.ncomp == 1 && plan.n_kinv > 0 && f.n_local <= 12 && plan.n_kinv + f.n_local <= 24;
+  const bool gather = gather_capable(plan, f.n_local, f.ncomp, cfg.block_size);
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
   {
     std::string d =
-        "__device__ __forceinline__ void ff_gather_dispatch(int i, const FfRec& r, const double (&g)[FF_NKP],\n"
+        "__device__ __forceinline__ void ff_gather_dispatch(int i, const FfRec& r, const double (&g)[FF_NKP], int d,\n"
         "                                                   double* __restrict__ arow) {\n  switch (i) {\n";
     for (int i = 0; i < f.n_local; ++i)
-      d += "    case " + std::to_string(i) + ": ff_gather_apply<" + std::to_string(i) + ">(r, g, arow); break;\n";
+      d += "    case " + std::to_string(i) + ": ff_gather_apply<" + std::to_string(i) + ">(r, g, d, arow); break;\n";
     d += "    default: break;\n  }\n}\n";
     fill(text, "ROW_DISPATCH", gather ? d : std::string());
   }
@@ -92,6 +92,15 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   return text;
 }
 
+
+bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size) {
+  // a reference-tensor plan and <= 12 slot bytes per record (node rows for
+  // vector forms); K2a stages [block / 32][32][FF_GS + 1] doubles in shared
+  // memory
+  return plan.n_kinv > 0 && ncomp >= 1 && n_local / ncomp <= 12 &&
+         (ncomp == 1 ? plan.n_kinv + n_local <= 24 : plan.n_kinv <= 64) &&
+         gather_invariants_smem(plan, block_size) <= 200 * 1024;
+}
 
 namespace {
 
@@ -171,15 +180,21 @@ int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fus
   return std::min(m, 33) | 1;  // odd: conflict-free lane-row stores
 }
 
-std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes, bool fused) {
+std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes, bool fused,
+                              int bs) {
   if (plan.n_kinv <= 0) throw CodegenError("row classes need a reference-tensor plan");
+  if (bs < 1 || n_local % bs) throw CodegenError("class source: bad component count");
+  // classes are over (node) rows with nsc slots per incidence; vector forms
+  // gather each (test c, trial d) component pair as its own sub-row
+  const int nsc = n_local / bs, nb = bs * bs;
   std::ostringstream os;
   const int nkp = plan.n_kinv + (plan.n_kinv & 1);
   const int erec = (plan.n_kinv + n_local + 1) & ~1;
   os << "// femforge-b200 class-specialised row gather (generated per (form, gather plan));\n"
         "// every class row stays in registers, indexed by compile-time slots.\n"
         "typedef long long ff_i64;\ntypedef int ff_i32;\n"
-     << "#define FF_NLOC " << n_local << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
+     << "#define FF_NLOC " << n_local << "\n#define FF_BS " << bs << "\n#define FF_NB " << nb
+     << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
      << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((plan.n_kinv + 3) / 4) * 4 << "\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
@@ -220,6 +235,16 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   }
 }
 #define FF_PRE 8  // records of the next item prefetched while this item computes
+// CSR value stores: streaming (evict-first) for scalar rows, which are written
+// whole; vector sub-rows fill every FF_BS-th value, so their lines must stay
+// in L2 until the other component pairs' CTAs complete them
+__device__ __forceinline__ void ff_stv(double* p, double v) {
+#if FF_BS == 1
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
 // staged rows -> CSR values: flat index f over 32 rows x cnt slots, so
 // consecutive lanes write consecutive values of one row. Shared by every
 // class (one copy, not unrolled: keeps the instruction footprint small).
@@ -230,7 +255,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, int sp, 
 #pragma unroll 4
     for (int m = 0; m < 32; ++m) {
       const ff_i64 rb = sr[m];
-      if (rb >= 0) __stcs(values + rb + q0 + lane, st[m * sp + lane]);
+      if (rb >= 0) ff_stv(values + rb + FF_BS * (q0 + lane), st[m * sp + lane]);
     }
   }
   __syncwarp();
@@ -246,7 +271,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
 #pragma unroll 4
     for (int m = 0; m < 32; ++m) {
       const ff_i64 rb = sr[m];
-      if (rb >= 0) __stcs(values + rb + off, st[m * sp + lane]);
+      if (rb >= 0) ff_stv(values + rb + FF_BS * off, st[m * sp + lane]);
     }
   }
   __syncwarp();
@@ -267,6 +292,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   auto class_fn = [&](int c) {
     const RowClass& k = classes[c];
     const char* sp = is_long(c) ? "FF_SP_L" : "FF_SP_S";
+    const int n_local = nsc;  // slots per incidence
     // one pass over the incidences in class_step_order: each element record
     // is loaded once; a slot's register opens at its first contribution and
     // goes to the staging row after its last one
@@ -301,9 +327,11 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
       for (int r = 0; r < k.len; ++r) os << (r ? ", " : "") << slot_at[r];
       os << "};\n";
     }
-    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences, at most "
-       << peak_live(k, n_local, order) << " open\n"
-       << "__device__ __forceinline__ void ff_cls_" << c
+    for (int cd = 0; cd < nb; ++cd) {
+    const int cc = cd / bs, dd = cd % bs;
+    os << "// class " << c << " (components " << cc << ", " << dd << "): " << k.len << " entries, " << k.steps
+       << " incidences, at most " << peak_live(k, n_local, order) << " open\n"
+       << "__device__ __forceinline__ void ff_cls_" << c << "_" << cd
        << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv, ff_i64 n_elems,\n"
           "    double* __restrict__ st, ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row,\n"
           "    double* __restrict__ values, double* __restrict__ rhs) {\n"
@@ -314,25 +342,25 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
       else
         os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
     }
-    os << "  double bs = 0.0;\n";
+    if (dd == 0) os << "  double bs = 0.0;\n";
     for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
     os << ";\n";
-    os << "  sr[lane] = row >= 0 ? rbeg : -1;\n";
-    const int depth = 8;
+    os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
+    const int depth = bs == 1 ? 8 : (std::getenv("FF_VDEPTH") ? std::max(1, std::atoi(std::getenv("FF_VDEPTH"))) : 2);
     for (int t0 = 0; t0 < k.steps; t0 += depth) {
       const int t1 = std::min(k.steps, t0 + depth);
       os << "  {\n";
       for (int t = t0; t < t1; ++t) {
         const int q = order[t];
-        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q]
+        os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] * bs + cc
            << ", einv, n_elems, g" << q << ", b" << q << ");\n";
       }
       for (int t = t0; t < t1; ++t) {
         const int q = order[t];
-        os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);";
+        os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] * bs + cc << ">(g" << q << ", v);";
         for (int j = 0; j < n_local; ++j) {
           const int sl = k.slots[q * n_local + j];
-          os << " a" << sl << (first[sl] == t ? " = v[" : " += v[") << j << "];";
+          os << " a" << sl << (first[sl] == t ? " = v[" : " += v[") << j * bs + dd << "];";
         }
         if (!chunked) {
           for (int j = 0; j < n_local; ++j) {
@@ -354,7 +382,8 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
                  << f - f % 32 << ", values);";
           }
         }
-        os << " }\n    bs += b" << q << ";\n";
+        os << " }\n";
+        if (dd == 0) os << "    bs += b" << q << ";\n";
       }
       os << "  }\n";
     }
@@ -364,7 +393,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
       for (int q0 = 0; q0 < k.len; q0 += 32)
         os << "  ff_writeout(st + " << q0 << ", " << sp << ", sr, lane, " << std::min(32, k.len - q0) << ", " << q0
            << ", values);\n";
-    os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
+    if (dd == 0) os << "  if (row >= 0) __stcs(rhs + FF_BS * row + " << cc << ", bs);\n";
+    os << "}\n";
+    }  // component pairs
   };
   for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
   os << "__constant__ int ff_csteps[" << std::max<std::size_t>(classes.size(), 1) << "] = {";
@@ -387,7 +418,10 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
           "  double* st = ff_dsm + wid * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ";\n"
           "  ff_i64* sr = (ff_i64*)(ff_dsm + 4 * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ") + wid * 32;\n"
-          "  const ff_i64 first = i0 + ((ff_i64)blockIdx.x * 4 + wid) * FF_IPW;\n"
+          "  // vector forms: FF_NB consecutive CTAs run the same items, one component\n"
+          "  // pair each (one code path per CTA; the items' records shared in L2)\n"
+          "  const int cd = (int)(blockIdx.x % FF_NB);\n"
+          "  const ff_i64 first = i0 + ((ff_i64)(blockIdx.x / FF_NB) * 4 + wid) * FF_IPW;\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
           "  // the next item's header and first records load while this item computes\n"
@@ -409,10 +443,12 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "      for (int u = 0; u < FF_PRE; ++u) epn[u] = __ldcs(recn + u * 32);\n"
           "    }\n"
           "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
-          "    switch (c) {\n";
+          "    switch (c * FF_NB + cd) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
-        os << "      case " << c << ": ff_cls_" << c << "(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
+        for (int cd = 0; cd < nb; ++cd)
+          os << "      case " << c * nb + cd << ": ff_cls_" << c << "_" << cd
+             << "(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
     os << "      default: break;\n    }\n"
           "    c = cn;\n    row = rown;\n    rec = recn;\n"
           "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"

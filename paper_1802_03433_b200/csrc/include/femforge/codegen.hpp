@@ -159,6 +159,13 @@ struct RowClass {
   std::vector<std::uint8_t> slots;   // [steps][n_local] slot of column dof[j] in the row
 };
 
+// Dynamic shared memory of K2a (ff_gather_invariants): per-warp record staging.
+inline int gather_invariants_smem(const ElementPlan& plan, int block_size) {
+  return block_size * (((plan.n_kinv + 3) / 4) * 4 + 1) * 8;
+}
+// Whether the plan's kernels include the row gather (K2a + generic K2b).
+bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size);
+
 // Incidence order of a row class that minimises the number of row slots whose
 // register accumulators are open at once (deterministic).
 std::vector<int> class_step_order(const RowClass& k, int n_local);
@@ -174,7 +181,7 @@ inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, 
 // entries) and ff_gather_classes_l (longer rows). Needs a gather-capable
 // plan (plan.n_kinv > 0). Byte-deterministic.
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes,
-                              bool fused = false);
+                              bool fused = false, int bs = 1);
 
 // The window row-gather kernel (ff_gather_windows) appended to the form's own
 // translation unit (it reuses the form's geometry and element body).

@@ -350,7 +350,9 @@ def test_window_gather_matches_oracle(ff, ctx, dim, deg, n, form, monkeypatch):
     assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
 
 
-def _elasticity_system(ff, ctx, n, row_begin=0, row_end=None, ids=None, lam="1", mu="1", force=("0", "0", "-1")):
+def _elasticity_system(ff, ctx, n, row_begin=0, row_end=None, ids=None, lam="1", mu="1", force=("0", "0", "-1"),
+                       scatter="gather"):
+    ctx.set_scatter(scatter)
     c, v = ff.kuhn_mesh(n)
     d, nd = ff.kuhn_p2_dofs(n, v)
     if ids is not None:
@@ -365,16 +367,38 @@ def _elasticity_system(ff, ctx, n, row_begin=0, row_end=None, ids=None, lam="1",
 
 
 @pytest.mark.parametrize("n", [2, 5])
-def test_elasticity_matches_oracle(ff, ctx, n):
+@pytest.mark.parametrize("scatter", ["gather", "atomic"])
+def test_elasticity_matches_oracle(ff, ctx, n, scatter):
     """Config 5 (vector P2 elasticity): block-expanded pattern bit-exact, values
-    and RHS <= 1e-12 normwise against the C restatement."""
-    c, v, d, nd, rp, ci, val, rhs, f, m, p = _elasticity_system(ff, ctx, n, lam="2", mu="0.5", force=("0", "1", "-1"))
-    assert p.scatter_for(f) == "atomic" and p.n_rows == 3 * nd
+    and RHS <= 1e-12 normwise against the C restatement, through the row
+    gather (per component-pair sub-rows) and the atomic scatter."""
+    c, v, d, nd, rp, ci, val, rhs, f, m, p = _elasticity_system(ff, ctx, n, lam="2", mu="0.5", force=("0", "1", "-1"),
+                                                                scatter=scatter)
+    assert p.scatter_for(f) == scatter and p.n_rows == 3 * nd
     orp, oci = po.build_pattern(d, nd)
     vrp, vci = po.block_pattern(orp, oci, 3)
     assert np.array_equal(rp, vrp) and np.array_equal(ci, vci)
     ov, ob = po.assemble_elasticity(3, 2, 4, c, v, d, vrp, vci, lam=2.0, mu=0.5, force=(0.0, 1.0, -1.0))
     assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
+
+
+def test_elasticity_class_gather_matches_atomic(ff, ctx):
+    """Vector forms through the class-specialised gather (node-row classes,
+    one register-resident sub-row per (test, trial) component pair): equal to
+    the atomic scatter to rounding, bitwise reproducible run to run."""
+    n = 8
+    ctx.set_gather_classes(200)
+    try:
+        *_, val_a, rhs_a, f, m, p = _elasticity_system(ff, ctx, n, scatter="atomic")
+        ctx.set_scatter("gather")
+        val_g, rhs_g = ff.assemble(f, m, p)
+        val_g2, rhs_g2 = ff.assemble(f, m, p)
+        gi = p.gather_info(m)
+    finally:
+        ctx.set_gather_classes(128)
+    assert gi["n_class_rows"] > 0 and gi["n_classes"] >= 8
+    assert normwise(val_g, val_a) <= 1e-15 and normwise(rhs_g, rhs_a) <= 1e-15
+    assert np.array_equal(val_g, val_g2) and np.array_equal(rhs_g, rhs_g2)
 
 
 def test_elasticity_rigid_body_modes_and_row_blocks(ff, ctx):
@@ -383,6 +407,14 @@ def test_elasticity_rigid_body_modes_and_row_blocks(ff, ctx):
     concatenate to the 1-GPU system (SURVEY §8e for config 5)."""
     import scipy.sparse as sp
     n = 16
+    ctx.set_gather_classes(0)  # generic sub-row gather here (classes: the test above)
+    try:
+        _elasticity_rbm(ff, ctx, sp, n)
+    finally:
+        ctx.set_gather_classes(128)
+
+
+def _elasticity_rbm(ff, ctx, sp, n):
     c, v, d, nd, rp, ci, val, rhs, *_ = _elasticity_system(ff, ctx, n)
     K = sp.csr_matrix((val, ci, rp), shape=(3 * nd, 3 * nd))
     L = 2 * n + 1
