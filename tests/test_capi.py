@@ -186,9 +186,11 @@ def test_window_source_compiles(ff):
 
 def test_blocked_elasticity_form_compiles(ff):
     """Vector P2 elasticity (3x3 blocks of scalar forms, 30 DOFs per element)
-    through instantiate_blocked -> tensor plan -> NVRTC for sm_100a."""
+    through instantiate_blocked -> tensor plan -> NVRTC for sm_100a, with the
+    component-pair row gather (K2a + generic sub-row kernel) in the module."""
     b, l = ff.elasticity_text(3)
     f = ff.Form.blocked(None, 3, 2, 3, b, l, quad_rule=4)
     info = f.info
-    assert info["n_local"] == 30 and info["n_kinv"] == 0
+    assert info["n_local"] == 30 and info["n_kinv"] == 36
     assert f.cubin[:4] == b"\x7fELF" and "#define FF_BS 3" in f.source
+    assert "ff_gather_invariants" in f.source and "ff_gather_apply<29>(r, g, d, arow)" in f.source
