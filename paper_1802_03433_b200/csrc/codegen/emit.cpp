@@ -218,21 +218,18 @@ __device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, do
 __device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
 #endif
 // element record: invariants [E][FF_GS] (256-bit loads), load vector [FF_NLOC][E]
+// (idle lanes, e < 0, only occur in rows that are never written: they read
+// element 0 instead of branching)
 __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, ff_i64 n_elems,
                                          double (&g)[FF_NKP], double& b) {
-  if (e >= 0) {
-    const double* base = einv + (ff_i64)e * FF_GS;
-    double t[FF_GS];
+  const ff_i64 ee = e >= 0 ? e : 0;
+  const double* base = einv + ee * FF_GS;
+  double t[FF_GS];
 #pragma unroll
-    for (int q = 0; q < FF_GS / 4; ++q) ff_ld4(base + 4 * q, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+  for (int q = 0; q < FF_GS / 4; ++q) ff_ld4(base + 4 * q, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
 #pragma unroll
-    for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
-    b = ff_ld1(einv + n_elems * FF_GS + (ff_i64)i * n_elems + e);
-  } else {
-#pragma unroll
-    for (int q = 0; q < FF_NKP; ++q) g[q] = 0.0;
-    b = 0.0;
-  }
+  for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
+  b = ff_ld1(einv + n_elems * FF_GS + (ff_i64)i * n_elems + ee);
 }
 #define FF_PRE 8  // records of the next item prefetched while this item computes
 // CSR value stores: streaming (evict-first) for scalar rows, which are written
