@@ -6,7 +6,8 @@ prebuilt pattern (the reference's criterion-9 protocol, acceptance.cpp:292-327)
 cube (12,582,912 tets, 16,974,593 DOFs, 484,609,025 nnz).
 
   python bench.py [--gpus N --steps K --warmup W] [--config ns|c1|c2|c3|c4]
-  torchrun --nproc-per-node N bench.py --gpus N ...   (row-block weak scaling)
+  torchrun --nproc-per-node N bench.py --gpus N ...   (weak scaling: one cell per GPU;
+                                                       --scaling strong: row blocks of one mesh)
   python bench.py --impl reference ...                (reference CPU arm)
 
 One JSON line on rank 0. Multi-GPU: contiguous DOF row blocks, halo elements
@@ -254,6 +255,9 @@ def main():
     ap.add_argument("--block", type=int, default=256)
     ap.add_argument("--strategy", default="auto")
     ap.add_argument("--scatter", default="gather", choices=["gather", "rowtile", "atomic"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = the 1-GPU workload stacked N times (one cell per GPU); "
+                         "strong = row blocks of the one 1-GPU mesh")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.n:
@@ -281,14 +285,24 @@ def main():
     from paper_1802_03433_b200 import femforge as ff
     from paper_1802_03433_b200 import rowblocks
 
-    coords, vconn, dconn, n_dofs = make_mesh(ff, cfg)
-    E = vconn.shape[0]
-    rb, re = rowblocks.row_block(n_dofs, world, rank)
-    if world > 1:
-        ids = rowblocks.local_elements(dconn, rb, re)   # owned + halo elements
-        vconn_l, dconn_l = np.ascontiguousarray(vconn[ids]), np.ascontiguousarray(dconn[ids])
+    weak = world > 1 and args.scaling == "weak"
+    if weak:
+        # weak scaling: the single-GPU cell stacked `world` times along the last
+        # axis; each rank builds only its slab (own cell + one halo layer)
+        coords, vconn_l, dconn_l, n_dofs, rb, re, E = rowblocks.weak_slab(ff, cfg["dim"], cfg["degree"], cfg["n"],
+                                                                          world, rank)
+        if dconn_l is None:
+            dconn_l = vconn_l
+        vconn = vconn_l
     else:
-        vconn_l, dconn_l = vconn, dconn
+        coords, vconn, dconn, n_dofs = make_mesh(ff, cfg)
+        E = vconn.shape[0]
+        rb, re = rowblocks.row_block(n_dofs, world, rank)
+        if world > 1:  # strong scaling: row blocks of the one mesh
+            ids = rowblocks.local_elements(dconn, rb, re)   # owned + halo elements
+            vconn_l, dconn_l = np.ascontiguousarray(vconn[ids]), np.ascontiguousarray(dconn[ids])
+        else:
+            vconn_l, dconn_l = vconn, dconn
     ctx = ff.Context(local)
     ctx.set_scatter(args.scatter)
     ncomp = cfg.get("ncomp", 1)
@@ -388,8 +402,10 @@ def main():
                "d2h_bytes_per_step": int(hval.nbytes + hrhs.nbytes), "ms_per_step": 1e3 * float(e2e_s)}
 
     nnz_tot = pat.nnz
+    dofs_tot = n_dofs
     if world > 1:  # global CSR offsets: exclusive prefix over the ranks' (rows, nnz), SURVEY §8e
-        _, _, _, nnz_tot = rowblocks.global_offsets(pat.nnz, pat.n_rows)
+        _, _, rows_tot, nnz_tot = rowblocks.global_offsets(pat.nnz, pat.n_rows)
+        dofs_tot = rows_tot // ncomp
     if rank != 0:
         dist.destroy_process_group()
         return
@@ -417,9 +433,12 @@ def main():
     value = E / (step_ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 and not weak else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic structured mesh)",
-        "config": {"workload": cfg["workload"], "n": cfg["n"], "elements": int(E), "dofs": int(n_dofs),
+        "config": {"workload": cfg["workload"] + (f", stacked x{world} along the last axis (one cell per GPU)"
+                                                  if weak else ""),
+                   "n": cfg["n"], "elements": int(E), "dofs": int(dofs_tot),
                    "nnz": int(nnz_tot), "form": cfg["form"], "quad_rule": cfg["quad"],
                    "parallelism": f"row-blocks x{world} (halo elements duplicated, no collective)",
                    "l2": "flushed (256 MiB write) between steps" if need_flush else
