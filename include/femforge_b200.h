@@ -236,6 +236,17 @@ int ff_export_csr(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, con
                   int fmt);
 
 /* ---- host helpers (CPU only; no device needed) --------------------------- */
+/* Parses `expr` (symbolic::parse, expr.cpp) and evaluates it at n points
+ * [n][dim] of (x, y[, z]) (symbolic::eval); a symbol other than the first
+ * `dim` coordinates fails with FF_E_SYMBOLIC "expression references symbol
+ * 's'" (the CLI's coefficient check, femforge.cpp:95-113, and l2_error's,
+ * linalg.cpp:101-104). n = 0 only validates. */
+int ff_expr_eval(const char* expr, int dim, const double* pts, int64_t n, double* out);
+/* The instantiated integrand of entry (i, j) (kind 0: bilinear) or i (kind
+ * 1: linear) as text (symbolic::print): the inspection view the CLI's
+ * `codegen --out-ir` writes (femforge.cpp:203-231). Same length protocol
+ * as ff_class_source. */
+int ff_form_entry_text(const ff_form* form, int kind, int i, int j, char* buf, size_t cap, size_t* out_len);
 /* meshgen.cpp:13-33 unit square; SURVEY.md Appendix C Kuhn cube + P2 lattice. */
 int ff_unit_square_mesh(int n, double* coords, int32_t* conn);
 int ff_kuhn_mesh(int n, double* coords, int32_t* conn);

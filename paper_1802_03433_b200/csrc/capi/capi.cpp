@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <new>
 #include <string>
@@ -677,6 +678,40 @@ int ff_ctx_set_gather_classes(ff_ctx* ctx, int64_t min_rows) {
 
 int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* len, const int32_t* steps,
                            const int32_t* local, const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
+
+int ff_expr_eval(const char* expr, int dim, const double* pts, int64_t n, double* out) {
+  return guarded([&] {
+    require(expr && dim >= 1 && dim <= 3 && n >= 0 && (n == 0 || (pts && out)), "ff_expr_eval: invalid argument");
+    const symbolic::Expr e = symbolic::parse(expr);
+    static const char* const kNames[3] = {"x", "y", "z"};
+    for (const std::string& s : symbolic::free_symbols(e)) {
+      bool ok = false;
+      for (int c = 0; c < dim; ++c) ok = ok || s == kNames[c];
+      if (!ok) throw symbolic::SymbolicError("expression references symbol '" + s + "'");
+    }
+    std::map<std::string, double> at;
+    for (int64_t i = 0; i < n; ++i) {
+      for (int c = 0; c < dim; ++c) at[kNames[c]] = pts[i * dim + c];
+      out[i] = symbolic::eval(e, at);
+    }
+  });
+}
+
+int ff_form_entry_text(const ff_form* f, int kind, int i, int j, char* buf, size_t cap, size_t* out_len) {
+  return guarded([&] {
+    require(f && !f->raw, "ff_form_entry_text: form without an instantiated weak form");
+    const int n = f->inst.n_local;
+    require(i >= 0 && i < n && (kind == 1 || (kind == 0 && j >= 0 && j < n)), "ff_form_entry_text: index out of range");
+    const std::string s = symbolic::print(kind == 0 ? f->inst.bilinear[static_cast<std::size_t>(i) * n + j]
+                                                    : f->inst.linear[i]);
+    if (out_len) *out_len = s.size();
+    if (buf && cap) {
+      const std::size_t k = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
 
 int ff_class_source(const ff_form* f, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {

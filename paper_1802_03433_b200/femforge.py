@@ -107,6 +107,8 @@ SIGNATURES = [
     ("ff_ctx_set_scatter", C.c_int, [_P, C.c_int]),
     ("ff_ctx_set_gather_classes", C.c_int, [_P, _i64]),
     ("ff_class_source", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("ff_expr_eval", C.c_int, [C.c_char_p, C.c_int, _P, _i64, _P]),
+    ("ff_form_entry_text", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_window_source", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_form_create", C.c_int, [_P, C.POINTER(_FormDesc), C.POINTER(_P)]),
     ("ff_compile", C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P), C.c_char_p, C.c_size_t]),
@@ -289,6 +291,16 @@ class Form:
         _ok(fn(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), None, 0, C.byref(m)))
         buf = C.create_string_buffer(m.value + 1)
         _ok(fn(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), buf, m.value + 1, C.byref(m)))
+        return buf.value.decode()
+
+    def entry_text(self, kind, i, j=0):
+        """Instantiated integrand of bilinear entry (i, j) (kind "bilinear") or
+        linear entry i (kind "linear") as text (ff_form_entry_text)."""
+        k = 0 if kind == "bilinear" else 1
+        m = C.c_size_t(0)
+        _ok(lib().ff_form_entry_text(self.h, k, i, j, None, 0, C.byref(m)))
+        buf = C.create_string_buffer(m.value + 1)
+        _ok(lib().ff_form_entry_text(self.h, k, i, j, buf, m.value + 1, C.byref(m)))
         return buf.value.decode()
 
     def close(self):
@@ -496,6 +508,19 @@ def select_elements(dconn, row_begin, row_end):
 
 
 # ---- weak-form text (the reference's helmholtz_form, fem.cpp:99-107) ---------
+
+def expr_eval(expr, dim, pts=None):
+    """Evaluates a coefficient / exact-solution expression over (x, y[, z]) at
+    points [n][dim] (ff_expr_eval); pts None only validates it (raises
+    SymbolicError on a parse error or a foreign symbol)."""
+    if pts is None:
+        _ok(lib().ff_expr_eval(expr.encode(), dim, None, 0, None))
+        return None
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, dim)
+    out = np.empty(pts.shape[0])
+    _ok(lib().ff_expr_eval(expr.encode(), dim, _ptr(pts), pts.shape[0], _ptr(out)))
+    return out
+
 
 def helmholtz_text(dim, sigma=None, lam="0", f="0", beta=None):
     """bilinear = grad v . sigma grad u + lam u v [+ (beta . grad u) v]; linear = f v."""
