@@ -157,6 +157,33 @@ def test_pattern_from_other_mesh_is_a_hard_error(ff, ctx, scatter):
         ff.assemble(f, m, p, vconn=other)
 
 
+@pytest.mark.parametrize("scatter", SCATTERS)
+def test_isolated_dofs_and_tiny_meshes(ff, ctx, scatter):
+    """Edge cases of the pattern rules (device.cpp:66-88: the diagonal is
+    always present): a node no element touches keeps a diagonal-only row whose
+    value and load are exactly 0 (the atomic-free scatters write every value,
+    nothing is zero-filled for them); one-cell meshes in 2D and 3D match the
+    oracle."""
+    ctx.set_scatter(scatter)
+    xy, conn = ff.unit_square_mesh(3)
+    xy = np.vstack([xy, [[2.0, 2.0]]])          # node 16: no element
+    rp, ci, v, b, *_ = gpu_system(ff, ctx, 2, 1, "demo2d", xy, conn, conn, xy.shape[0], scatter=scatter)
+    assert rp[-1] - rp[-2] == 1 and ci[-1] == 16 and v[-1] == 0.0 and b[-1] == 0.0
+    orp, oci = po.build_pattern(conn, xy.shape[0])
+    ov, ob = po.assemble("demo2d", 2, 1, 3, xy, conn, conn, orp, oci)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert normwise(v, ov) <= TOL and normwise(b, ob) <= TOL
+    for dim, deg in [(2, 1), (3, 1), (3, 2)]:
+        c, vc, d, nd = _mesh(ff, dim, deg, 1)
+        form = "demo2d" if dim == 2 else "helmholtz"
+        rp, ci, v, b, *_ = gpu_system(ff, ctx, dim, deg, form, c, vc, d, nd, quad=3 if dim == 2 else 4,
+                                      scatter=scatter)
+        orp, oci = po.build_pattern(d, nd)
+        ov, ob = po.assemble(form, dim, deg, 3 if dim == 2 else 4, c, vc, d, orp, oci)
+        assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+        assert normwise(v, ov) <= TOL and normwise(b, ob) <= TOL
+
+
 @pytest.mark.parametrize("parts", [2, 3, 4])
 @pytest.mark.parametrize("scatter", SCATTERS)
 def test_row_blocks_concatenate_to_full_system(ff, ctx, parts, scatter):
