@@ -463,7 +463,10 @@ def main():
                      "bytes_per_launch": int(B), "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e if e2e is not None else ({"skipped": e2e_note} if e2e_note else None),
-        "gpu_launches": (1 if scatter == "rowtile" else 2) * args.steps,  # ours only (flush is a torch fill)
+        # ours only (the L2 flush is a torch fill): gather = K2a + class + generic
+        # launches (plan-dependent), atomic = K0 + K2, rowtile = one kernel
+        "gpu_launches": (gather_info["launches"] if scatter == "gather" else 1 if scatter == "rowtile" else 2)
+                        * args.steps,
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -162,6 +162,7 @@ typedef struct ff_gather_info {
   int64_t n_windows;                        /* window plan (0: none): windows of window_rows rows, */
   int window_rows;                          /* each with <= window_max_elems elements in shared memory */
   int64_t window_max_elems, n_window_items;
+  int launches;                             /* kernel launches per gather assembly (K2a, class, generic) */
 } ff_gather_info;
 /* Row classes of the gather plan: rows with identical incidence sequences
  * get an NVRTC kernel specialised to the class (slots as compile-time

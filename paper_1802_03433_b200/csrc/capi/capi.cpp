@@ -1096,6 +1096,15 @@ int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* m, ff_gather_info* out)
     out->window_rows = p->gather.win_rows;
     out->window_max_elems = p->gather.win_max_elems;
     out->n_window_items = p->gather.n_witems;
+    // what launch_gather issues: the window kernel alone, or K2a + the class
+    // kernel(s) + the non-empty generic ranges
+    const auto& g = p->gather;
+    if (g.n_win > 0) {
+      out->launches = 1;
+    } else {
+      out->launches = (m->ne > 0 ? 1 : 0) + (g.n_citems_short > 0) + (g.n_citems > g.n_citems_short) +
+                      (g.n_short > 0) + (g.n_items > g.n_short);
+    }
   });
 }
 

@@ -75,7 +75,8 @@ class GatherInfo(C.Structure):
     _fields_ = [("n_items", C.c_int64), ("n_steps", C.c_int64), ("n_incidences", C.c_int64),
                 ("record_bytes", C.c_int), ("build_ms", C.c_double), ("n_classes", C.c_int),
                 ("n_class_rows", C.c_int64), ("n_class_items", C.c_int64), ("n_windows", C.c_int64),
-                ("window_rows", C.c_int), ("window_max_elems", C.c_int64), ("n_window_items", C.c_int64)]
+                ("window_rows", C.c_int), ("window_max_elems", C.c_int64), ("n_window_items", C.c_int64),
+                ("launches", C.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
