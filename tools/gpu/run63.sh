@@ -1,0 +1,4 @@
+# ablation (timing only): drop the load-vector load / half of the invariant loads
+for v in FF_NONE=1 FF_ABLATE_NOB=1 FF_ABLATE_HALFG=1 "FF_ABLATE_NOB=1 FF_ABLATE_HALFG=1"; do
+  echo "$v $(env $v timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print(round(d['ms_per_step'],4), d['config'].get('k2_ms'))")"
+done
