@@ -90,7 +90,14 @@ void load_module(ff_form* f, int w) {
   ffb::cuda_check(cudaLibraryLoadData(&f->lib[w], f->module[w].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
                   "cudaLibraryLoadData");
   ffb::cuda_check(cudaLibraryGetKernel(&f->kernel[w], f->lib[w], "ff_assemble_atomic"), "cudaLibraryGetKernel");
-  if (cudaLibraryGetKernel(&f->kernel_tile[w], f->lib[w], "ff_assemble_rowtile") == cudaSuccess) {
+  // which optional kernels the module holds: known from the template for
+  // generated forms (row tiles: scalar forms; gather: gather_capable); probed
+  // for caller-written sources
+  const bool tile_known = !f->raw, gather_known = !f->raw;
+  const bool has_tile = f->ncomp == 1;
+  const bool has_gather = codegen::gather_capable(f->plan, f->n_local, f->ncomp, f->block);
+  if ((tile_known ? has_tile : true) &&
+      cudaLibraryGetKernel(&f->kernel_tile[w], f->lib[w], "ff_assemble_rowtile") == cudaSuccess) {
     f->tile = codegen::rowtile_params(f->n_local, f->block);
     f->tile_smem[w] = f->tile.smem_bytes(f->n_local, w);
     ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_tile[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -100,7 +107,8 @@ void load_module(ff_form* f, int w) {
     cudaGetLastError();
     f->kernel_tile[w] = nullptr;
   }
-  if (cudaLibraryGetKernel(&f->kernel_ginv[w], f->lib[w], "ff_gather_invariants") == cudaSuccess &&
+  if ((gather_known ? has_gather : true) &&
+      cudaLibraryGetKernel(&f->kernel_ginv[w], f->lib[w], "ff_gather_invariants") == cudaSuccess &&
       cudaLibraryGetKernel(&f->kernel_grows[w], f->lib[w], "ff_gather_rows") == cudaSuccess) {
     ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_grows[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     kGatherSmemMax, f->ctx->device),
