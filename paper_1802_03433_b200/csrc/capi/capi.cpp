@@ -475,9 +475,13 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       int pitch = pitches[c];
       const int smem = gather_smem(pitch);
       require(smem <= kGatherSmemMax, "row gather: rows too long for the shared-memory accumulators");
-      // a few items per warp (grid-stride): CTAs run in item order, so the items
-      // in flight stay contiguous and their element data stays in L2
-      const int64_t per_cta = int64_t(kGatherWarps) * 4;
+      // a few items per warp: CTAs run in item order, so the items in flight
+      // stay contiguous and their element data stays in L2; one item per warp
+      // when the range would not fill the GPU (small meshes, boundary rows)
+      int ipw = 4;
+      if ((i1 - i0) < int64_t(ctx->sm_count) * kGatherWarps * 4 * 4) ipw = 1;
+      if (const char* v = std::getenv("FF_GENERIC_IPW")) ipw = std::max(1, std::atoi(v));  // tuning knob
+      const int64_t per_cta = int64_t(kGatherWarps) * ipw;
       const unsigned grid = static_cast<unsigned>((i1 - i0 + per_cta - 1) / per_cta);
       const double* ginv = p->ginv;
       long long ne_arg = m->ne;
@@ -488,7 +492,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       const int64_t* wrec = gp.warp_rec;
       const void* rec = gp.rec;
       void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &order, &i0, &i1, &wrows, &wsteps, &wrec, &rec,
-                      &pitch};
+                      &pitch, &ipw};
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_grows[w]), dim3(grid),
                                        dim3(kGatherWarps * 32), args, smem, sg),
                       "K2b (row gather) launch");

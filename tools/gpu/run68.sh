@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "gather or isolated or elasticity" -p no:cacheprovider 2>&1 | tail -1
+for c in c1 c2 c3 ns; do
+  echo "$c $(timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print(round(d['ms_per_step'],4), d['config'].get('k2a_ms'), d['config'].get('k2_ms'))")"
+done

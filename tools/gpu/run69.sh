@@ -1,0 +1,4 @@
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -1
+for c in ns c3 c2; do for v in FF_NONE=1 FF_GENERIC_IPW=1 FF_GENERIC_IPW=2; do
+  echo "$c $v $(env $v timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print(round(d['ms_per_step'],4))")"
+done; done
