@@ -50,6 +50,7 @@ struct ff_ctx {
 
 struct ff_form {
   ff_ctx* ctx = nullptr;
+  std::uint64_t id = 0;             // process-unique (graph replay keys)
   int dim = 2, degree = 1, n_local = 3, block = 256;
   int ncomp = 1;                    // components of a vector (blocked) form
   femforge::codegen::ElementPlan plan;
@@ -111,6 +112,10 @@ struct ff_pattern {
   int tile_acc = 0, tile_rows = 0, tile_stage = 0, tile_chunk = 0;
   // row-gather plan for plan_mesh, and the per-element invariant buffers
   std::uint64_t gather_generation = ~0ull;
+  // CUDA graph of the last device assembly (ff_assemble_device replays it when
+  // every pointer and plan it captured is unchanged)
+  std::vector<std::uint64_t> graph_key, graph_warm_key;
+  cudaGraphExec_t graph_exec = nullptr;
   int64_t gather_class_min = -1;            // class_min_rows the plan was built with
   const ff_mesh* gather_mesh = nullptr;
   ffb::kernels::GatherPlan gather;

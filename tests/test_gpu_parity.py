@@ -125,6 +125,49 @@ def test_device_path_equals_e2e_path(ff, ctx, scatter):
 
 
 @pytest.mark.parametrize("scatter", SCATTERS)
+def test_graph_replay_follows_the_mesh(ff, ctx, scatter):
+    """Repeated ff_assemble_device calls on a created stream replay one CUDA
+    graph (first call plain, second captured): the replay reads the current
+    coordinates, and a connectivity update (new plans) re-captures; every
+    result equals the host-buffer path on the same mesh."""
+    import torch
+    c, v, d, nd = _mesh(ff, 3, 2, 6)
+    rp, ci, val, rhs, f, m, p = gpu_system(ff, ctx, 3, 2, "helmholtz", c, v, d, nd, quad=4, scatter=scatter)
+    stream = torch.cuda.Stream()
+    dv = torch.empty(p.nnz, dtype=torch.float64, device="cuda")
+    db = torch.empty(p.n_rows, dtype=torch.float64, device="cuda")
+
+    def run(k):
+        out = []
+        for _ in range(k):
+            dv.fill_(float("nan"))
+            torch.cuda.synchronize()
+            ff.assemble_device(f, m, p, dv.data_ptr(), db.data_ptr(), stream.cuda_stream)
+            torch.cuda.synchronize()
+            ctx.check()
+            out.append((dv.cpu().numpy().copy(), db.cpu().numpy().copy()))
+        return out
+
+    for a, b in run(4):
+        assert normwise(a, val) <= 1e-14 and normwise(b, rhs) <= 1e-14
+    rng = np.random.default_rng(7)
+    c2 = c.copy()
+    inner = np.all((c > 1e-12) & (c < 1 - 1e-12), axis=1)
+    c2[inner] += rng.uniform(-0.02, 0.02, size=(inner.sum(), 3)) / 6
+    val2, rhs2 = ff.assemble(f, m, p, coords=c2)   # uploads the new coordinates
+    torch.cuda.synchronize()
+    for a, b in run(2):
+        assert normwise(a, val2) <= 1e-14 and normwise(b, rhs2) <= 1e-14
+    perm = rng.permutation(v.shape[0])
+    v3, d3 = np.ascontiguousarray(v[perm]), np.ascontiguousarray(d[perm])
+    val3, rhs3 = ff.assemble(f, m, p, coords=c2, vconn=v3, dconn=d3)
+    torch.cuda.synchronize()
+    for a, b in run(3):
+        assert normwise(a, val3) <= 1e-14 and normwise(b, rhs3) <= 1e-14
+    assert normwise(val3, val2) <= 1e-13
+
+
+@pytest.mark.parametrize("scatter", SCATTERS)
 def test_degenerate_element_reported_by_lowest_index(ff, ctx, scatter):
     ctx.set_scatter(scatter)
     xy, conn = ff.unit_square_mesh(4)
