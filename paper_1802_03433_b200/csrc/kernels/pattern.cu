@@ -12,11 +12,14 @@
 // entry) is derived from the finished pattern with one binary search per
 // entry; it is what lets the numeric kernel scatter without any search.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <unordered_map>
 #include <vector>
@@ -409,6 +412,28 @@ __global__ void item_steps(const int32_t* __restrict__ order, int64_t n_rows, in
   }
 }
 
+// class id of every row: binary search of its signature among the class
+// signatures (sorted); representative row = the lowest row of the class
+__global__ void row_class(const uint64_t* __restrict__ sig, int64_t n_rows, const uint64_t* __restrict__ csig,
+                          const int32_t* __restrict__ cid, int n_cls, int32_t* __restrict__ cls,
+                          int32_t* __restrict__ reps) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t h = sig[r];
+    int lo = 0, hi = n_cls;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (csig[mid] < h)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    const int c = lo < n_cls && csig[lo] == h ? cid[lo] : -1;
+    cls[r] = c;
+    if (c >= 0) atomicMin(reps + c, static_cast<int32_t>(r));
+  }
+}
+
 // class templates of the representative rows: [c][2 + kMaxSteps*(1+k)] ints:
 // len, steps, then per step the local index and the k slot bytes
 constexpr int kMaxClassSteps = 64;
@@ -755,6 +780,16 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               bool use_eorder, int max_win_elems, bool split_long) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  // FF_PLAN_TIMING=1: phase times of the plan build on stderr
+  const bool timing = std::getenv("FF_PLAN_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[plan] %-24s %8.1f ms\n", name, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   const int cap = sm_count * 16;
   const int64_t nk = ne * k;
   int32_t* cnt = nullptr;
@@ -853,53 +888,71 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     cudaFree(eid);
     if (err != cudaSuccess) return done(err);
   }
+  phase("incidences+morton");
   tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, rows, order, n_rows, 0, 64, s);
   if ((err = need_temp(tb)) != cudaSuccess) return done(err);
   if ((err = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, rows, order, n_rows, 0, 64, s)) != cudaSuccess)
     return done(err);
+  phase("row sort");
   // ---- row classes (signature counts on the host, verified on the device)
   std::vector<int32_t> morton(n_rows), cls_h(n_rows, -1);
   {
-    std::vector<uint64_t> sig_h(n_rows);
+    // signature counts on the device: sort + run-length encode; the host sees
+    // only the distinct signatures
+    if (n_rows > 0) cudaMemcpyAsync(morton.data(), order, n_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    std::vector<uint64_t> usig;
+    std::vector<int32_t> ucnt;
     if (n_rows > 0) {
-      cudaMemcpyAsync(morton.data(), order, n_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-      cudaMemcpyAsync(sig_h.data(), sig, n_rows * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+      uint64_t *ssorted = nullptr, *uniq = nullptr;
+      int32_t *counts = nullptr, *nruns = nullptr;
+      auto sfree = [&]() {
+        cudaFree(ssorted);
+        cudaFree(uniq);
+        cudaFree(counts);
+        cudaFree(nruns);
+      };
+      if ((err = cudaMalloc(&ssorted, n_rows * sizeof(uint64_t))) != cudaSuccess) return sfree(), done(err);
+      if ((err = cudaMalloc(&uniq, n_rows * sizeof(uint64_t))) != cudaSuccess) return sfree(), done(err);
+      if ((err = cudaMalloc(&counts, n_rows * sizeof(int32_t))) != cudaSuccess) return sfree(), done(err);
+      if ((err = cudaMalloc(&nruns, sizeof(int32_t))) != cudaSuccess) return sfree(), done(err);
+      size_t t1 = 0, t2 = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, t1, sig, ssorted, static_cast<int>(n_rows), 0, 64, s);
+      cub::DeviceRunLengthEncode::Encode(nullptr, t2, ssorted, uniq, counts, nruns, static_cast<int>(n_rows), s);
+      if ((err = need_temp(std::max(t1, t2))) != cudaSuccess) return sfree(), done(err);
+      err = cub::DeviceRadixSort::SortKeys(temp, t1, sig, ssorted, static_cast<int>(n_rows), 0, 64, s);
+      if (err == cudaSuccess)
+        err = cub::DeviceRunLengthEncode::Encode(temp, t2, ssorted, uniq, counts, nruns, static_cast<int>(n_rows), s);
+      int32_t nr = 0;
+      if (err == cudaSuccess) err = cudaMemcpyAsync(&nr, nruns, sizeof nr, cudaMemcpyDeviceToHost, s);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+      if (err == cudaSuccess) {
+        usig.resize(nr);
+        ucnt.resize(nr);
+        cudaMemcpyAsync(usig.data(), uniq, nr * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(ucnt.data(), counts, nr * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        err = cudaStreamSynchronize(s);
+      }
+      sfree();
+      if (err != cudaSuccess) return done(err);
     }
     if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
-    std::unordered_map<uint64_t, std::pair<int64_t, int32_t>> count;  // sig -> (rows, first row in Morton order)
-    count.reserve(1024);
-    for (int64_t pos = 0; pos < n_rows; ++pos) {
-      const int32_t r = morton[pos];
-      auto [it, fresh] = count.emplace(sig_h[r], std::make_pair(int64_t(0), r));
-      ++it->second.first;
-    }
-    std::vector<std::pair<int64_t, uint64_t>> big;
     // classes worth a specialised kernel: >= min_class_rows rows and >= 0.5 %
     // of the block (boundary classes stay generic: smaller code, fewer
-    // instruction-cache misses)
+    // instruction-cache misses); ordered by row count, then signature
     const char* frac_env = std::getenv("FF_CLASS_FRAC");  // tuning knob, default 0.5 %
     const double frac = frac_env ? std::atof(frac_env) : 0.005;
     const int64_t min_rows = std::max<int64_t>(min_class_rows, static_cast<int64_t>(frac * n_rows));
-    for (const auto& [h, v] : count)
-      if (v.first >= min_rows) big.push_back({v.first, h});
-    std::sort(big.begin(), big.end(), [&](const auto& a, const auto& b) {
-      return a.first != b.first ? a.first > b.first : count[a.second].second < count[b.second].second;
+    std::vector<std::pair<int64_t, uint64_t>> big;
+    for (size_t u = 0; u < usig.size(); ++u)
+      if (ucnt[u] >= min_rows) big.push_back({ucnt[u], usig[u]});
+    std::sort(big.begin(), big.end(), [](const auto& a, const auto& b) {
+      return a.first != b.first ? a.first > b.first : a.second < b.second;
     });
     if (static_cast<int>(big.size()) > max_classes) big.resize(max_classes);
-    std::unordered_map<uint64_t, int> cid;
-    std::vector<int32_t> reps;
-    for (const auto& [n, h] : big) {
-      cid[h] = static_cast<int>(reps.size());
-      reps.push_back(count[h].second);
-    }
-    const int n_cls = static_cast<int>(reps.size());
+    const int n_cls = static_cast<int>(big.size());
     out->classes.clear();
     if (n_cls > 0) {
-      for (int64_t r = 0; r < n_rows; ++r) {
-        auto it = cid.find(sig_h[r]);
-        if (it != cid.end()) cls_h[r] = it->second;
-      }
       const int stride = 2 + kMaxClassSteps * (1 + k);
       int32_t *d_reps = nullptr, *d_tmpl = nullptr, *d_cls = nullptr;
       auto cleanup = [&]() {
@@ -911,10 +964,30 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       if ((err = cudaMalloc(&d_tmpl, static_cast<size_t>(n_cls) * stride * sizeof(int32_t))) != cudaSuccess)
         return cleanup(), done(err);
       if ((err = cudaMalloc(&d_cls, n_rows * sizeof(int32_t))) != cudaSuccess) return cleanup(), done(err);
-      cudaMemcpyAsync(d_reps, reps.data(), n_cls * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      {
+        // class signatures sorted (for the per-row binary search) with their ids
+        std::vector<std::pair<uint64_t, int32_t>> by_sig;
+        for (int c = 0; c < n_cls; ++c) by_sig.push_back({big[c].second, c});
+        std::sort(by_sig.begin(), by_sig.end());
+        std::vector<uint64_t> csig(n_cls);
+        std::vector<int32_t> cidv(n_cls);
+        for (int c = 0; c < n_cls; ++c) csig[c] = by_sig[c].first, cidv[c] = by_sig[c].second;
+        uint64_t* d_csig = nullptr;
+        int32_t* d_cid = nullptr;
+        if ((err = cudaMalloc(&d_csig, n_cls * sizeof(uint64_t))) != cudaSuccess) return cleanup(), done(err);
+        if ((err = cudaMalloc(&d_cid, n_cls * sizeof(int32_t))) != cudaSuccess)
+          return cudaFree(d_csig), cleanup(), done(err);
+        cudaMemcpyAsync(d_csig, csig.data(), n_cls * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_cid, cidv.data(), n_cls * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+        cudaMemsetAsync(d_reps, 0x7f, n_cls * sizeof(int32_t), s);
+        row_class<<<grid_for(n_rows, cap), kThreads, 0, s>>>(sig, n_rows, d_csig, d_cid, n_cls, d_cls, d_reps);
+        err = cudaStreamSynchronize(s);
+        cudaFree(d_csig);
+        cudaFree(d_cid);
+        if (err != cudaSuccess) return cleanup(), done(err);
+      }
       cudaMemsetAsync(d_tmpl, 0, static_cast<size_t>(n_cls) * stride * sizeof(int32_t), s);
       class_templates<<<1, 64, 0, s>>>(d_reps, n_cls, inc_ptr, inc, d_slots, k, d_row_ptr, d_tmpl);
-      cudaMemcpyAsync(d_cls, cls_h.data(), n_rows * sizeof(int32_t), cudaMemcpyHostToDevice, s);
       class_verify<<<grid_for(n_rows, cap), kThreads, 0, s>>>(d_cls, n_rows, d_tmpl, k, inc_ptr, inc, d_slots,
                                                              d_row_ptr);
       std::vector<int32_t> tmpl(static_cast<size_t>(n_cls) * stride);
@@ -935,6 +1008,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
         out->classes.push_back(std::move(cl));
       }
     }
+    phase("class detection");
     // class items: each class's rows in Morton order, 32 per item; items
     // interleaved by the Morton position of their first row
     std::vector<std::vector<int32_t>> members(n_cls);
@@ -1013,6 +1087,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       if (err != cudaSuccess) return done(err);
     }
   }
+  phase("class items");
   // ---- generic rows: the rest, ordered by (Morton window, signature)
   if (n_rows > 0) row_order_keys<<<grid_for(n_rows, cap), kThreads, 0, s>>>(sig, order, n_rows, window, keys, rows);
   if ((err = cub::DeviceRadixSort::SortPairs(temp, tb, keys, keys2, rows, order, n_rows, 0, 64, s)) != cudaSuccess)
@@ -1089,6 +1164,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
   }
   if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
 
+  phase("generic items");
   // ---- window plan: windows of W consecutive rows in Morton order; their
   // elements (halo included) are computed into shared memory by the window
   // kernel, which then gathers the window's rows (class items with
