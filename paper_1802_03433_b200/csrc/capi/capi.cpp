@@ -114,10 +114,6 @@ void load_module(ff_form* f, int w) {
     ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_grows[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     kGatherSmemMax, f->ctx->device),
                     "row-gather shared memory attribute");
-    ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_ginv[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    codegen::gather_invariants_smem(f->plan, f->block),
-                                                    f->ctx->device),
-                    "K2a shared memory attribute");
   } else {
     cudaGetLastError();
     f->kernel_ginv[w] = f->kernel_grows[w] = nullptr;
@@ -449,7 +445,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       void* args[] = {&coords, &vconn, &dconn, &eorder, &ne, &ginv, &status};
       const unsigned grid = static_cast<unsigned>((m->ne + f->block - 1) / f->block);
       ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_ginv[w]), dim3(grid), dim3(f->block),
-                                       args, codegen::gather_invariants_smem(f->plan, f->block), s),
+                                       args, 0, s),
                       "K2a (element invariants) launch");
     }
   }

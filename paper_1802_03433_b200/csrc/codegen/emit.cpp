@@ -95,11 +95,10 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
 
 bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size) {
   // a reference-tensor plan and <= 12 slot bytes per record (node rows for
-  // vector forms); K2a stages [block / 32][32][FF_GS + 1] doubles in shared
-  // memory
+  // vector forms)
+  (void)block_size;
   return plan.n_kinv > 0 && ncomp >= 1 && n_local / ncomp <= 12 &&
-         (ncomp == 1 ? plan.n_kinv + n_local <= 24 : plan.n_kinv <= 64) &&
-         gather_invariants_smem(plan, block_size) <= 200 * 1024;
+         (ncomp == 1 ? plan.n_kinv + n_local <= 24 : plan.n_kinv <= 64);
 }
 
 namespace {
@@ -216,16 +215,23 @@ __device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, do
 }
 __device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
 #endif
-// element record: invariants [E][FF_GS] (256-bit loads), load vector [FF_NLOC][E]
+// element record: invariants in FF_GS / 4 chunk arrays [E][4] (vector forms: rows [E][FF_GS]; 256-bit
+// loads), load vector [FF_NLOC][E]
 // (idle lanes, e < 0, only occur in rows that are never written: they read
 // element 0 instead of branching)
 __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, ff_i64 n_elems,
                                          double (&g)[FF_NKP], double& b) {
   const ff_i64 ee = e >= 0 ? e : 0;
-  const double* base = einv + ee * FF_GS;
   double t[FF_GS];
 #pragma unroll
-  for (int q = 0; q < FF_GS / 4; ++q) ff_ld4(base + 4 * q, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+  for (int q = 0; q < FF_GS / 4; ++q) {
+#if FF_BS == 1
+    const double* src = einv + (ff_i64)q * n_elems * 4 + ee * 4;  // chunk arrays [FF_GS / 4][E][4]
+#else
+    const double* src = einv + ee * FF_GS + 4 * q;  // vector forms: one row per element
+#endif
+    ff_ld4(src, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+  }
 #pragma unroll
   for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
   b = ff_ld1(einv + n_elems * FF_GS + (ff_i64)i * n_elems + ee);

@@ -159,10 +159,6 @@ struct RowClass {
   std::vector<std::uint8_t> slots;   // [steps][n_local] slot of column dof[j] in the row
 };
 
-// Dynamic shared memory of K2a (ff_gather_invariants): per-warp record staging.
-inline int gather_invariants_smem(const ElementPlan& plan, int block_size) {
-  return block_size * (((plan.n_kinv + 3) / 4) * 4 + 1) * 8;
-}
 // Whether the plan's kernels include the row gather (K2a + generic K2b).
 bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size);
 
