@@ -46,6 +46,31 @@ RowTileParams rowtile_params(int n_local, int block_size) {
   return p;
 }
 
+// Invariant loads for the element-record layout (FF_NFULL / FF_GTAIL /
+// FF_GSTORE macros); shared by the form module (K2a, generic gather) and the
+// class-specialised module so both read what K2a wrote.
+const char* const kInvariantLoad = R"(// invariants of record e into t (scalar forms: FF_NFULL chunk arrays [E][4]
+// and the tail array; vector forms: rows [E][FF_GS])
+__device__ __forceinline__ void ff_load_inv(const double* __restrict__ einv, ff_i64 n, ff_i64 e, double (&t)[FF_GS]) {
+#if FF_BS == 1
+#pragma unroll
+  for (int c = 0; c < FF_NFULL; ++c)
+    ff_ld4(einv + (ff_i64)c * n * 4 + e * 4, t[4 * c], t[4 * c + 1], t[4 * c + 2], t[4 * c + 3]);
+#if FF_GTAIL == 4
+  ff_ld4(einv + (ff_i64)FF_NFULL * n * 4 + e * 4, t[4 * FF_NFULL], t[4 * FF_NFULL + 1], t[4 * FF_NFULL + 2],
+         t[4 * FF_NFULL + 3]);
+#elif FF_GTAIL == 2
+  ff_ld2(einv + (ff_i64)FF_NFULL * n * 4 + e * 2, t[4 * FF_NFULL], t[4 * FF_NFULL + 1]);
+  t[4 * FF_NFULL + 2] = 0.0;
+  t[4 * FF_NFULL + 3] = 0.0;
+#endif
+#else
+#pragma unroll
+  for (int q = 0; q < FF_GS / 4; ++q) ff_ld4(einv + e * FF_GS + 4 * q, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+#endif
+}
+)";
+
 std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg) {
   return emit_source(f, cfg, nullptr);
 }
@@ -76,6 +101,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   fill(text, "ELEMENT_BODY", body);
   fill(text, "ELEMENT_PRELUDE", plan.prelude);
   const bool gather = gather_capable(plan, f.n_local, f.ncomp, cfg.block_size);
+  fill(text, "INVARIANT_LOAD", gather ? kInvariantLoad : "");
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
   {
@@ -195,6 +221,9 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "#define FF_NLOC " << n_local << "\n#define FF_BS " << bs << "\n#define FF_NB " << nb
      << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
      << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((plan.n_kinv + 3) / 4) * 4 << "\n"
+     << "#define FF_NFULL (FF_NKINV / 4)\n"
+     << "#define FF_GTAIL (FF_NKINV % 4 == 0 ? 0 : ((FF_NKINV % 4 <= 2 && FF_NLOC <= 4) ? 2 : 4))\n"
+     << "#if FF_BS == 1\n#define FF_GSTORE (4 * FF_NFULL + FF_GTAIL)\n#else\n#define FF_GSTORE FF_GS\n#endif\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
      << class_stage_pitch(classes, 1, fused) << "\n"
@@ -205,6 +234,9 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
 __device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, double& c, double& d) {
   asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
+__device__ __forceinline__ void ff_ld2(const double* p, double& a, double& b) {
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+}
 // load-vector entries stay L1-allocating: the lanes of a class item and the
 // items of a CTA read neighbouring elements' entry i, which share lines
 // (2.81 -> 2.61 ms at the north star against no-allocate, run 72)
@@ -213,28 +245,23 @@ __device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
 __device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, double& c, double& d) {
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
+__device__ __forceinline__ void ff_ld2(const double* p, double& a, double& b) {
+  asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+}
 __device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
 #endif
-// element record: invariants in FF_GS / 4 chunk arrays [E][4] (vector forms: rows [E][FF_GS]; 256-bit
-// loads), load vector [FF_NLOC][E]
+)" << kInvariantLoad << R"(
+// element record: invariants (ff_load_inv), load vector [FF_NLOC][E]
 // (idle lanes, e < 0, only occur in rows that are never written: they read
 // element 0 instead of branching)
 __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, ff_i64 n_elems,
                                          double (&g)[FF_NKP], double& b) {
   const ff_i64 ee = e >= 0 ? e : 0;
   double t[FF_GS];
-#pragma unroll
-  for (int q = 0; q < FF_GS / 4; ++q) {
-#if FF_BS == 1
-    const double* src = einv + (ff_i64)q * n_elems * 4 + ee * 4;  // chunk arrays [FF_GS / 4][E][4]
-#else
-    const double* src = einv + ee * FF_GS + 4 * q;  // vector forms: one row per element
-#endif
-    ff_ld4(src, t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
-  }
+  ff_load_inv(einv, n_elems, ee, t);
 #pragma unroll
   for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
-  b = ff_ld1(einv + n_elems * FF_GS + (ff_i64)i * n_elems + ee);
+  b = ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)i * n_elems + ee);
 }
 #define FF_PRE 8  // records of the next item prefetched while this item computes
 // CSR value stores: streaming (evict-first) for scalar rows, which are written
