@@ -437,7 +437,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     ffb::cuda_check(cudaMemsetAsync(status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
     if (m->ne > 0) {
       const double* coords = m->coords;
-      const int32_t* vconn = m->vconn;
+      const int32_t* vconn = p->gather.vconn_m;  // vertex ids in record order
       const int32_t* dconn = m->dconn;
       long long ne = m->ne;
       double* ginv = p->ginv;

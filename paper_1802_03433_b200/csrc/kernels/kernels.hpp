@@ -54,6 +54,7 @@ struct GatherPlan {
   int64_t n_citems = 0, n_citems_short = 0, n_crec = 0, n_class_rows = 0;
   int32_t* citem_class = nullptr;   // [n_citems]
   int32_t* citem_rows = nullptr;    // [n_citems][32] local row or -1
+  int32_t* vconn_m = nullptr;       // [E][dim+1] vertex ids in record (Morton) order, read by K2a
   int64_t* citem_rec = nullptr;     // [n_citems] first record of the item ([steps][32] element ids)
   int32_t* crec = nullptr;          // [n_crec] element records (-1: idle lane)
   // element order of the per-element records: record t belongs to element

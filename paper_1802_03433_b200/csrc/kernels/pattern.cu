@@ -479,6 +479,16 @@ __global__ void class_verify(int32_t* __restrict__ cls, int64_t n_rows, const in
 }
 
 // class item records: [steps][32] element ids of each item (incidence order)
+// out[t][c] = in[order[t]][c] for c < cols (row stride in_stride)
+__global__ void gather_rows_i32(const int32_t* __restrict__ in, int in_stride, int cols,
+                                const int32_t* __restrict__ order, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; f < n * cols;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = f / cols;
+    out[f] = in[static_cast<int64_t>(order[t]) * in_stride + f % cols];
+  }
+}
+
 __global__ void fill_class_records(const int32_t* __restrict__ erank, const int32_t* __restrict__ citem_class,
                                    const int32_t* __restrict__ citem_rows,
                                    const int64_t* __restrict__ citem_rec, int64_t n_citems,
@@ -882,6 +892,12 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     if ((err = need_temp(te)) != cudaSuccess) return cudaFree(ek), cudaFree(ek2), cudaFree(eid), done(err);
     err = cub::DeviceRadixSort::SortPairs(temp, te, ek, ek2, eid, out->eorder, ne, 0, 64, s);
     if (err == cudaSuccess) invert_perm<<<grid_for(ne, cap), kThreads, 0, s>>>(out->eorder, ne, out->erank);
+    // vertex ids in record order for K2a (P1: the DOF ids are the vertices)
+    if (err == cudaSuccess) err = cudaMalloc(&out->vconn_m, ne * (dim + 1) * sizeof(int32_t));
+    if (err == cudaSuccess)
+      gather_rows_i32<<<grid_for(ne * (dim + 1), cap), kThreads, 0, s>>>(k == dim + 1 ? d_dconn : d_vconn,
+                                                                        k == dim + 1 ? k : dim + 1, dim + 1,
+                                                                        out->eorder, ne, out->vconn_m);
     if (err == cudaSuccess) err = cudaStreamSynchronize(s);
     cudaFree(ek);
     cudaFree(ek2);
@@ -1365,6 +1381,7 @@ void free_gather_plan(GatherPlan* p) {
   cudaFree(p->erank);
   cudaFree(p->citem_class);
   cudaFree(p->citem_rows);
+  cudaFree(p->vconn_m);
   cudaFree(p->citem_rec);
   cudaFree(p->crec);
   cudaFree(p->item_order);
