@@ -309,7 +309,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // element records bypass L1 allocation (streamed once per lane; -6 %, run 27)
   // (vector forms read each record once per component pair: keep L1)
   if (!std::getenv("FF_EINV_L1") && f->ncomp == 1) src = "#define FF_EINV_NA 1\n" + src;
-  for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L"})
+  for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L", "FF_WUNROLL"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
