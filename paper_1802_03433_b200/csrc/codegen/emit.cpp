@@ -265,8 +265,9 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
 }
 #define FF_PRE 8  // records of the next item prefetched while this item computes
 #ifndef FF_WUNROLL
-#define FF_WUNROLL 32  // write-out loop unroll (full: 2.499 vs 2.517 ms at NS with 4, run 91)
+#define FF_WUNROLL 32  // write-out loop unroll (NS 2.484 vs 2.514 ms with 4, run 94)
 #endif
+constexpr int ff_wunroll = FF_WUNROLL;  // (#pragma unroll takes a constant expression, not a macro)
 // CSR value stores: streaming (evict-first) for scalar rows, which are written
 // whole; vector sub-rows fill every FF_BS-th value, so their lines must stay
 // in L2 until the other component pairs' CTAs complete them
@@ -284,7 +285,7 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, int sp, 
                                          int lane, int cnt, int q0, double* __restrict__ values) {
   __syncwarp();
   if (lane < cnt) {
-#pragma unroll FF_WUNROLL
+#pragma unroll ff_wunroll
     for (int m = 0; m < 32; ++m) {
       const ff_i64 rb = sr[m];
       if (rb >= 0) ff_stv(values + rb + FF_BS * (q0 + lane), st[m * sp + lane]);
@@ -300,7 +301,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   __syncwarp();
   if (lane < cnt) {
     const int off = __ldg(map + lane);
-#pragma unroll FF_WUNROLL
+#pragma unroll ff_wunroll
     for (int m = 0; m < 32; ++m) {
       const ff_i64 rb = sr[m];
       if (rb >= 0) ff_stv(values + rb + FF_BS * off, st[m * sp + lane]);
@@ -463,7 +464,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  const ff_i32* rec = crec + __ldg(citem_rec + first) * 32 + lane;\n"
           "  int ep[FF_PRE];\n"
           "#pragma unroll\n"
-          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(rec + u * 32);\n"
+          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = u < ff_csteps[c] ? __ldcs(rec + u * 32) : -1;\n"
           "  for (ff_i64 w = first; w < last; ++w) {\n"
           "    int cn = 0, rown = -1, epn[FF_PRE];\n"
           "    const ff_i32* recn = rec;\n"
@@ -472,7 +473,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "      rown = __ldg(citem_rows + (w + 1) * 32 + lane);\n"
           "      recn = crec + __ldg(citem_rec + w + 1) * 32 + lane;\n"
           "#pragma unroll\n"
-          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = __ldcs(recn + u * 32);\n"
+          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = u < ff_csteps[cn] ? __ldcs(recn + u * 32) : -1;\n"
           "    }\n"
           "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
           "    switch (c * FF_NB + cd) {\n";

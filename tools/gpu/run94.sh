@@ -1,0 +1,3 @@
+for i in 1 2; do for v in FF_NONE=1 FF_WUNROLL=8 FF_WUNROLL=32; do
+  echo "ns $v $(env $v timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print(round(d['ms_per_step'],4))")"
+done; done
