@@ -274,6 +274,13 @@ void ensure_window_module(ff_form* f, ff_pattern* p) {
   p->window_key = key;
 }
 
+// Warps per CTA of the class kernels (FF_CWARPS knob): 2 for scalar forms
+// (2.475 vs 2.485 ms at NS with 4, run 98), 4 for vector forms.
+int class_cwarps(const ff_form* f) {
+  const char* v = std::getenv("FF_CWARPS");
+  return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
+}
+
 // Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
 int class_ipw(const ff_form* f) {
   const char* v = std::getenv("FF_IPW");
@@ -301,7 +308,9 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
   const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp);
-  if (fused && !std::getenv("FF_MINB_S")) src = "#define FF_MINB_S 3\n" + src;
+  // register budget: 12 warps/SM (168 registers) whatever the CTA size
+  if (fused && !std::getenv("FF_MINB_S")) src = "#define FF_MINB_S " + std::to_string(12 / class_cwarps(f)) + "\n" + src;
+  if (!std::getenv("FF_CWARPS")) src = "#define FF_CWARPS " + std::to_string(class_cwarps(f)) + "\n" + src;
   // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
   // 82.6 ms at config 5, run 43)
   if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
@@ -309,7 +318,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // element records bypass L1 allocation (streamed once per lane; -6 %, run 27)
   // (vector forms read each record once per component pair: keep L1)
   if (!std::getenv("FF_EINV_L1") && f->ncomp == 1) src = "#define FF_EINV_NA 1\n" + src;
-  for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L", "FF_WUNROLL"})
+  for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
@@ -319,7 +328,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[0], p->class_lib, "ff_gather_classes_s"), "class kernel");
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[1], p->class_lib, "ff_gather_classes_l"), "class kernel");
   for (int c = 0; c < 2; ++c) {
-    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused);
+    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused, class_cwarps(f));
     ffb::cuda_check(cudaKernelSetAttributeForDevice(p->class_kernel[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     p->class_smem[c], p->ctx->device),
                     "class kernel shared memory attribute");
@@ -515,7 +524,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       if (i1 <= i0) continue;
       const int64_t ipw = class_ipw(f);
       // 4 warps x FF_IPW items per CTA; vector forms: one CTA per component pair
-      const unsigned grid = static_cast<unsigned>((i1 - i0 + 4 * ipw - 1) / (4 * ipw) * f->ncomp * f->ncomp);
+      const int cw = class_cwarps(f);
+      const unsigned grid = static_cast<unsigned>((i1 - i0 + cw * ipw - 1) / (cw * ipw) * f->ncomp * f->ncomp);
       const double* ginv = p->ginv;
       long long ne_arg = m->ne;
       const int64_t* row_ptr = p->row_ptr;
@@ -524,7 +534,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
       const int64_t* irec = gp.citem_rec;
       const int32_t* crec = gp.crec;
       void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
-      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(128), args,
+      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(32 * cw), args,
                                        p->class_smem[c], sc),
                       "K2b (class row gather) launch");
     }

@@ -312,6 +312,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
 #ifndef FF_IPW
 #define FF_IPW 2  // consecutive items per warp
 #endif
+#ifndef FF_CWARPS
+#define FF_CWARPS 4  // warps per CTA
+#endif
 #ifndef FF_MINB_S
 #define FF_MINB_S 4  // CTAs per SM the register budgets are sized for
 #endif
@@ -440,7 +443,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "// items are sorted by (Morton window, class): a CTA runs one class (small\n"
           "// instruction footprint per SM) and the items in flight stay spatially\n"
           "// compact (element data reused in L1/L2)\n"
-          "extern \"C\" __global__ void __launch_bounds__(128, "
+          "extern \"C\" __global__ void __launch_bounds__(32 * FF_CWARPS, "
        << (longrows ? "FF_MINB_L" : "FF_MINB_S") << ")\n" << name
        << "(const double* __restrict__ einv, ff_i64 n_elems, const ff_i64* __restrict__ row_ptr,\n"
           "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
@@ -450,11 +453,11 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  extern __shared__ double ff_dsm[];\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
           "  double* st = ff_dsm + wid * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ";\n"
-          "  ff_i64* sr = (ff_i64*)(ff_dsm + 4 * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ") + wid * 32;\n"
+          "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ") + wid * 32;\n"
           "  // vector forms: FF_NB consecutive CTAs run the same items, one component\n"
           "  // pair each (one code path per CTA; the items' records shared in L2)\n"
           "  const int cd = (int)(blockIdx.x % FF_NB);\n"
-          "  const ff_i64 first = i0 + ((ff_i64)(blockIdx.x / FF_NB) * 4 + wid) * FF_IPW;\n"
+          "  const ff_i64 first = i0 + ((ff_i64)(blockIdx.x / FF_NB) * FF_CWARPS + wid) * FF_IPW;\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
           "  // the next item's header and first records load while this item computes\n"

@@ -169,8 +169,8 @@ std::vector<int> class_step_order(const RowClass& k, int n_local);
 // longest class row).
 int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused);
 // Dynamic shared memory of class kernel `kernel` (4 warps).
-inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused) {
-  return 4 * 32 * class_stage_pitch(classes, kernel, fused) * 8 + 4 * 32 * 8;
+inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused, int warps = 4) {
+  return warps * 32 * class_stage_pitch(classes, kernel, fused) * 8 + warps * 32 * 8;
 }
 
 // NVRTC translation unit with ff_gather_classes_s (classes of rows <= 33
