@@ -1,4 +1,4 @@
-# round-1 final artifacts (write-out unroll, prefetch guard)
+# round-1 final artifacts (2-warp class CTAs)
 nvidia-smi --query-gpu=name,clocks.max.sm,memory.total --format=csv,noheader; nproc
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -3 > gpurun_out/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
