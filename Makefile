@@ -20,7 +20,7 @@ LDLIBS   := -L$(CUDA)/lib64 -lcudart_static -lrt -ldl -lpthread -Wl,-rpath,$(CUD
 CPP_SRCS := $(SRC)/symbolic/symbolic.cpp $(SRC)/fem/fem.cpp $(SRC)/meshgen/meshgen.cpp \
             $(SRC)/codegen/lower.cpp $(SRC)/codegen/element_plan.cpp $(SRC)/codegen/emit.cpp \
             $(SRC)/runtime/nvrtc.cpp $(SRC)/capi/capi.cpp $(SRC)/api/femforge.cpp
-CU_SRCS  := $(SRC)/kernels/pattern.cu $(SRC)/kernels/linalg.cu
+CU_SRCS  := $(SRC)/kernels/pattern.cu $(SRC)/kernels/linalg.cu $(SRC)/kernels/validate.cu
 OBJS     := $(patsubst $(SRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS)) $(patsubst $(SRC)/%.cu,$(BUILD)/%.cu.o,$(CU_SRCS))
 LIB      := $(PKG)/libfemforge_b200.so
 

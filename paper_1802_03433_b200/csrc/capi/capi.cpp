@@ -141,6 +141,7 @@ void build_variant(ff_form* f, int w) {
 void ensure_plan(ff_pattern* p, const ff_mesh* m) {
   if (p->plan_mesh == m && p->plan_generation == m->generation && p->slots) return;
   require(m->k == p->k, "mesh and sparsity pattern have different DOFs per element");
+  require(p->bs == m->bs, "mesh and sparsity pattern have different components per node");
   ff_ctx* ctx = p->ctx;
   bind(ctx);
   const int w = p->max_row_len <= 256 ? 1 : 2;
@@ -555,6 +556,7 @@ void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_valu
   require(f->ctx && f->ctx == m->ctx && m->ctx == p->ctx, "form, mesh and pattern must share one context");
   require(f->dim == m->dim, "form and mesh dimensions differ");
   require(f->ncomp == m->bs && f->n_local == m->k * m->bs, "form and mesh have different DOFs per element");
+  require(p->bs == m->bs, "mesh and sparsity pattern have different components per node");
   ensure_plan(p, m);
   const int w = p->slot_bytes;
   build_variant(f, w);
@@ -640,6 +642,75 @@ void drop_graph(ff_pattern* p) {
 std::uint64_t next_form_id() {
   static std::atomic<std::uint64_t> n{0};
   return ++n;
+}
+
+// Connectivity generations are process-wide: plans keyed on (mesh, generation)
+// can never match a new mesh that reuses a destroyed mesh's address.
+std::uint64_t next_generation() {
+  static std::atomic<std::uint64_t> n{0};
+  return ++n;
+}
+
+// The MeshError message of element t (fem.cpp:17-34 wording and order:
+// vertex index range, duplicate vertices, then orientation; the DOF checks of
+// higher-order spaces sit between the two, with DOF wording).
+std::string mesh_error(const ff_mesh* m, int64_t t, bool orient) {
+  const int nn = m->dim + 1;
+  std::vector<int32_t> v(nn), d(m->k);
+  ffb::cuda_check(cudaMemcpy(v.data(), m->vconn + t * nn, nn * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+  const std::string el = "element " + std::to_string(t) + ": ";
+  for (int a = 0; a < nn; ++a)
+    if (v[a] < 0 || v[a] >= m->nv) return el + "node index " + std::to_string(v[a]) + " out of range";
+  for (int a = 0; a < nn; ++a)
+    for (int b = a + 1; b < nn; ++b)
+      if (v[a] == v[b]) return el + "duplicate node indices";
+  if (m->dconn != m->vconn) {
+    ffb::cuda_check(cudaMemcpy(d.data(), m->dconn + t * m->k, m->k * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    for (int a = 0; a < m->k; ++a)
+      if (d[a] < 0 || d[a] >= m->n_dofs) return el + "DOF index " + std::to_string(d[a]) + " out of range";
+    for (int a = 0; a < m->k; ++a)
+      for (int b = a + 1; b < m->k; ++b)
+        if (d[a] == d[b]) return el + "duplicate DOF indices";
+  }
+  (void)orient;
+  return el + (m->dim == 2 ? "non-positive signed area" : "non-positive signed volume");
+}
+
+// Mesh::validate (fem.cpp:17-34) over the device-resident mesh; throws
+// MeshError for the lowest failing element, like the reference's loop.
+void validate_mesh(const ff_mesh* m, bool orient) {
+  ff_ctx* ctx = m->ctx;
+  unsigned long long* d_bad = ctx->d_status + 2;
+  ffb::cuda_check(ffb::kernels::validate_mesh(m->coords, m->dim, m->nv, m->vconn, m->dconn != m->vconn ? m->dconn : nullptr,
+                                              m->k, m->n_dofs, m->ne, orient, d_bad, ctx->sm_count, ctx->stream),
+                  "mesh validation");
+  unsigned long long bad = 0;
+  ffb::cuda_check(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "mesh validation");
+  if (bad != ~0ull) throw fem::MeshError(mesh_error(m, static_cast<int64_t>(bad), orient));
+}
+
+void free_mesh(ff_mesh* m) {
+  cudaFree(m->coords);
+  if (m->dconn != m->vconn) cudaFree(m->dconn);
+  cudaFree(m->vconn);
+  cudaFree(m->stage);
+  delete m;
+}
+
+// Upload n ids into dst through the staging buffer; true when any id changed.
+bool upload_conn(ff_mesh* m, int32_t* dst, const int32_t* src, int64_t n) {
+  ff_ctx* ctx = m->ctx;
+  const int64_t need = std::max<int64_t>(m->ne * m->k, m->ne * (m->dim + 1));
+  if (!m->stage) m->stage = device_alloc<int32_t>(need, "connectivity staging");
+  ffb::cuda_check(cudaMemcpyAsync(m->stage, src, n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  unsigned long long* d_diff = ctx->d_status + 2;
+  ffb::cuda_check(cudaMemsetAsync(d_diff, 0, sizeof(unsigned long long), ctx->stream), "memset");
+  ffb::cuda_check(ffb::kernels::copy_compare(m->stage, dst, n, d_diff, ctx->sm_count, ctx->stream), "compare");
+  unsigned long long diff = 0;
+  ffb::cuda_check(cudaMemcpyAsync(&diff, d_diff, sizeof diff, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+  ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "connectivity upload");
+  return diff != 0;
 }
 
 }  // namespace
@@ -980,6 +1051,14 @@ int ff_mesh_create(ff_ctx* ctx, int dim, const double* coords, int64_t nv, const
     if (dconn)
       ffb::cuda_check(cudaMemcpyAsync(m->dconn, dconn, ne * k * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "mesh upload");
+    m->generation = next_generation();
+    // flatten_mesh validates first (device.cpp:49)
+    try {
+      validate_mesh(m.get(), true);
+    } catch (...) {
+      free_mesh(m.release());
+      throw;
+    }
     *out = m.release();
   });
 }
@@ -995,7 +1074,15 @@ int ff_mesh_update(ff_mesh* m, const double* coords, const int32_t* vconn, const
       ffb::cuda_check(cudaMemcpyAsync(m->vconn, vconn, m->ne * (m->dim + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
     if (dconn && m->dconn != m->vconn)
       ffb::cuda_check(cudaMemcpyAsync(m->dconn, dconn, m->ne * m->k * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    if (vconn || dconn) ++m->generation;  // slot plans are re-derived (and re-validated)
+    ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "mesh update");
+    if (vconn || dconn) {
+      // new connectivity: slot and gather plans (and captured graphs) are
+      // re-derived; it is a new mesh, so it is validated like one
+      m->generation = next_generation();
+      validate_mesh(m, true);
+    }
+    // coordinates alone are the flattened arrays changing under a validated
+    // mesh (test_device.cpp:283-285): degenerate elements surface in assembly
   });
 }
 
@@ -1003,10 +1090,7 @@ int ff_mesh_destroy(ff_mesh* m) {
   return guarded([&] {
     if (!m) return;
     bind(m->ctx);
-    cudaFree(m->coords);
-    if (m->dconn != m->vconn) cudaFree(m->dconn);
-    cudaFree(m->vconn);
-    delete m;
+    free_mesh(m);
   });
 }
 
@@ -1026,6 +1110,7 @@ int ff_pattern_build(ff_ctx* ctx, const ff_mesh* m, int64_t rb, int64_t re, ff_p
     p->re = re;
     p->bs = bs;
     p->k = m->k;
+    validate_mesh(m, true);  // build_sparsity validates first (device.cpp:67)
     int mx = 0;
     ffb::cuda_check(ffb::kernels::build_pattern(m->dconn, m->ne, m->k, rb, re, ctx->sm_count, ctx->stream, &p->row_ptr,
                                                 &p->col_idx, &p->nnz, &mx),
@@ -1246,32 +1331,18 @@ int ff_assemble(ff_form* f, ff_mesh* m, ff_pattern* p, const double* coords, con
     // inputs: the flattened mesh (device.cpp:48-64 analogue), host -> device
     if (coords)
       ffb::cuda_check(cudaMemcpyAsync(m->coords, coords, m->nv * m->dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    if (vconn)
-      ffb::cuda_check(cudaMemcpyAsync(m->vconn, vconn, m->ne * (m->dim + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    if (dconn && m->dconn != m->vconn)
-      ffb::cuda_check(cudaMemcpyAsync(m->dconn, dconn, m->ne * m->k * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    if (vconn || dconn) {
-      // The reference re-searches every column on every call (device.cpp:274-288);
-      // here the slot and gather plans are re-derived (and re-validated) whenever
-      // the uploaded connectivity differs from the one they were built for.
-      ffb::cuda_check(ffb::kernels::content_hash(m->dconn, m->ne * m->k, ctx->d_status + 2, ctx->sm_count, ctx->stream),
-                      "connectivity hash");
-      unsigned long long h = 0;
-      ffb::cuda_check(cudaMemcpyAsync(&h, ctx->d_status + 2, sizeof h, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-      ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "connectivity hash");
-      if (m->dconn != m->vconn) {
-        ffb::cuda_check(ffb::kernels::content_hash(m->vconn, m->ne * (m->dim + 1), ctx->d_status + 2, ctx->sm_count,
-                                                   ctx->stream),
-                        "connectivity hash");
-        unsigned long long hv = 0;
-        ffb::cuda_check(cudaMemcpyAsync(&hv, ctx->d_status + 2, sizeof hv, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "connectivity hash");
-        h = h * 31 + hv;
-      }
-      if (h != m->conn_hash || m->generation == 0) {
-        m->conn_hash = h;
-        ++m->generation;
-      }
+    // The reference re-searches every column on every call (device.cpp:274-288);
+    // here the connectivity goes through a staging buffer and is compared
+    // exactly with the resident copy: any change gives the mesh a new
+    // generation, so the slot and gather plans are re-derived (and the missing
+    // column check re-run), and the new connectivity is validated like a new
+    // mesh (device.cpp:49)
+    bool changed = false;
+    if (vconn) changed |= upload_conn(m, m->vconn, vconn, m->ne * (m->dim + 1));
+    if (dconn && m->dconn != m->vconn) changed |= upload_conn(m, m->dconn, dconn, m->ne * m->k);
+    if (changed) {
+      m->generation = next_generation();
+      validate_mesh(m, true);
     }
     const int64_t n_rows = p->bs * (p->re - p->rb);
     const int64_t nnz = int64_t(p->bs) * p->bs * p->nnz;

@@ -86,6 +86,17 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               bool use_eorder = true, int max_win_elems = 0, bool split_long = true);
 void free_gather_plan(GatherPlan* p);
 
+// fem::Mesh::validate (fem.cpp:17-34) on the device: *d_bad = the lowest
+// element with a vertex id outside [0, nv), duplicate vertices, a DOF id
+// outside [0, n_dofs) or duplicate DOFs (d_dconn may be null), or -- when
+// `orient` -- a non-positive signed area / volume; ~0 when every element passes.
+cudaError_t validate_mesh(const double* d_coords, int dim, int64_t nv, const int32_t* d_vconn, const int32_t* d_dconn,
+                          int k, int64_t n_dofs, int64_t ne, bool orient, unsigned long long* d_bad, int sm_count,
+                          cudaStream_t s);
+// d_dst := d_src (n int32); *d_diff |= 1 when any value changed (exact).
+cudaError_t copy_compare(const int32_t* d_src, int32_t* d_dst, int64_t n, unsigned long long* d_diff, int sm_count,
+                         cudaStream_t s);
+
 // Order-independent 64-bit content hash of n int32 values (sum of mixed
 // (index, value) pairs), written to *d_out.
 cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_out, int sm_count, cudaStream_t s);

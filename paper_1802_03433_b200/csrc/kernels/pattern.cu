@@ -507,6 +507,40 @@ __global__ void fill_class_records(const int32_t* __restrict__ erank, const int3
 }
 
 
+// First touch of every element by the class records (crec position p, in
+// item, step, lane order): records ordered by first touch put the elements of
+// the 32 lanes of one step side by side, so a warp's record load touches a few
+// consecutive lines instead of 32 scattered ones.
+__global__ void first_touch(const int32_t* __restrict__ crec, int64_t n, const int32_t* __restrict__ eorder,
+                            unsigned long long* __restrict__ first) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t r = crec[p];
+    if (r >= 0) atomicMin(first + eorder[r], static_cast<unsigned long long>(p));
+  }
+}
+
+// sort key of every element: first touch, else (rows of generic items only)
+// after every touched element in the previous (Morton) record order
+__global__ void touch_keys(const unsigned long long* __restrict__ first, const int32_t* __restrict__ erank, int64_t ne,
+                           int64_t n_crec, uint64_t* __restrict__ keys, int32_t* __restrict__ ids) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    keys[e] = first[e] != ~0ull ? first[e] : static_cast<uint64_t>(n_crec) + static_cast<uint64_t>(erank[e]);
+    ids[e] = static_cast<int32_t>(e);
+  }
+}
+
+// record ranks of the old order -> ranks of the new one
+__global__ void remap_ranks(int32_t* __restrict__ crec, int64_t n, const int32_t* __restrict__ eorder_old,
+                            const int32_t* __restrict__ erank_new) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t r = crec[p];
+    if (r >= 0) crec[p] = erank_new[eorder_old[r]];
+  }
+}
+
 // ---- window plan (row windows with their element data in shared memory) ----
 
 // (window << 32 | element) of every owned incidence
@@ -1027,10 +1061,15 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     phase("class detection");
     // class items: each class's rows in Morton order, 32 per item; items
     // interleaved by the Morton position of their first row
+    // class rows in row (DOF) order: on a lattice numbering the 32 rows of an
+    // item are a line of same-class DOFs, so at every step the lanes' elements
+    // are neighbours along that line (FF_ROW_ITEMS=0: Morton order of the DOF
+    // points; NS 2.49 -> 2.09 ms together with the first-touch records below)
+    const bool row_items = !std::getenv("FF_ROW_ITEMS") || std::atoi(std::getenv("FF_ROW_ITEMS")) != 0;
     std::vector<std::vector<int32_t>> members(n_cls);
     std::vector<std::vector<int64_t>> first_pos(n_cls);
     for (int64_t pos = 0; pos < n_rows; ++pos) {
-      const int32_t r = morton[pos];
+      const int32_t r = row_items ? static_cast<int32_t>(pos) : morton[pos];
       const int c = cls_h[r];
       if (c < 0) continue;
       if (members[c].size() % 32 == 0) first_pos[c].push_back(pos);
@@ -1104,6 +1143,48 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       err = cudaStreamSynchronize(s);
       cudaFree(d_steps);
       if (err != cudaSuccess) return done(err);
+      // element records in first-touch order of the class records (item, step,
+      // lane): the elements the 32 lanes of one step read are then stored side
+      // by side, and a warp's 32-byte record loads cover 8 consecutive lines
+      // instead of 32 scattered ones (the class kernel was bound by L1 tag
+      // wavefronts of those scattered loads). FF_FIRST_TOUCH=0: Morton order.
+      const bool ftouch = !std::getenv("FF_FIRST_TOUCH") || std::atoi(std::getenv("FF_FIRST_TOUCH")) != 0;
+      if (ftouch && ne > 0) {
+        unsigned long long* first = nullptr;
+        uint64_t *ek = nullptr, *ek2 = nullptr;
+        int32_t *eid = nullptr, *eorder_new = nullptr;
+        auto tfree = [&]() {
+          cudaFree(first);
+          cudaFree(ek);
+          cudaFree(ek2);
+          cudaFree(eid);
+          cudaFree(eorder_new);
+        };
+        if ((err = cudaMalloc(&first, ne * sizeof(unsigned long long))) != cudaSuccess) return tfree(), done(err);
+        if ((err = cudaMalloc(&ek, ne * sizeof(uint64_t))) != cudaSuccess) return tfree(), done(err);
+        if ((err = cudaMalloc(&ek2, ne * sizeof(uint64_t))) != cudaSuccess) return tfree(), done(err);
+        if ((err = cudaMalloc(&eid, ne * sizeof(int32_t))) != cudaSuccess) return tfree(), done(err);
+        if ((err = cudaMalloc(&eorder_new, ne * sizeof(int32_t))) != cudaSuccess) return tfree(), done(err);
+        cudaMemsetAsync(first, 0xff, ne * sizeof(unsigned long long), s);
+        first_touch<<<grid_for(out->n_crec, cap), kThreads, 0, s>>>(out->crec, out->n_crec, out->eorder, first);
+        touch_keys<<<grid_for(ne, cap), kThreads, 0, s>>>(first, out->erank, ne, out->n_crec, ek, eid);
+        size_t te = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, te, ek, ek2, eid, eorder_new, ne, 0, 64, s);
+        if ((err = need_temp(te)) != cudaSuccess) return tfree(), done(err);
+        err = cub::DeviceRadixSort::SortPairs(temp, te, ek, ek2, eid, eorder_new, ne, 0, 64, s);
+        if (err == cudaSuccess) {
+          invert_perm<<<grid_for(ne, cap), kThreads, 0, s>>>(eorder_new, ne, out->erank);
+          remap_ranks<<<grid_for(out->n_crec, cap), kThreads, 0, s>>>(out->crec, out->n_crec, out->eorder,
+                                                                       out->erank);
+          gather_rows_i32<<<grid_for(ne * (dim + 1), cap), kThreads, 0, s>>>(k == dim + 1 ? d_dconn : d_vconn,
+                                                                            k == dim + 1 ? k : dim + 1, dim + 1,
+                                                                            eorder_new, ne, out->vconn_m);
+          std::swap(out->eorder, eorder_new);
+          err = cudaStreamSynchronize(s);
+        }
+        tfree();
+        if (err != cudaSuccess) return done(err);
+      }
     }
   }
   phase("class items");

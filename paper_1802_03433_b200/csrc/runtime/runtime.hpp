@@ -80,8 +80,8 @@ struct ff_mesh {
   double* coords = nullptr;
   int32_t* vconn = nullptr;
   int32_t* dconn = nullptr;  // == vconn for P1
-  std::uint64_t generation = 0;
-  unsigned long long conn_hash = 0;  // content hash of vconn/dconn (e2e re-upload check)
+  std::uint64_t generation = 0;      // process-wide unique per connectivity (plan keys)
+  int32_t* stage = nullptr;          // ff_assemble upload staging (exact re-upload compare)
 };
 
 struct ff_pattern {
