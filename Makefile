@@ -23,11 +23,12 @@ CPP_SRCS := $(SRC)/symbolic/symbolic.cpp $(SRC)/fem/fem.cpp $(SRC)/meshgen/meshg
 CU_SRCS  := $(SRC)/kernels/pattern.cu $(SRC)/kernels/linalg.cu $(SRC)/kernels/validate.cu
 OBJS     := $(patsubst $(SRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRCS)) $(patsubst $(SRC)/%.cu,$(BUILD)/%.cu.o,$(CU_SRCS))
 LIB      := $(PKG)/libfemforge_b200.so
+ARCHIVE  := $(BUILD)/libfemforge_b200.a
 
 TEST_SRCS := $(wildcard tests/cpp/test_*.cpp)
 TEST_BINS := $(patsubst tests/cpp/%.cpp,$(BUILD)/tests/%,$(TEST_SRCS))
 
-all: $(LIB) $(TEST_BINS)
+all: $(LIB) $(ARCHIVE) $(TEST_BINS)
 
 $(BUILD)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/include/femforge/*.hpp) include/femforge_b200.h $(SRC)/runtime/runtime.hpp $(SRC)/kernels/assemble_template.inc
 	@mkdir -p $(dir $@)
@@ -37,12 +38,19 @@ $(BUILD)/%.cu.o: $(SRC)/%.cu $(SRC)/kernels/kernels.hpp
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIB): $(OBJS)
-	$(CXX) -shared -o $@ $(OBJS) $(LDLIBS)
+# the shared library exports the C ABI only (ff_*; exports.map)
+$(LIB): $(OBJS) $(SRC)/capi/exports.map
+	$(CXX) -shared -o $@ $(OBJS) -Wl,--version-script=$(SRC)/capi/exports.map $(LDLIBS)
 
-$(BUILD)/tests/%: tests/cpp/%.cpp tests/cpp/check.hpp $(LIB)
+$(ARCHIVE): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(CXX) $(CXXFLAGS) -Itests/cpp $< -o $@ -L$(PKG) -lfemforge_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' $(LDLIBS)
+	rm -f $@ && ar rcs $@ $(OBJS)
+
+# C++ host-API suites link the static archive (the C++ API is not exported
+# by the shared library)
+$(BUILD)/tests/%: tests/cpp/%.cpp tests/cpp/check.hpp $(ARCHIVE)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -Itests/cpp $< -o $@ $(ARCHIVE) $(LDLIBS)
 
 oracle:
 	$(MAKE) -C oracle

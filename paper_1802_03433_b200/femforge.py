@@ -334,6 +334,7 @@ class Mesh:
             _ok(lib().ff_mesh_set_components(h, ncomp))
 
     def update(self, coords=None, vconn=None, dconn=None):
+        coords, vconn, dconn = _mesh_arrays(self, coords, vconn, dconn)
         _ok(lib().ff_mesh_update(self.h, _ptr(coords), _ptr(vconn), _ptr(dconn)))
 
     def close(self):
@@ -419,11 +420,40 @@ def assemble_device_ex(form, mesh, pattern, values_ptr, rhs_ptr, stream=None, fl
                                     _stream(stream), flags))
 
 
+def _mesh_arrays(mesh, coords, vconn, dconn):
+    """Caller mesh arrays as the C ABI reads them: C-contiguous float64 /
+    int32 of exactly the mesh's sizes (the library copies nv*dim, ne*(dim+1)
+    and ne*k values from the raw pointers)."""
+    def conv(a, dtype, n, what):
+        if a is None:
+            return None
+        a = np.ascontiguousarray(a, dtype)
+        if a.size != n:
+            raise ValueError(f"{what}: {a.size} values, the mesh needs {n}")
+        return a
+    coords = conv(coords, np.float64, mesh.coords.shape[0] * mesh.dim, "coords")
+    vconn = conv(vconn, np.int32, mesh.n_elems * (mesh.dim + 1), "vconn")
+    if dconn is not None and mesh.dconn is None:
+        raise ValueError("dconn given for a mesh whose DOFs are its vertices")
+    dconn = conv(dconn, np.int32, mesh.n_elems * mesh.k, "dconn")
+    return coords, vconn, dconn
+
+
+def _out_array(a, n, what):
+    if a is None:
+        return np.empty(n)
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.size == n
+            and a.flags.writeable):
+        raise ValueError(f"{what}: needs a writable C-contiguous float64 array of {n} values")
+    return a
+
+
 def assemble(form, mesh, pattern, coords=None, vconn=None, dconn=None, values=None, rhs=None):
     """End-to-end with host buffers (assemble_sparse's call shape): uploads the
     given mesh arrays, assembles, returns host (values, rhs)."""
-    values = np.empty(pattern.nnz) if values is None else values
-    rhs = np.empty(pattern.n_rows) if rhs is None else rhs
+    coords, vconn, dconn = _mesh_arrays(mesh, coords, vconn, dconn)
+    values = _out_array(values, pattern.nnz, "values")
+    rhs = _out_array(rhs, pattern.n_rows, "rhs")
     st = Stats()
     _ok(lib().ff_assemble(form.h, mesh.h, pattern.h, _ptr(coords), _ptr(vconn), _ptr(dconn), _ptr(values), _ptr(rhs),
                           C.byref(st)))
