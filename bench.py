@@ -43,14 +43,12 @@ CONFIGS = {
 METRIC = "assembled elements/sec (3D P2 Poisson tets)"
 STEP_DESC = {
     "atomic": "K0 zero-fill + K2 element kernel with fp64-RED scatter",
-    "rowtile": "K2 row-tile element kernel (atomic-free, each CSR value written once)",
     "gather": "K2a element invariants + K2b row gather (class-specialised + generic; atomic-free, each CSR value "
               "written once, no zero-fill), one ff_assemble_device call per step (replayed CUDA graph); "
               "k2a_ms / k2_ms from a separate phase-split run",
 }
 KERNEL_DESC = {
     "atomic": "ff_assemble_atomic (K2)",
-    "rowtile": "ff_assemble_rowtile (K2)",
     "gather": "ff_gather_invariants + ff_gather_classes_s/_l + ff_gather_rows (K2a + K2b, the whole step)",
 }
 UNIT = "elements/s"
@@ -255,7 +253,7 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=2.0)
     ap.add_argument("--block", type=int, default=256)
     ap.add_argument("--strategy", default="auto")
-    ap.add_argument("--scatter", default="gather", choices=["gather", "rowtile", "atomic"])
+    ap.add_argument("--scatter", default="gather", choices=["gather", "atomic"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = the 1-GPU workload stacked N times (one cell per GPU); "
                          "strong = row blocks of the one 1-GPU mesh")
@@ -476,8 +474,8 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e if e2e is not None else ({"skipped": e2e_note} if e2e_note else None),
         # ours only (the L2 flush is a torch fill): gather = K2a + class + generic
-        # launches (plan-dependent), atomic = K0 + K2, rowtile = one kernel
-        "gpu_launches": (gather_info["launches"] if scatter == "gather" else 1 if scatter == "rowtile" else 2)
+        # launches (plan-dependent), atomic = K0 + K2
+        "gpu_launches": (gather_info["launches"] if scatter == "gather" else 2)
                         * args.steps,
         "clocks": clocks.summary(),
     }

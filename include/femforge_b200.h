@@ -99,9 +99,9 @@ void* ff_ctx_stream(ff_ctx* ctx); /* cudaStream_t of the context */
  *     CSR row per lane accumulated in shared memory and written once
  *     (atomic-free, deterministic; needs a reference-tensor form, <= 12 DOFs
  *     per element and rows of <= 221 entries, else the atomic kernel runs);
- *   FF_SCATTER_ROWTILE: CTA row tiles with staged element rows (atomic-free);
- *   FF_SCATTER_ATOMIC_MODE: element-parallel fp64 RED after a zero-fill. */
-enum { FF_SCATTER_ROWTILE = 0, FF_SCATTER_ATOMIC_MODE = 1, FF_SCATTER_GATHER_MODE = 2 };
+ *   FF_SCATTER_ATOMIC_MODE: element-parallel fp64 RED after a zero-fill (the
+ *     reference's parallel mode, device.cpp:193-200). */
+enum { FF_SCATTER_ATOMIC_MODE = 1, FF_SCATTER_GATHER_MODE = 2 };
 int ff_ctx_set_scatter(ff_ctx* ctx, int mode);
 
 /* ---- forms: weak form text -> symbolic -> CUDA source -> NVRTC (sm_100a) - */
@@ -159,9 +159,6 @@ typedef struct ff_gather_info {
   double build_ms;
   int n_classes;                            /* row classes with a specialised kernel */
   int64_t n_class_rows, n_class_items;
-  int64_t n_windows;                        /* window plan (0: none): windows of window_rows rows, */
-  int window_rows;                          /* each with <= window_max_elems elements in shared memory */
-  int64_t window_max_elems, n_window_items;
   int launches;                             /* kernel launches per gather assembly (K2a, class, generic) */
 } ff_gather_info;
 /* Row classes of the gather plan: rows with identical incidence sequences
@@ -174,10 +171,6 @@ int ff_ctx_set_gather_classes(ff_ctx* ctx, int64_t min_rows);
  * the concatenated per-step local indices and [steps][n_local] slot bytes. */
 int ff_class_source(const ff_form* form, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
-/* Same classes -> the window row-gather translation unit (form source +
- * ff_gather_windows). */
-int ff_window_source(const ff_form* form, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
-                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
 int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* mesh, ff_gather_info* out);
 /* Which scatter the next assembly of (form, pattern) runs: FF_SCATTER_*_MODE. */
 int ff_scatter_selected(const ff_form* form, const ff_pattern* p, unsigned flags, int* mode);
@@ -190,14 +183,13 @@ int ff_assemble_device(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double
                        void* stream);
 /* Same with flags. Scatter flags override the context mode:
  * FF_SCATTER_ATOMIC (element-parallel fp64 RED, needs K0: FF_SKIP_ZERO = K2
- * only on already-zero buffers, FF_ZERO_ONLY = K0 only), FF_SCATTER_TILES
- * (row tiles), FF_SCATTER_GATHER (row gather; FF_GATHER_INVARIANTS_ONLY /
+ * only on already-zero buffers, FF_ZERO_ONLY = K0 only), FF_SCATTER_GATHER
+ * (row gather; FF_GATHER_INVARIANTS_ONLY /
  * FF_GATHER_ROWS_ONLY launch only its first / second kernel, for timing). */
 enum {
   FF_SKIP_ZERO = 1,
   FF_ZERO_ONLY = 2,
   FF_SCATTER_ATOMIC = 4,
-  FF_SCATTER_TILES = 8,
   FF_SCATTER_GATHER = 16,
   FF_GATHER_INVARIANTS_ONLY = 32,
   FF_GATHER_ROWS_ONLY = 64

@@ -91,23 +91,10 @@ void load_module(ff_form* f, int w) {
   ffb::cuda_check(cudaLibraryLoadData(&f->lib[w], f->module[w].cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
                   "cudaLibraryLoadData");
   ffb::cuda_check(cudaLibraryGetKernel(&f->kernel[w], f->lib[w], "ff_assemble_atomic"), "cudaLibraryGetKernel");
-  // which optional kernels the module holds: known from the template for
-  // generated forms (row tiles: scalar forms; gather: gather_capable); probed
-  // for caller-written sources
-  const bool tile_known = !f->raw, gather_known = !f->raw;
-  const bool has_tile = f->ncomp == 1;
+  // whether the module holds the gather kernels: known from the template for
+  // generated forms (gather_capable); probed for caller-written sources
+  const bool gather_known = !f->raw;
   const bool has_gather = codegen::gather_capable(f->plan, f->n_local, f->ncomp, f->block);
-  if ((tile_known ? has_tile : true) &&
-      cudaLibraryGetKernel(&f->kernel_tile[w], f->lib[w], "ff_assemble_rowtile") == cudaSuccess) {
-    f->tile = codegen::rowtile_params(f->n_local, f->block);
-    f->tile_smem[w] = f->tile.smem_bytes(f->n_local, w);
-    ffb::cuda_check(cudaKernelSetAttributeForDevice(f->kernel_tile[w], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    f->tile_smem[w], f->ctx->device),
-                    "row-tile shared memory attribute");
-  } else {
-    cudaGetLastError();
-    f->kernel_tile[w] = nullptr;
-  }
   if ((gather_known ? has_gather : true) &&
       cudaLibraryGetKernel(&f->kernel_ginv[w], f->lib[w], "ff_gather_invariants") == cudaSuccess &&
       cudaLibraryGetKernel(&f->kernel_grows[w], f->lib[w], "ff_gather_rows") == cudaSuccess) {
@@ -169,50 +156,6 @@ void ensure_plan(ff_pattern* p, const ff_mesh* m) {
   }
 }
 
-void free_tile_plan(ff_pattern* p) {
-  cudaFree(p->tile_row);
-  cudaFree(p->tile_vptr);
-  cudaFree(p->visit_elem);
-  cudaFree(p->visit_stage);
-  p->tile_row = p->tile_vptr = nullptr;
-  p->visit_elem = nullptr;
-  p->visit_stage = nullptr;
-  p->tile_generation = ~0ull;
-}
-
-// Row tiles: greedy contiguous row ranges with <= tp.rows rows and <= tp.acc
-// CSR slots, then the element visits of every tile (K1-style sort + unique).
-void ensure_tile_plan(ff_pattern* p, const ff_mesh* m, const codegen::RowTileParams& tp) {
-  if (p->tile_generation == m->generation && p->plan_mesh == m && p->tile_acc == tp.acc && p->tile_rows == tp.rows &&
-      p->tile_stage == tp.stage && p->tile_chunk == tp.chunk && p->tile_row)
-    return;
-  free_tile_plan(p);
-  ff_ctx* ctx = p->ctx;
-  bind(ctx);
-  const int64_t n = p->re - p->rb;
-  std::vector<int64_t> rp(n + 1);
-  ffb::cuda_check(cudaMemcpy(rp.data(), p->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost), "row_ptr D2H");
-  std::vector<int64_t> tiles{0};
-  for (int64_t r = 0; r < n;) {
-    const int64_t start = r;
-    if (rp[r + 1] - rp[r] > tp.acc) throw Error(FF_E_ARG, "row " + std::to_string(p->rb + r) + " is longer than a row tile");
-    while (r < n && r - start < tp.rows && rp[r + 1] - rp[start] <= tp.acc) ++r;
-    tiles.push_back(r);
-  }
-  p->n_tiles = static_cast<int64_t>(tiles.size()) - 1;
-  p->tile_row = device_alloc<int64_t>(tiles.size(), "tile rows");
-  ffb::cuda_check(cudaMemcpy(p->tile_row, tiles.data(), tiles.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "H2D");
-  ffb::cuda_check(ffb::kernels::build_rowtile_plan(m->dconn, m->ne, m->k, p->rb, n, p->tile_row, p->n_tiles, tp.stage,
-                                                   tp.chunk, ctx->sm_count, ctx->stream, &p->tile_vptr, &p->visit_elem,
-                                                   &p->visit_stage, &p->n_visits),
-                  "row-tile plan");
-  p->tile_generation = m->generation;
-  p->tile_acc = tp.acc;
-  p->tile_rows = tp.rows;
-  p->tile_stage = tp.stage;
-  p->tile_chunk = tp.chunk;
-}
-
 void free_class_module(ff_pattern* p) {
   if (p->class_lib) cudaLibraryUnload(p->class_lib);
   p->class_lib = nullptr;
@@ -220,63 +163,13 @@ void free_class_module(ff_pattern* p) {
   p->class_key.clear();
 }
 
-void free_window_module(ff_pattern* p) {
-  if (p->window_lib) cudaLibraryUnload(p->window_lib);
-  p->window_lib = nullptr;
-  p->window_kernel = nullptr;
-  p->window_key.clear();
-}
-
-// shared-memory budget of the window kernel (element records of one window);
-// FF_WIN_ELEMS overrides (smaller windows, more CTAs per SM)
-int window_max_elems() {
-  const char* v = std::getenv("FF_WIN_ELEMS");
-  return v ? std::max(64, std::atoi(v)) : 280;
-}
-const int kWindowMaxElems = window_max_elems();
-int window_es(const ff_form* f) { return ((f->plan.n_kinv + f->n_local + 1) & ~1) + 2; }  // FF_ES
-
 void free_gather(ff_pattern* p) {
   ffb::kernels::free_gather_plan(&p->gather);
   p->gather_generation = ~0ull;
   p->gather_mesh = nullptr;
   free_class_module(p);
-  free_window_module(p);
 }
 
-// NVRTC-compiles the window row-gather kernel of (form, plan).
-void ensure_window_module(ff_form* f, ff_pattern* p) {
-  const std::string key = f->source[1] + "#w" + std::to_string(p->gather_generation) + "#" +
-                          std::to_string(reinterpret_cast<std::uintptr_t>(p->gather.wrec16));
-  if (p->window_key == key && p->window_lib) return;
-  free_window_module(p);
-  std::vector<codegen::RowClass> rc;
-  for (const auto& c : p->gather.classes) {
-    codegen::RowClass r;
-    r.len = c.len;
-    r.steps = c.steps;
-    r.local = c.local;
-    r.slots = c.slots;
-    rc.push_back(std::move(r));
-  }
-  const auto t0 = std::chrono::steady_clock::now();
-  std::string src = codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc);
-  if (const char* v = std::getenv("FF_WMINB"))  // tuning knob: register budget (CTAs per SM)
-    src = "#define FF_WMINB " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
-  const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_windows.cu");
-  bind(p->ctx);
-  ffb::cuda_check(cudaLibraryLoadData(&p->window_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
-                  "cudaLibraryLoadData (windows)");
-  ffb::cuda_check(cudaLibraryGetKernel(&p->window_kernel, p->window_lib, "ff_gather_windows"), "window kernel");
-  ffb::cuda_check(cudaKernelSetAttributeForDevice(p->window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  kWindowMaxElems * window_es(f) * 8, p->ctx->device),
-                  "window kernel shared memory attribute");
-  p->class_compile_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  p->window_key = key;
-}
-
-// Warps per CTA of the class kernels (FF_CWARPS knob): 2 for scalar forms
-// (2.475 vs 2.485 ms at NS with 4, run 98), 4 for vector forms.
 int class_cwarps(const ff_form* f) {
   const char* v = std::getenv("FF_CWARPS");
   return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
@@ -371,7 +264,6 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
-                                                        std::getenv("FF_WINDOWS") ? kWindowMaxElems : 0,
                                                         std::getenv("FF_SPLIT_CLASSES") != nullptr);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
@@ -387,13 +279,11 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
 int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w) {
   int mode = f->ctx ? f->ctx->scatter : FF_SCATTER_GATHER_MODE;
   if (flags & FF_SCATTER_ATOMIC) mode = FF_SCATTER_ATOMIC_MODE;
-  if (flags & FF_SCATTER_TILES) mode = FF_SCATTER_ROWTILE;
   if (flags & (FF_SCATTER_GATHER | FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) mode = FF_SCATTER_GATHER_MODE;
   if (flags & (FF_ZERO_ONLY | FF_SKIP_ZERO)) mode = FF_SCATTER_ATOMIC_MODE;
   if (mode == FF_SCATTER_GATHER_MODE &&
       !(f->kernel_grows[w] && p->max_row_len <= 255 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax))
     mode = FF_SCATTER_ATOMIC_MODE;
-  if (mode == FF_SCATTER_ROWTILE && !f->kernel_tile[w]) mode = FF_SCATTER_ATOMIC_MODE;
   return mode;
 }
 
@@ -402,38 +292,6 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   ff_ctx* ctx = f->ctx;
   ensure_gather_plan(p, m);
   unsigned long long* wstatus = ctx->d_status;
-  if (p->gather.n_win > 0 && f->ncomp == 1 && window_es(f) * 8 * p->gather.win_max_elems <= kWindowMaxElems * window_es(f) * 8) {
-    // window row gather: element records computed in shared memory per window
-    if (flags & FF_GATHER_INVARIANTS_ONLY) {
-      ffb::cuda_check(cudaMemsetAsync(wstatus, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
-      return;
-    }
-    if (!(flags & FF_GATHER_ROWS_ONLY))
-      ffb::cuda_check(cudaMemsetAsync(wstatus, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
-    ensure_window_module(f, p);
-    const ffb::kernels::GatherPlan& gp = p->gather;
-    const double* coords = m->coords;
-    const int32_t* vconn = m->vconn;
-    const int32_t* dconn = m->dconn;
-    const int64_t* weptr = gp.win_eptr;
-    const int32_t* welem = gp.win_elem;
-    const int32_t* wiptr = gp.win_iptr;
-    const int32_t* irows = gp.witem_rows;
-    const int32_t* icls = gp.witem_class;
-    const int32_t* isteps = gp.witem_steps;
-    const int64_t* irec = gp.witem_rec;
-    const int64_t* igoff = gp.witem_goff;
-    const uint16_t* rec16 = gp.wrec16;
-    const uint8_t* gsl = gp.gslot;
-    const int64_t* row_ptr = p->row_ptr;
-    void* args[] = {&coords, &vconn, &dconn, &weptr, &welem, &wiptr, &irows, &icls, &isteps, &irec, &igoff,
-                    &rec16, &gsl, &row_ptr, &d_values, &d_rhs, &wstatus};
-    const int smem = static_cast<int>(gp.win_max_elems) * window_es(f) * 8;
-    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->window_kernel), dim3(static_cast<unsigned>(gp.n_win)),
-                                     dim3(128), args, smem, s),
-                    "K2 (window row gather) launch");
-    return;
-  }
   const int gs = ((f->plan.n_kinv + 3) / 4) * 4;  // FF_GS: invariants [E][gs] + load vectors [k][E]
   const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * (gs + f->n_local);
   if (p->ginv_cap < ng) {
@@ -567,28 +425,6 @@ void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_valu
     launch_gather(f, m, p, d_values, d_rhs, s, flags, w);
     return;
   }
-  if (mode == FF_SCATTER_ROWTILE) {
-    ensure_tile_plan(p, m, f->tile);
-    ffb::cuda_check(cudaMemsetAsync(ctx->d_status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
-    if (p->n_tiles == 0) return;
-    const double* coords = m->coords;
-    const int32_t* vconn = m->vconn;
-    const int32_t* dconn = m->dconn;
-    const void* slots = p->slots;
-    const int64_t* row_ptr = p->row_ptr;
-    long long rb = p->rb, nt = p->n_tiles;
-    const int64_t* tile_row = p->tile_row;
-    const int64_t* tile_vptr = p->tile_vptr;
-    const int32_t* visit_elem = p->visit_elem;
-    const uint16_t* visit_stage = p->visit_stage;
-    unsigned long long* status = ctx->d_status;
-    void* args[] = {&coords, &vconn, &dconn, &slots, &row_ptr, &d_values, &d_rhs, &rb,
-                    &tile_row, &tile_vptr, &visit_elem, &visit_stage, &nt, &status};
-    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_tile[w]), dim3(static_cast<unsigned>(nt)),
-                                     dim3(f->block), args, f->tile_smem[w], s),
-                    "K2 (row tiles) launch");
-    return;
-  }
   if (!(flags & FF_SKIP_ZERO))
     ffb::cuda_check(ffb::kernels::zero_fill(d_values, int64_t(p->bs) * p->bs * p->nnz, d_rhs, p->bs * n_rows,
                                             ctx->d_status, ctx->sm_count, s),
@@ -629,7 +465,7 @@ std::vector<std::uint64_t> graph_key(const ff_form* f, const ff_mesh* m, const f
   auto u = [](const void* x) { return static_cast<std::uint64_t>(reinterpret_cast<std::uintptr_t>(x)); };
   return {f->id, u(m), m->generation, u(m->coords), u(m->vconn), u(m->dconn), u(p), p->plan_generation,
           p->gather_generation, u(p->slots), u(p->ginv), u(p->gather.crec), u(p->gather.rec), u(p->class_lib),
-          u(p->window_lib), u(v), u(r), u(s), static_cast<std::uint64_t>(f->ctx->scatter),
+          u(v), u(r), u(s), static_cast<std::uint64_t>(f->ctx->scatter),
           static_cast<std::uint64_t>(f->ctx->class_min_rows)};
 }
 
@@ -775,7 +611,7 @@ void* ff_ctx_stream(ff_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) 
 int ff_ctx_set_scatter(ff_ctx* ctx, int mode) {
   return guarded([&] {
     require(ctx, "null context");
-    require(mode == FF_SCATTER_ROWTILE || mode == FF_SCATTER_ATOMIC_MODE || mode == FF_SCATTER_GATHER_MODE,
+    require(mode == FF_SCATTER_ATOMIC_MODE || mode == FF_SCATTER_GATHER_MODE,
             "unknown scatter mode");
     ctx->scatter = mode;
   });
@@ -787,9 +623,6 @@ int ff_ctx_set_gather_classes(ff_ctx* ctx, int64_t min_rows) {
     ctx->class_min_rows = min_rows;
   });
 }
-
-int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* len, const int32_t* steps,
-                           const int32_t* local, const uint8_t* slots, char* buf, size_t cap, size_t* out_len);
 
 int ff_expr_eval(const char* expr, int dim, const double* pts, int64_t n, double* out) {
   return guarded([&] {
@@ -827,20 +660,9 @@ int ff_form_entry_text(const ff_form* f, int kind, int i, int j, char* buf, size
 
 int ff_class_source(const ff_form* f, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {
-  return class_or_window_source(false, f, n, len, steps, local, slots, buf, cap, out_len);
-}
-
-int ff_window_source(const ff_form* f, int n, const int32_t* len, const int32_t* steps, const int32_t* local,
-                     const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {
-  return class_or_window_source(true, f, n, len, steps, local, slots, buf, cap, out_len);
-}
-
-int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* len, const int32_t* steps,
-                           const int32_t* local, const uint8_t* slots, char* buf, size_t cap, size_t* out_len) {
   return guarded([&] {
     require(f && n >= 0 && (n == 0 || (len && steps && local && slots)), "null argument");
     require(f->plan.n_kinv > 0, "form has no reference-tensor plan (no row gather)");
-    require(!window || f->ncomp == 1, "window gather: scalar forms only");
     const int nsc = f->n_local / f->ncomp;  // slots per incidence (node rows of vector forms)
     std::vector<codegen::RowClass> rc(n);
     int64_t at = 0;
@@ -853,9 +675,8 @@ int class_or_window_source(bool window, const ff_form* f, int n, const int32_t* 
       }
       at += steps[c];
     }
-    const std::string src = window ? codegen::emit_window_source(f->source[1], f->plan, f->n_local, rc)
-                                   : codegen::emit_class_source(f->plan, f->n_local, rc,
-                                                                std::getenv("FF_SPLIT_CLASSES") == nullptr, f->ncomp);
+    const std::string src = codegen::emit_class_source(f->plan, f->n_local, rc,
+                                                       std::getenv("FF_SPLIT_CLASSES") == nullptr, f->ncomp);
     if (out_len) *out_len = src.size();
     if (buf && cap) {
       const std::size_t k = std::min(cap - 1, src.size());
@@ -1192,7 +1013,6 @@ int ff_pattern_destroy(ff_pattern* p) {
     cudaFree(p->vcol_idx);
     cudaFree(p->slots);
     drop_graph(p);
-    free_tile_plan(p);
     free_gather(p);
     cudaFree(p->ginv);
     cudaFree(p->bvec);
@@ -1222,19 +1042,11 @@ int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* m, ff_gather_info* out)
     out->n_classes = static_cast<int>(p->gather.classes.size());
     out->n_class_rows = p->gather.n_class_rows;
     out->n_class_items = p->gather.n_citems;
-    out->n_windows = p->gather.n_win;
-    out->window_rows = p->gather.win_rows;
-    out->window_max_elems = p->gather.win_max_elems;
-    out->n_window_items = p->gather.n_witems;
-    // what launch_gather issues: the window kernel alone, or K2a + the class
-    // kernel(s) + the non-empty generic ranges
+    // what launch_gather issues: K2a + the class kernel(s) + the non-empty
+    // generic ranges
     const auto& g = p->gather;
-    if (g.n_win > 0) {
-      out->launches = 1;
-    } else {
-      out->launches = (m->ne > 0 ? 1 : 0) + (g.n_citems_short > 0) + (g.n_citems > g.n_citems_short) +
-                      (g.n_short > 0) + (g.n_items > g.n_short);
-    }
+    out->launches = (m->ne > 0 ? 1 : 0) + (g.n_citems_short > 0) + (g.n_citems > g.n_citems_short) +
+                    (g.n_short > 0) + (g.n_items > g.n_short);
   });
 }
 

@@ -26,26 +26,6 @@ void fill(std::string& text, const std::string& key, const std::string& value) {
 
 }  // namespace
 
-int RowTileParams::smem_bytes(int n_local, int slot_bytes) const {
-  return 8 * acc + 8 * stage * n_local + 8 * stage + 8 * rows + 4 * 2 * (rows + 1) + 4 * 2 * stage +
-         slot_bytes * stage * n_local;
-}
-
-RowTileParams rowtile_params(int n_local, int block_size) {
-  RowTileParams p;
-  p.chunk = block_size;
-  if (n_local >= 10) {        // 3D P2: ~28 nnz/row
-    p.acc = 6144, p.rows = 256, p.stage = 384;
-  } else if (n_local >= 6) {  // 2D P2
-    p.acc = 6144, p.rows = 512, p.stage = 512;
-  } else if (n_local >= 4) {  // 3D P1: ~15 nnz/row
-    p.acc = 6144, p.rows = 512, p.stage = 768;
-  } else {                    // 2D P1: ~7 nnz/row
-    p.acc = 4096, p.rows = 512, p.stage = 768;
-  }
-  return p;
-}
-
 // Invariant loads for the element-record layout (FF_NFULL / FF_GTAIL /
 // FF_GSTORE macros); shared by the form module (K2a, generic gather) and the
 // class-specialised module so both read what K2a wrote.
@@ -91,10 +71,6 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   fill(text, "NLOC", std::to_string(f.n_local));
   fill(text, "BS", std::to_string(f.ncomp));
   fill(text, "BLOCK", std::to_string(cfg.block_size));
-  const RowTileParams tp = rowtile_params(f.n_local, cfg.block_size);
-  fill(text, "TILE_ACC", std::to_string(tp.acc));
-  fill(text, "TILE_ROWS", std::to_string(tp.rows));
-  fill(text, "TILE_STAGE", std::to_string(tp.stage));
   std::string body = "  // element body: " + std::string(plan.strategy == Strategy::ReferenceTensor ? "reference-tensor" : "pointwise") +
                      " strategy, " + std::to_string(plan.n_quad) + "-point rule " + std::to_string(rule_id) + ", ~" +
                      std::to_string(plan.flops) + " flops\n" + plan.body;
@@ -492,237 +468,6 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   };
   kernel("ff_gather_classes_s", false);
   kernel("ff_gather_classes_l", true);
-  return os.str();
-}
-
-std::string emit_window_source(const std::string& form_source, const ElementPlan& plan, int n_local,
-                               const std::vector<RowClass>& classes) {
-  if (plan.n_kinv <= 0) throw CodegenError("windows need a reference-tensor plan");
-  constexpr int FF_WDEPTH_GEN = 3;  // element records in flight per step batch
-  std::ostringstream os;
-  os << form_source << R"(
-// ===========================================================================
-// window row gather (generated per (form, gather plan)): one CTA per window of
-// consecutive rows (Morton order). Phase 1 computes the per-element records
-// (invariants + load vector) of every element touching the window into shared
-// memory; phase 2 gathers the window's rows from there: class items keep each
-// row in registers indexed by compile-time slots, generic items add into the
-// (zeroed) CSR row through their slot bytes. No atomics; each value written by
-// its row's lane.
-#define FF_ES (FF_EREC + 2)  // shared-memory stride of an element record (bank spread)
-#define FF_SP 17             // staging pitch (odd: conflict-free lane-row stores; 16-slot chunks)
-#define FF_WWARPS 4
-#ifndef FF_WMINB
-#define FF_WMINB 4           // CTAs per SM the register budget is sized for
-#endif
-
-__device__ __forceinline__ void ff_wload(int le, int i, const double* __restrict__ es, double (&g)[FF_NKP],
-                                         double& b) {
-  if (le != 0xffff) {
-    const double* base = es + le * FF_ES;
-    const double2* g2 = (const double2*)base;
-#pragma unroll
-    for (int q = 0; q < FF_NKP / 2; ++q) {
-      const double2 t = g2[q];
-      g[2 * q] = t.x;
-      g[2 * q + 1] = t.y;
-    }
-    b = base[FF_NKINV + i];
-  } else {
-#pragma unroll
-    for (int q = 0; q < FF_NKP; ++q) g[q] = 0.0;
-    b = 0.0;
-  }
-}
-
-// staged rows (<= 16 slots each) -> CSR values: half-warps take one row each,
-// consecutive lanes = consecutive values of a row
-__device__ __noinline__ void ff_wout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane, int cnt,
-                                     int q0, double* __restrict__ values) {
-  __syncwarp();
-  const int h = lane >> 4, j = lane & 15;
-  if (j < cnt) {
-#pragma unroll 4
-    for (int m = h; m < 32; m += 2) {
-      const ff_i64 rb = sr[m];
-      if (rb >= 0) __stcs(values + rb + q0 + j, st[m * FF_SP + j]);
-    }
-  }
-  __syncwarp();
-}
-
-template <int I>
-__device__ __forceinline__ void ff_wgen_row(const double (&g)[FF_NKP], const unsigned char* __restrict__ sl,
-                                            double* __restrict__ vrow) {
-  double v[FF_NLOC];
-  ff_row<I>(g, v);
-#pragma unroll
-  for (int j = 0; j < FF_NLOC; ++j) vrow[sl[j]] += v[j];
-}
-
-// generic item: the lane's row is zeroed, then every contribution is added
-// in place through its slot byte (rows of rare classes only)
-__device__ __noinline__ void ff_wgen(const unsigned short* __restrict__ rec, const unsigned char* __restrict__ gsl,
-                                     const ff_i32* __restrict__ steps, const double* __restrict__ es, int lane,
-                                     ff_i64 rbeg, int len, int row, double* __restrict__ values,
-                                     double* __restrict__ rhs) {
-  double* vrow = values + rbeg;
-  for (int p = 0; p < len; ++p) vrow[p] = 0.0;
-  double bs = 0.0;
-  int st = 0;
-  for (int i = 0; i < FF_NLOC; ++i) {
-    const int n = steps[i];
-    for (int q = 0; q < n; ++q, ++st) {
-      const int le = rec[st * 32];
-      if (le == 0xffff || row < 0) continue;
-      double g[FF_NKP], b;
-      ff_wload(le, i, es, g, b);
-      const unsigned char* sl = gsl + (ff_i64)st * 32 * FF_NLOC;
-      switch (i) {
-)";
-  for (int i = 0; i < n_local; ++i) os << "        case " << i << ": ff_wgen_row<" << i << ">(g, sl, vrow); break;\n";
-  os << R"(        default: break;
-      }
-      bs += b;
-    }
-  }
-  if (row >= 0) __stcs(rhs + row, bs);
-}
-)";
-  // class rows live in registers; rows longer than FF_WPASS entries are
-  // accumulated in slot-range passes (each pass re-reads the element records
-  // from shared memory and computes only its entries) to bound registers
-  constexpr int kPass = 33;
-  auto class_fn = [&](int c) {
-    const RowClass& k = classes[c];
-    const int n_pass = std::max(1, (k.len + kPass - 1) / kPass);
-    const int per = (k.len + n_pass - 1) / n_pass;
-    os << "// class " << c << ": " << k.len << " entries, " << k.steps << " incidences, " << n_pass << " pass(es)\n"
-       << "__device__ __forceinline__ void ff_wcls_" << c
-       << "(const unsigned short* __restrict__ rec, const double* __restrict__ es, double* __restrict__ st,\n"
-          "    ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row, double* __restrict__ values,\n"
-          "    double* __restrict__ rhs) {\n"
-          "  double bs = 0.0;\n"
-          "  sr[lane] = row >= 0 ? rbeg : -1;\n";
-    for (int ps = 0; ps < n_pass; ++ps) {
-      const int lo = ps * per, hi = std::min(k.len, lo + per);
-      os << "  {  // slots [" << lo << ", " << hi << ")\n";
-      for (int p = lo; p < hi; ++p) os << "    double a" << p << " = 0.0;\n";
-      for (int s0 = 0; s0 < k.steps; s0 += FF_WDEPTH_GEN) {
-        const int s1 = std::min(k.steps, s0 + FF_WDEPTH_GEN);
-        os << "    {\n";
-        for (int q = s0; q < s1; ++q)
-          os << "      double g" << q << "[FF_NKP], b" << q << "; ff_wload(rec[" << q * 32 << "], " << k.local[q]
-             << ", es, g" << q << ", b" << q << ");\n";
-        for (int q = s0; q < s1; ++q) {
-          std::string adds;
-          for (int j = 0; j < n_local; ++j) {
-            const int sl = k.slots[q * n_local + j];
-            if (sl >= lo && sl < hi) adds += " a" + std::to_string(sl) + " += v[" + std::to_string(j) + "];";
-          }
-          if (!adds.empty())
-            os << "      { double v[FF_NLOC]; ff_row<" << k.local[q] << ">(g" << q << ", v);" << adds << " }\n";
-          if (ps == 0) os << "      bs += b" << q << ";\n";
-        }
-        os << "    }\n";
-      }
-      for (int q0 = lo; q0 < hi; q0 += 16) {
-        const int cnt = std::min(16, hi - q0);
-        for (int j = 0; j < cnt; ++j) os << "    st[lane * FF_SP + " << j << "] = a" << q0 + j << ";\n";
-        os << "    ff_wout(st, sr, lane, " << cnt << ", " << q0 << ", values);\n";
-      }
-      os << "  }\n";
-    }
-    os << "  if (row >= 0) __stcs(rhs + row, bs);\n}\n";
-  };
-  for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
-  os << R"(
-extern "C" __global__ void __launch_bounds__(FF_WWARPS * 32, FF_WMINB)
-ff_gather_windows(const double* __restrict__ coords, const ff_i32* __restrict__ vconn, const ff_i32* __restrict__ dconn,
-                  const ff_i64* __restrict__ win_eptr, const ff_i32* __restrict__ win_elem,
-                  const ff_i32* __restrict__ win_iptr, const ff_i32* __restrict__ witem_rows,
-                  const ff_i32* __restrict__ witem_class, const ff_i32* __restrict__ witem_steps,
-                  const ff_i64* __restrict__ witem_rec, const ff_i64* __restrict__ witem_goff,
-                  const unsigned short* __restrict__ wrec16, const unsigned char* __restrict__ gslot,
-                  const ff_i64* __restrict__ row_ptr, double* __restrict__ values, double* __restrict__ rhs,
-                  FfStatus* __restrict__ status) {
-  extern __shared__ __align__(16) double ff_es[];
-  __shared__ double stage[FF_WWARPS][32 * FF_SP];
-  __shared__ ff_i64 srow[FF_WWARPS][32];
-  __shared__ int next_item;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) next_item = win_iptr[blockIdx.x] + FF_WWARPS;
-  const ff_i64 eb = win_eptr[blockIdx.x];
-  const int nwe = (int)(win_eptr[blockIdx.x + 1] - eb);
-  // ---- phase 1: element records of the window (halo elements included)
-  for (int b0 = 0; b0 < nwe; b0 += 4 * FF_WWARPS * 32) {
-    ff_i64 vid[4][FF_NV];
-    ff_i64 el[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int le = b0 + u * FF_WWARPS * 32 + threadIdx.x;
-      el[u] = le < nwe ? (ff_i64)__ldg(win_elem + eb + le) : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int a = 0; a < FF_NV; ++a) {
-        const ff_i64 e = el[u] >= 0 ? el[u] : 0;
-#if FF_DEGREE > 1
-        vid[u][a] = __ldg(vconn + e * FF_NV + a);
-#else
-        vid[u][a] = __ldg(dconn + e * FF_NLOC + a);
-#endif
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (el[u] < 0) continue;
-      double out[FF_EREC];
-#pragma unroll
-      for (int q = 0; q < FF_EREC; ++q) out[q] = 0.0;
-      FfGeom geo;
-      if (ff_geometry(coords, vid[u], geo)) {
-        FfInvEmit emit{out};
-        ff_element(geo, emit);
-      } else {
-        atomicMin(&status->bad_elem, (ff_u64)el[u]);
-      }
-      double* dst = ff_es + (b0 + u * FF_WWARPS * 32 + threadIdx.x) * FF_ES;
-#pragma unroll
-      for (int q = 0; q < FF_EREC; ++q) dst[q] = out[q];
-    }
-  }
-  __syncthreads();
-  // ---- phase 2: the window's items, one warp per item
-  double* st = stage[wid];
-  ff_i64* sr = srow[wid];
-  // items are taken dynamically (their costs differ by class)
-  const int it_end = win_iptr[blockIdx.x + 1];
-  for (int it = win_iptr[blockIdx.x] + wid; it < it_end;) {
-    const int c = __ldg(witem_class + it);
-    const int row = __ldg(witem_rows + (ff_i64)it * 32 + lane);
-    ff_i64 rbeg = 0;
-    int len = 0;
-    if (row >= 0) {
-      rbeg = __ldg(row_ptr + row);
-      len = (int)(__ldg(row_ptr + row + 1) - rbeg);
-    }
-    const unsigned short* rec = wrec16 + __ldg(witem_rec + it) * 32 + lane;
-    switch (c) {
-)";
-  for (int c = 0; c < static_cast<int>(classes.size()); ++c)
-    os << "      case " << c << ": ff_wcls_" << c << "(rec, ff_es, st, sr, lane, rbeg, row, values, rhs); break;\n";
-  os << R"(      default:
-        ff_wgen(rec, gslot + (__ldg(witem_goff + it) * 32 + lane) * FF_NLOC, witem_steps + (ff_i64)it * FF_NLOC, ff_es,
-                lane, rbeg, len, row, values, rhs);
-        break;
-    }
-    int nx = 0;
-    if (lane == 0) nx = atomicAdd(&next_item, 1);
-    it = __shfl_sync(0xffffffffu, nx, 0);
-  }
-}
-)";
   return os.str();
 }
 

@@ -115,7 +115,6 @@ ElementPlan plan_element(const fem::InstantiatedForm& f, const fem::QuadratureRu
 enum class Scatter : int {
   Auto = 0,
   Atomic = 1,     // element-parallel, fp64 RED into CSR slots (K0 zero-fill first)
-  RowTiles = 2,   // row-tile ownership: atomic-free, each CSR slot written once
   Gather = 3,     // row per lane: element invariants + lock-step row gather
 };
 
@@ -132,17 +131,6 @@ struct LaunchParams {
 };
 
 int default_quad_rule(int dim, int degree);
-
-// Shared-memory geometry of the row-tile kernel for n_local DOFs per element
-// (the template and the host plan builder must agree on these numbers).
-struct RowTileParams {
-  int acc = 6144;    // max CSR slots per tile (fp64 accumulators)
-  int rows = 256;    // max rows per tile
-  int stage = 384;   // max staged element rows per chunk
-  int chunk = 256;   // max element visits per chunk (= block size)
-  int smem_bytes(int n_local, int slot_bytes) const;
-};
-RowTileParams rowtile_params(int n_local, int block_size);
 
 // Renders the complete NVRTC translation unit (template + element body).
 // Byte-deterministic for identical inputs; throws CodegenError on bad params.
@@ -178,11 +166,6 @@ inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, 
 // plan (plan.n_kinv > 0). Byte-deterministic.
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes,
                               bool fused = false, int bs = 1);
-
-// The window row-gather kernel (ff_gather_windows) appended to the form's own
-// translation unit (it reuses the form's geometry and element body).
-std::string emit_window_source(const std::string& form_source, const ElementPlan& plan, int n_local,
-                               const std::vector<RowClass>& classes);
 
 // Shortest round-trip double literal valid in C/CUDA source.
 std::string double_literal(double v);

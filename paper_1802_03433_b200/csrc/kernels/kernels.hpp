@@ -19,15 +19,6 @@ cudaError_t build_slots(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, i
                         const int32_t* col_idx, int slot_bytes, void* d_slots, unsigned long long* d_bad_row,
                         int sm_count, cudaStream_t s);
 
-// Row-tile plan: tiles are row ranges [tile_row[t], tile_row[t+1]) (local rows,
-// device array of n_tiles+1). Produces the element visits of every tile
-// (elements with >= 1 DOF in the tile, ascending), and per visit its staging
-// offset inside its chunk with bit 15 set on chunk starts.
-cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
-                               const int64_t* d_tile_row, int64_t n_tiles, int stage_cap, int chunk_cap, int sm_count,
-                               cudaStream_t s, int64_t** tile_vptr, int32_t** visit_elem, uint16_t** visit_stage,
-                               int64_t* n_visits);
-
 // Row-gather plan (one CSR row per lane, 32 rows per warp item, lock-step
 // records [step][32] of (element id, k slot bytes); see pattern.cu).
 struct GatherPlan {
@@ -61,29 +52,13 @@ struct GatherPlan {
   // eorder[t]; records (rec, crec) hold erank[e]
   int32_t* eorder = nullptr;
   int32_t* erank = nullptr;
-  // Window plan: windows of win_rows consecutive rows (Morton order); the
-  // window kernel computes the window's elements (win_elem) into shared
-  // memory and gathers its items from there. n_win == 0: no window plan.
-  int64_t n_win = 0, win_max_elems = 0, n_witems = 0, n_wsteps = 0, n_gsteps = 0;
-  int win_rows = 0;
-  int64_t* win_eptr = nullptr;       // [n_win + 1]
-  int32_t* win_elem = nullptr;       // [.] element ids, ascending per window
-  int32_t* win_iptr = nullptr;       // [n_win + 1] items of each window
-  int32_t* witem_rows = nullptr;     // [n_witems][32]
-  int32_t* witem_class = nullptr;    // [n_witems] row class, -1: generic
-  int32_t* witem_win = nullptr;      // [n_witems]
-  int32_t* witem_steps = nullptr;    // [n_witems][k] lock-step records per local index
-  int64_t* witem_rec = nullptr;      // [n_witems + 1] first step
-  int64_t* witem_goff = nullptr;     // [n_witems] first slot-byte step (generic items), -1
-  uint16_t* wrec16 = nullptr;        // [n_wsteps][32] window-local element, 0xffff: idle
-  uint8_t* gslot = nullptr;          // [n_gsteps][32][k] slot bytes of generic items
 };
 // bbox: {min x, min y, min z, max x, max y, max z} of the mesh coordinates.
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64,
-                              bool use_eorder = true, int max_win_elems = 0, bool split_long = true);
+                              bool use_eorder = true, bool split_long = true);
 void free_gather_plan(GatherPlan* p);
 
 // fem::Mesh::validate (fem.cpp:17-34) on the device: *d_bad = the lowest

@@ -134,77 +134,6 @@ __global__ void zero_kernel(double* __restrict__ a, int64_t na, double* __restri
 }
 
 
-// ---- row-tile plan ---------------------------------------------------------
-
-__global__ void row_tile_map(const int64_t* __restrict__ tile_row, int64_t n_tiles, int64_t n_rows,
-                             int32_t* __restrict__ row_tile) {
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t lo = 0, hi = n_tiles;  // last t with tile_row[t] <= r
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (tile_row[mid] <= r)
-        lo = mid;
-      else
-        hi = mid;
-    }
-    row_tile[r] = static_cast<int32_t>(lo);
-  }
-}
-
-__global__ void visit_keys(const int32_t* __restrict__ dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
-                           const int32_t* __restrict__ row_tile, int64_t n_tiles, uint64_t* __restrict__ keys) {
-  const uint64_t invalid = static_cast<uint64_t>(n_tiles) << 32;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ne * k;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t e = t / k;
-    const int64_t row = static_cast<int64_t>(dconn[t]) - rb;
-    keys[t] = (row >= 0 && row < n_rows) ? (static_cast<uint64_t>(row_tile[row]) << 32) | static_cast<uint32_t>(e)
-                                         : invalid;
-  }
-}
-
-__global__ void split_visits(const uint64_t* __restrict__ keys, const int64_t* __restrict__ n_unique, int64_t n_tiles,
-                             int64_t* __restrict__ tile_vptr, int32_t* __restrict__ visit_elem) {
-  const int64_t n = *n_unique;
-  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
-       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t tile = static_cast<int64_t>(keys[v] >> 32);
-    if (tile >= n_tiles) continue;
-    visit_elem[v] = static_cast<int32_t>(keys[v] & 0xffffffffu);
-    const int64_t prev = v == 0 ? -1 : static_cast<int64_t>(keys[v - 1] >> 32);
-    for (int64_t t = prev + 1; t <= tile; ++t) tile_vptr[t] = v;
-    if (v == n - 1 || static_cast<int64_t>(keys[v + 1] >> 32) >= n_tiles)
-      for (int64_t t = tile + 1; t <= n_tiles; ++t) tile_vptr[t] = v + 1;
-  }
-}
-
-// one thread per tile: staging offsets and chunk starts (bit 15)
-__global__ void chunk_visits(const int32_t* __restrict__ dconn, int k, int64_t rb, const int64_t* __restrict__ tile_row,
-                             const int64_t* __restrict__ tile_vptr, const int32_t* __restrict__ visit_elem,
-                             int64_t n_tiles, int stage_cap, int chunk_cap, uint16_t* __restrict__ visit_stage) {
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_tiles;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t lo = rb + tile_row[t], hi = rb + tile_row[t + 1];
-    int stage = 0, count = 0;
-    for (int64_t v = tile_vptr[t]; v < tile_vptr[t + 1]; ++v) {
-      const int32_t* d = dconn + static_cast<int64_t>(visit_elem[v]) * k;
-      int own = 0;
-      for (int a = 0; a < k; ++a) own += d[a] >= lo && d[a] < hi;
-      bool start = count == 0;
-      if (count == chunk_cap || stage + own > stage_cap) {
-        stage = 0;
-        count = 0;
-        start = true;
-      }
-      visit_stage[v] = static_cast<uint16_t>(stage | (start ? 0x8000 : 0));
-      stage += own;
-      ++count;
-    }
-  }
-}
-
-
 // ---- row-gather plan ---------------------------------------------------------
 //
 // The row-gather kernel (assemble_template.inc: ff_gather_rows) gives every
@@ -541,110 +470,6 @@ __global__ void remap_ranks(int32_t* __restrict__ crec, int64_t n, const int32_t
   }
 }
 
-// ---- window plan (row windows with their element data in shared memory) ----
-
-// (window << 32 | element) of every owned incidence
-__global__ void win_keys(const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc, int64_t n_rows, int k,
-                         const int32_t* __restrict__ rwin, uint64_t* __restrict__ keys) {
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t w = static_cast<uint64_t>(rwin[r]) << 32;
-    for (int64_t p = inc_ptr[r]; p < inc_ptr[r + 1]; ++p) keys[p] = w | static_cast<uint32_t>(inc[p] / k);
-  }
-}
-
-// unique sorted (window, element) keys -> win_eptr (window starts) + win_elem
-__global__ void win_split(const uint64_t* __restrict__ keys, const int64_t* __restrict__ n_unique, int64_t n_win,
-                          int64_t* __restrict__ win_eptr, int32_t* __restrict__ win_elem) {
-  const int64_t n = *n_unique;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t w = static_cast<int64_t>(keys[t] >> 32);
-    win_elem[t] = static_cast<int32_t>(keys[t] & 0xffffffffu);
-    const int64_t prev = t == 0 ? -1 : static_cast<int64_t>(keys[t - 1] >> 32);
-    for (int64_t q = prev + 1; q <= w; ++q) win_eptr[q] = t;
-    if (t == n - 1)
-      for (int64_t q = w + 1; q <= n_win; ++q) win_eptr[q] = n;
-  }
-}
-
-// per item: lock-step record count per local index (max over its lanes)
-__global__ void witem_steps(const int32_t* __restrict__ wrows, int64_t n_items, int k,
-                            const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
-                            int32_t* __restrict__ steps, int64_t* __restrict__ total) {
-  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < n_items;
-       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int mx[32];
-    for (int i = 0; i < k; ++i) mx[i] = 0;
-    for (int l = 0; l < 32; ++l) {
-      const int32_t row = wrows[w * 32 + l];
-      if (row < 0) continue;
-      int64_t p = inc_ptr[row];
-      const int64_t e = inc_ptr[row + 1];
-      for (int i = 0; i < k; ++i) {
-        int c = 0;
-        while (p < e && inc[p] % k == i) {
-          ++c;
-          ++p;
-        }
-        mx[i] = max(mx[i], c);
-      }
-    }
-    int64_t t = 0;
-    for (int i = 0; i < k; ++i) {
-      steps[w * k + i] = mx[i];
-      t += mx[i];
-    }
-    total[w] = t;
-  }
-}
-
-// records: u16 window-local element index per (step, lane) (0xffff: idle);
-// generic items also get the k slot bytes per (step, lane)
-__global__ void witem_fill(const int32_t* __restrict__ wrows, const int32_t* __restrict__ wwin,
-                           const int32_t* __restrict__ steps, const int64_t* __restrict__ rec_off,
-                           const int64_t* __restrict__ goff, int64_t n_items, int k, const int64_t* __restrict__ inc_ptr,
-                           const int32_t* __restrict__ inc, const uint8_t* __restrict__ slots,
-                           const int64_t* __restrict__ win_eptr, const int32_t* __restrict__ win_elem,
-                           uint16_t* __restrict__ rec16, uint8_t* __restrict__ gslot) {
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_items * 32;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t w = t / 32;
-    const int lane = static_cast<int>(t % 32);
-    const int32_t row = wrows[t];
-    const int64_t wb = win_eptr[wwin[w]], we = win_eptr[wwin[w] + 1];
-    int64_t p = row >= 0 ? inc_ptr[row] : 0;
-    const int64_t pe = row >= 0 ? inc_ptr[row + 1] : 0;
-    int64_t st = rec_off[w];
-    const int64_t g0 = goff[w];
-    int64_t gs = 0;
-    for (int i = 0; i < k; ++i) {
-      const int n = steps[w * k + i];
-      for (int q = 0; q < n; ++q, ++st, ++gs) {
-        uint16_t le = 0xffff;
-        const uint8_t* sl = nullptr;
-        if (p < pe && inc[p] % k == i) {
-          const int32_t x = inc[p++];
-          const int32_t e = x / k;
-          int64_t lo = wb, hi = we;
-          while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (win_elem[mid] < e)
-              lo = mid + 1;
-            else
-              hi = mid;
-          }
-          le = static_cast<uint16_t>(lo - wb);
-          sl = slots + static_cast<int64_t>(x) * k;
-        }
-        rec16[st * 32 + lane] = le;
-        if (g0 >= 0)
-          for (int j = 0; j < k; ++j) gslot[((g0 + gs) * 32 + lane) * k + j] = sl ? sl[j] : 0;
-      }
-    }
-  }
-}
-
 template <int K>
 __global__ void fill_records(const int32_t* __restrict__ erank, const int32_t* __restrict__ warp_rows,
                              const int32_t* __restrict__ warp_steps,
@@ -765,63 +590,11 @@ cudaError_t build_pattern(const int32_t* d_dconn, int64_t ne, int k, int64_t rb,
 }
 
 
-cudaError_t build_rowtile_plan(const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
-                               const int64_t* d_tile_row, int64_t n_tiles, int stage_cap, int chunk_cap, int sm_count,
-                               cudaStream_t s, int64_t** tile_vptr, int32_t** visit_elem, uint16_t** visit_stage,
-                               int64_t* n_visits) {
-  const int cap = sm_count * 16;
-  const int64_t n_keys = ne * k;
-  int32_t* row_tile = nullptr;
-  uint64_t *keys = nullptr, *sorted = nullptr;
-  int64_t* d_count = nullptr;
-  void* temp = nullptr;
-  cudaError_t err = cudaSuccess;
-  auto done = [&](cudaError_t e) {
-    cudaFree(row_tile);
-    cudaFree(keys);
-    cudaFree(sorted);
-    cudaFree(d_count);
-    cudaFree(temp);
-    return e;
-  };
-  if ((err = cudaMalloc(&row_tile, (n_rows > 0 ? n_rows : 1) * sizeof(int32_t))) != cudaSuccess) return done(err);
-  if ((err = cudaMalloc(&keys, (n_keys > 0 ? n_keys : 1) * sizeof(uint64_t))) != cudaSuccess) return done(err);
-  if ((err = cudaMalloc(&sorted, (n_keys > 0 ? n_keys : 1) * sizeof(uint64_t))) != cudaSuccess) return done(err);
-  if ((err = cudaMalloc(&d_count, sizeof(int64_t))) != cudaSuccess) return done(err);
-  row_tile_map<<<grid_for(n_rows, cap), kThreads, 0, s>>>(d_tile_row, n_tiles, n_rows, row_tile);
-  visit_keys<<<grid_for(n_keys, cap), kThreads, 0, s>>>(d_dconn, ne, k, rb, n_rows, row_tile, n_tiles, keys);
-  int end_bit = 32;
-  while ((static_cast<int64_t>(1) << (end_bit - 32)) <= n_tiles) ++end_bit;
-  size_t t_sort = 0, t_uniq = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, t_sort, keys, sorted, n_keys, 0, end_bit, s);
-  cub::DeviceSelect::Unique(nullptr, t_uniq, sorted, keys, d_count, n_keys, s);
-  if ((err = cudaMalloc(&temp, t_sort > t_uniq ? t_sort : t_uniq)) != cudaSuccess) return done(err);
-  if ((err = cub::DeviceRadixSort::SortKeys(temp, t_sort, keys, sorted, n_keys, 0, end_bit, s)) != cudaSuccess)
-    return done(err);
-  if ((err = cub::DeviceSelect::Unique(temp, t_uniq, sorted, keys, d_count, n_keys, s)) != cudaSuccess) return done(err);
-  int64_t n_unique = 0;
-  cudaMemcpyAsync(&n_unique, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-  if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
-  if ((err = cudaMalloc(tile_vptr, (n_tiles + 1) * sizeof(int64_t))) != cudaSuccess) return done(err);
-  if ((err = cudaMalloc(visit_elem, (n_unique > 0 ? n_unique : 1) * sizeof(int32_t))) != cudaSuccess) return done(err);
-  if ((err = cudaMalloc(visit_stage, (n_unique > 0 ? n_unique : 1) * sizeof(uint16_t))) != cudaSuccess) return done(err);
-  cudaMemsetAsync(*tile_vptr, 0, (n_tiles + 1) * sizeof(int64_t), s);
-  split_visits<<<grid_for(n_unique, cap), kThreads, 0, s>>>(keys, d_count, n_tiles, *tile_vptr, *visit_elem);
-  chunk_visits<<<grid_for(n_tiles, cap), 64, 0, s>>>(d_dconn, k, rb, d_tile_row, *tile_vptr, *visit_elem, n_tiles,
-                                                     stage_cap, chunk_cap, *visit_stage);
-  int64_t last_key = 0;
-  if (n_unique > 0) cudaMemcpyAsync(&last_key, keys + (n_unique - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-  if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
-  *n_visits = n_unique - ((static_cast<uint64_t>(last_key) >> 32) >= static_cast<uint64_t>(n_tiles) ? 1 : 0);
-  return done(cudaGetLastError());
-}
-
-
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes,
-                              bool use_eorder, int max_win_elems, bool split_long) {
+                              bool use_eorder, bool split_long) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   // FF_PLAN_TIMING=1: phase times of the plan build on stderr
@@ -1265,156 +1038,6 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
   if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return done(err);
 
   phase("generic items");
-  // ---- window plan: windows of W consecutive rows in Morton order; their
-  // elements (halo included) are computed into shared memory by the window
-  // kernel, which then gathers the window's rows (class items with
-  // compile-time slots, generic items with slot bytes)
-  if (max_win_elems > 0 && n_rows > 0) {
-    std::vector<int32_t> rank(n_rows);
-    for (int64_t pos = 0; pos < n_rows; ++pos) rank[morton[pos]] = static_cast<int32_t>(pos);
-    int32_t* rwin = nullptr;
-    uint64_t *wk = nullptr, *wk2 = nullptr;
-    int64_t* d_cnt = nullptr;
-    auto wdone = [&](cudaError_t e) {
-      cudaFree(rwin);
-      cudaFree(wk);
-      cudaFree(wk2);
-      cudaFree(d_cnt);
-      return done(e);
-    };
-    if ((err = cudaMalloc(&rwin, n_rows * sizeof(int32_t))) != cudaSuccess) return wdone(err);
-    if ((err = cudaMalloc(&wk, std::max<int64_t>(n_inc, 1) * sizeof(uint64_t))) != cudaSuccess) return wdone(err);
-    if ((err = cudaMalloc(&wk2, std::max<int64_t>(n_inc, 1) * sizeof(uint64_t))) != cudaSuccess) return wdone(err);
-    if ((err = cudaMalloc(&d_cnt, sizeof(int64_t))) != cudaSuccess) return wdone(err);
-    int W = 256;
-    int64_t n_win = 0, n_we = 0;
-    std::vector<int64_t> eptr;
-    for (;;) {
-      n_win = (n_rows + W - 1) / W;
-      std::vector<int32_t> rw(n_rows);
-      for (int64_t r = 0; r < n_rows; ++r) rw[r] = rank[r] / W;
-      cudaMemcpyAsync(rwin, rw.data(), n_rows * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-      win_keys<<<grid_for(n_rows, cap), kThreads, 0, s>>>(inc_ptr, inc, n_rows, k, rwin, wk);
-      int end_bit = 32;
-      while ((static_cast<int64_t>(1) << (end_bit - 32)) <= n_win) ++end_bit;
-      size_t t1 = 0, t2 = 0;
-      cub::DeviceRadixSort::SortKeys(nullptr, t1, wk, wk2, n_inc, 0, end_bit, s);
-      cub::DeviceSelect::Unique(nullptr, t2, wk2, wk, d_cnt, n_inc, s);
-      if ((err = need_temp(std::max(t1, t2))) != cudaSuccess) return wdone(err);
-      if ((err = cub::DeviceRadixSort::SortKeys(temp, t1, wk, wk2, n_inc, 0, end_bit, s)) != cudaSuccess) return wdone(err);
-      if ((err = cub::DeviceSelect::Unique(temp, t2, wk2, wk, d_cnt, n_inc, s)) != cudaSuccess) return wdone(err);
-      cudaMemcpyAsync(&n_we, d_cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-      if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return wdone(err);
-      cudaFree(out->win_eptr);
-      cudaFree(out->win_elem);
-      out->win_eptr = nullptr;
-      out->win_elem = nullptr;
-      if ((err = cudaMalloc(&out->win_eptr, (n_win + 1) * sizeof(int64_t))) != cudaSuccess) return wdone(err);
-      if ((err = cudaMalloc(&out->win_elem, std::max<int64_t>(n_we, 1) * sizeof(int32_t))) != cudaSuccess)
-        return wdone(err);
-      win_split<<<grid_for(n_we, cap), kThreads, 0, s>>>(wk, d_cnt, n_win, out->win_eptr, out->win_elem);
-      eptr.resize(n_win + 1);
-      cudaMemcpyAsync(eptr.data(), out->win_eptr, (n_win + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-      if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return wdone(err);
-      int64_t mx = 0;
-      for (int64_t w = 0; w < n_win; ++w) mx = std::max(mx, eptr[w + 1] - eptr[w]);
-      out->win_max_elems = mx;
-      if (mx <= max_win_elems || W <= 32) break;
-      W /= 2;
-    }
-    out->win_rows = W;
-    out->n_win = n_win;
-    if (out->win_max_elems <= max_win_elems && out->win_max_elems < 65535) {
-      // items: per window, each class's rows (Morton order) in chunks of 32,
-      // then the generic rows in chunks of 32
-      const int n_cls = static_cast<int>(out->classes.size());
-      std::vector<int32_t> ir, ic, iw, wip(n_win + 1, 0);
-      std::vector<std::vector<int32_t>> bucket(n_cls + 1);
-      for (int64_t w = 0; w < n_win; ++w) {
-        for (auto& b : bucket) b.clear();
-        for (int64_t pos = w * W; pos < std::min<int64_t>(n_rows, (w + 1) * W); ++pos) {
-          const int32_t r = morton[pos];
-          bucket[cls_h[r] >= 0 ? cls_h[r] : n_cls].push_back(r);
-        }
-        for (int c = 0; c <= n_cls; ++c)
-          for (size_t q = 0; q < bucket[c].size(); q += 32) {
-            for (size_t l = 0; l < 32; ++l) ir.push_back(q + l < bucket[c].size() ? bucket[c][q + l] : -1);
-            ic.push_back(c < n_cls ? c : -1);
-            iw.push_back(static_cast<int32_t>(w));
-          }
-        wip[w + 1] = static_cast<int32_t>(ic.size());
-      }
-      const int64_t ni = static_cast<int64_t>(ic.size());
-      out->n_witems = ni;
-      int32_t* d_steps = nullptr;
-      int64_t *d_tot = nullptr, *d_goff = nullptr;
-      auto idone = [&](cudaError_t e) {
-        cudaFree(d_steps);
-        cudaFree(d_tot);
-        cudaFree(d_goff);
-        return wdone(e);
-      };
-      if ((err = cudaMalloc(&out->win_iptr, (n_win + 1) * sizeof(int32_t))) != cudaSuccess) return idone(err);
-      if ((err = cudaMalloc(&out->witem_rows, std::max<int64_t>(ni, 1) * 32 * sizeof(int32_t))) != cudaSuccess)
-        return idone(err);
-      if ((err = cudaMalloc(&out->witem_class, std::max<int64_t>(ni, 1) * sizeof(int32_t))) != cudaSuccess)
-        return idone(err);
-      if ((err = cudaMalloc(&out->witem_win, std::max<int64_t>(ni, 1) * sizeof(int32_t))) != cudaSuccess)
-        return idone(err);
-      if ((err = cudaMalloc(&out->witem_steps, std::max<int64_t>(ni, 1) * k * sizeof(int32_t))) != cudaSuccess)
-        return idone(err);
-      if ((err = cudaMalloc(&out->witem_rec, (ni + 1) * sizeof(int64_t))) != cudaSuccess) return idone(err);
-      if ((err = cudaMalloc(&out->witem_goff, std::max<int64_t>(ni, 1) * sizeof(int64_t))) != cudaSuccess)
-        return idone(err);
-      if ((err = cudaMalloc(&d_tot, (ni + 1) * sizeof(int64_t))) != cudaSuccess) return idone(err);
-      cudaMemcpyAsync(out->win_iptr, wip.data(), (n_win + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-      if (ni > 0) {
-        cudaMemcpyAsync(out->witem_rows, ir.data(), ni * 32 * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(out->witem_class, ic.data(), ni * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(out->witem_win, iw.data(), ni * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-      }
-      cudaMemsetAsync(d_tot, 0, (ni + 1) * sizeof(int64_t), s);
-      if (ni > 0)
-        witem_steps<<<grid_for(ni, cap), kThreads, 0, s>>>(out->witem_rows, ni, k, inc_ptr, inc, out->witem_steps, d_tot);
-      std::vector<int64_t> tot(ni + 1, 0), roff(ni + 1, 0), goff(std::max<int64_t>(ni, 1), -1);
-      if (ni > 0) cudaMemcpyAsync(tot.data(), d_tot, ni * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-      if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return idone(err);
-      int64_t gtot = 0;
-      for (int64_t w = 0; w < ni; ++w) {
-        roff[w + 1] = roff[w] + tot[w];
-        if (ic[w] < 0) {
-          goff[w] = gtot;
-          gtot += tot[w];
-        }
-      }
-      out->n_wsteps = roff[ni];
-      out->n_gsteps = gtot;
-      if ((err = cudaMalloc(&out->wrec16, std::max<int64_t>(roff[ni], 1) * 32 * sizeof(uint16_t))) != cudaSuccess)
-        return idone(err);
-      if ((err = cudaMalloc(&out->gslot, std::max<int64_t>(gtot, 1) * 32 * k)) != cudaSuccess) return idone(err);
-      cudaMemcpyAsync(out->witem_rec, roff.data(), (ni + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
-      if (ni > 0) {
-        cudaMemcpyAsync(out->witem_goff, goff.data(), ni * sizeof(int64_t), cudaMemcpyHostToDevice, s);
-        witem_fill<<<grid_for(ni * 32, cap), kThreads, 0, s>>>(out->witem_rows, out->witem_win, out->witem_steps,
-                                                               out->witem_rec, out->witem_goff, ni, k, inc_ptr, inc,
-                                                               d_slots, out->win_eptr, out->win_elem, out->wrec16,
-                                                               out->gslot);
-      }
-      if ((err = cudaStreamSynchronize(s)) != cudaSuccess) return idone(err);
-      cudaFree(d_steps);
-      cudaFree(d_tot);
-      cudaFree(d_goff);
-      d_steps = nullptr;
-      d_tot = nullptr;
-      d_goff = nullptr;
-    } else {
-      out->n_win = 0;  // element sets too large for shared memory: no window plan
-    }
-    cudaFree(rwin);
-    cudaFree(wk);
-    cudaFree(wk2);
-    cudaFree(d_cnt);
-  }
   return done(cudaGetLastError());
 }
 
@@ -1447,17 +1070,6 @@ cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_ou
 }
 
 void free_gather_plan(GatherPlan* p) {
-  cudaFree(p->win_eptr);
-  cudaFree(p->win_elem);
-  cudaFree(p->win_iptr);
-  cudaFree(p->witem_rows);
-  cudaFree(p->witem_class);
-  cudaFree(p->witem_win);
-  cudaFree(p->witem_steps);
-  cudaFree(p->witem_rec);
-  cudaFree(p->witem_goff);
-  cudaFree(p->wrec16);
-  cudaFree(p->gslot);
   cudaFree(p->eorder);
   cudaFree(p->erank);
   cudaFree(p->citem_class);

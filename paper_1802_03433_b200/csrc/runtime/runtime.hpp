@@ -64,9 +64,6 @@ struct ff_form {
   ffb::CompiledModule module[3];
   cudaLibrary_t lib[3] = {nullptr, nullptr, nullptr};
   cudaKernel_t kernel[3] = {nullptr, nullptr, nullptr};          // ff_assemble_atomic
-  cudaKernel_t kernel_tile[3] = {nullptr, nullptr, nullptr};     // ff_assemble_rowtile
-  femforge::codegen::RowTileParams tile;
-  int tile_smem[3] = {0, 0, 0};
   cudaKernel_t kernel_ginv[3] = {nullptr, nullptr, nullptr};     // ff_gather_invariants
   cudaKernel_t kernel_grows[3] = {nullptr, nullptr, nullptr};    // ff_gather_rows
 };
@@ -102,14 +99,6 @@ struct ff_pattern {
   std::uint64_t plan_generation = ~0ull;
   void* slots = nullptr;
   int slot_bytes = 1;
-  // row-tile plan (atomic-free scatter) for plan_mesh
-  std::uint64_t tile_generation = ~0ull;
-  int64_t n_tiles = 0, n_visits = 0;
-  int64_t* tile_row = nullptr;     // [n_tiles + 1] local rows
-  int64_t* tile_vptr = nullptr;    // [n_tiles + 1]
-  int32_t* visit_elem = nullptr;   // [n_visits]
-  uint16_t* visit_stage = nullptr; // [n_visits]
-  int tile_acc = 0, tile_rows = 0, tile_stage = 0, tile_chunk = 0;
   // row-gather plan for plan_mesh, and the per-element invariant buffers
   std::uint64_t gather_generation = ~0ull;
   // CUDA graph of the last device assembly (ff_assemble_device replays it when
@@ -125,10 +114,6 @@ struct ff_pattern {
   cudaLibrary_t class_lib = nullptr;
   cudaKernel_t class_kernel[2] = {nullptr, nullptr};  // short rows, long rows
   int class_smem[2] = {0, 0};                           // their dynamic shared memory
-  // window row-gather kernel for (form source, plan)
-  std::string window_key;
-  cudaLibrary_t window_lib = nullptr;
-  cudaKernel_t window_kernel = nullptr;
   double class_compile_ms = 0.0;
   double* ginv = nullptr;   // [ne][nkp]
   double* bvec = nullptr;   // [ne][k]

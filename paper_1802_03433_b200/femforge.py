@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libfemforge_b200.so")
 FF_OK, FF_E_ARG, FF_E_DEGENERATE, FF_E_PATTERN, FF_E_NVRTC, FF_E_CUDA, FF_E_FORM, FF_E_MESH, FF_E_SYMBOLIC, FF_E_NOMEM = \
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9
 STRATEGY = {"auto": 0, "tensor": 1, "pointwise": 2}
-SCATTER_MODE = {"rowtile": 0, "atomic": 1, "gather": 2}
+SCATTER_MODE = {"atomic": 1, "gather": 2}
 SCATTER_NAME = {v: k for k, v in SCATTER_MODE.items()}
 
 
@@ -74,8 +74,7 @@ class FormInfo(C.Structure):
 class GatherInfo(C.Structure):
     _fields_ = [("n_items", C.c_int64), ("n_steps", C.c_int64), ("n_incidences", C.c_int64),
                 ("record_bytes", C.c_int), ("build_ms", C.c_double), ("n_classes", C.c_int),
-                ("n_class_rows", C.c_int64), ("n_class_items", C.c_int64), ("n_windows", C.c_int64),
-                ("window_rows", C.c_int), ("window_max_elems", C.c_int64), ("n_window_items", C.c_int64),
+                ("n_class_rows", C.c_int64), ("n_class_items", C.c_int64),
                 ("launches", C.c_int)]
 
     def as_dict(self):
@@ -110,7 +109,6 @@ SIGNATURES = [
     ("ff_class_source", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_expr_eval", C.c_int, [C.c_char_p, C.c_int, _P, _i64, _P]),
     ("ff_form_entry_text", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
-    ("ff_window_source", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("ff_form_create", C.c_int, [_P, C.POINTER(_FormDesc), C.POINTER(_P)]),
     ("ff_compile", C.c_int, [_P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P), C.c_char_p, C.c_size_t]),
     ("ff_form_create_blocked", C.c_int, [_P, C.POINTER(_FormDesc), C.c_int, C.POINTER(C.c_char_p),
@@ -198,8 +196,8 @@ class Context:
         _ok(lib().ff_ctx_synchronize(self.h))
 
     def set_scatter(self, mode):
-        """'gather' (row gather, atomic-free, default), 'rowtile' (CTA row tiles,
-        atomic-free) or 'atomic' (fp64 RED after a zero-fill)."""
+        """'gather' (row gather, atomic-free, default) or 'atomic' (fp64 RED
+        after a zero-fill)."""
         _ok(lib().ff_ctx_set_scatter(self.h, SCATTER_MODE[mode]))
         self.scatter = mode
 
@@ -279,16 +277,15 @@ class Form:
         _ok(lib().ff_form_info_get(self.h, C.byref(i)))
         return i.as_dict()
 
-    def class_source(self, classes, window=False):
-        """Specialised gather source for classes [(len, [local i], [[slot bytes]])]
-        (window=True: the window row-gather translation unit)."""
+    def class_source(self, classes):
+        """Specialised gather source for classes [(len, [local i], [[slot bytes]])]."""
         n = len(classes)
         ln = np.array([c[0] for c in classes], np.int32)
         st = np.array([len(c[1]) for c in classes], np.int32)
         lo = np.ascontiguousarray(np.concatenate([np.asarray(c[1], np.int32) for c in classes]) if n else np.zeros(1, np.int32))
         sl = np.ascontiguousarray(np.concatenate([np.asarray(c[2], np.uint8).ravel() for c in classes]) if n else np.zeros(1, np.uint8))
         m = C.c_size_t(0)
-        fn = lib().ff_window_source if window else lib().ff_class_source
+        fn = lib().ff_class_source
         _ok(fn(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), None, 0, C.byref(m)))
         buf = C.create_string_buffer(m.value + 1)
         _ok(fn(self.h, n, _ptr(ln), _ptr(st), _ptr(lo), _ptr(sl), buf, m.value + 1, C.byref(m)))
@@ -411,7 +408,7 @@ def assemble_device(form, mesh, pattern, values_ptr, rhs_ptr, stream=None):
                                  _stream(stream)))
 
 
-FF_SKIP_ZERO, FF_ZERO_ONLY, FF_SCATTER_ATOMIC, FF_SCATTER_TILES, FF_SCATTER_GATHER = 1, 2, 4, 8, 16
+FF_SKIP_ZERO, FF_ZERO_ONLY, FF_SCATTER_ATOMIC, FF_SCATTER_GATHER = 1, 2, 4, 16
 FF_GATHER_INVARIANTS_ONLY, FF_GATHER_ROWS_ONLY = 32, 64
 
 

@@ -168,22 +168,6 @@ def test_class_specialised_source_compiles(ff):
     assert g.cubin[:4] == b"\x7fELF"
 
 
-def test_window_source_compiles(ff):
-    """The window row-gather kernel (element records in shared memory, class
-    rows in registers, generic rows through slot bytes) compiles for sm_100a."""
-    import pyoracle as po
-    c, v = po.kuhn_mesh(4)
-    d, nd = po.p2_dofs_kuhn(4, v)
-    rp, ci = po.build_pattern(d, nd)
-    classes = _row_classes(d, nd, rp, ci, 8)
-    bil, lin = ff.named_form("poisson", 3)
-    f = ff.Form(None, 3, 2, bil, lin, quad_rule=4)
-    src = f.class_source(classes, window=True)
-    assert "ff_gather_windows" in src and "ff_assemble_atomic" in src
-    g = ff.Form.from_source(None, src, 3, 2)
-    assert g.cubin[:4] == b"\x7fELF"
-
-
 def test_blocked_elasticity_form_compiles(ff):
     """Vector P2 elasticity (3x3 blocks of scalar forms, 30 DOFs per element)
     through instantiate_blocked -> tensor plan -> NVRTC for sm_100a, with the

@@ -19,7 +19,7 @@ def _golden(pattern):
     return sorted(glob.glob(os.path.join(GOLDEN, pattern)))
 
 
-SCATTERS = ["gather", "rowtile", "atomic"]
+SCATTERS = ["gather", "atomic"]
 
 
 def gpu_system(ff, ctx, dim, deg, form, coords, vconn, dconn, n_dofs, quad=0, strategy="auto",
@@ -248,9 +248,6 @@ def test_row_blocks_concatenate_to_full_system(ff, ctx, parts, scatter):
 
 
 ATOMIC_FREE = [  # (scatter, dim, degree, n, form, quad)
-    ("rowtile", 3, 1, 20, "varcoef", 14),
-    ("rowtile", 3, 2, 12, "varcoef", 14),
-    ("rowtile", 2, 1, 128, "demo2d", 3),
     ("gather", 3, 1, 20, "helmholtz", 4),
     ("gather", 3, 2, 12, "poisson", 4),
     ("gather", 2, 1, 128, "demo2d", 3),
@@ -300,7 +297,6 @@ def test_gather_falls_back_to_atomic_for_pointwise_forms(ff, ctx):
     m = ff.Mesh(ctx, 3, c, v, d, nd)
     p = ff.Pattern(ctx, m)
     assert p.scatter_for(f) == "atomic"
-    assert p.scatter_for(f, ff.FF_SCATTER_TILES) == "rowtile"
 
 
 def test_gather_phases_compose(ff, ctx):
@@ -396,28 +392,6 @@ def test_class_specialised_gather_equals_generic(ff, ctx, dim, deg, n, form):
     assert normwise(v1, ov) <= TOL and normwise(b1, ob) <= TOL
 
 
-@pytest.mark.parametrize("dim,deg,n,form", [(3, 2, 8, "poisson"), (2, 1, 48, "demo2d")])
-def test_window_gather_matches_oracle(ff, ctx, dim, deg, n, form, monkeypatch):
-    """Opt-in window row gather (FF_WINDOWS=1: element records computed per
-    window in shared memory) against the oracle."""
-    monkeypatch.setenv("FF_WINDOWS", "1")
-    c, v, d, nd = _mesh(ff, dim, deg, n)
-    ctx.set_scatter("gather")
-    quad = 4 if dim == 3 else 3
-    b, l = ff.named_form(form, dim)
-    f = ff.Form(ctx, dim, deg, b, l, quad_rule=quad)
-    m = ff.Mesh(ctx, dim, c, v, None if deg == 1 else d, nd)
-    p = ff.Pattern(ctx, m)
-    ctx.set_gather_classes(16)
-    try:
-        gi = p.gather_info(m)
-        assert gi["n_windows"] > 0 and gi["n_window_items"] * 32 >= nd
-        val, rhs = ff.assemble(f, m, p)
-    finally:
-        ctx.set_gather_classes(128)
-    orp, oci = po.build_pattern(d, nd)
-    ov, ob = po.assemble(form, dim, deg, quad, c, v, d, orp, oci, workers=8)
-    assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
 
 
 def _elasticity_system(ff, ctx, n, row_begin=0, row_end=None, ids=None, lam="1", mu="1", force=("0", "0", "-1"),

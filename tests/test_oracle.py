@@ -166,3 +166,21 @@ def test_export_matches_reference_bytes(fmt, tmp_path):
     assert (tmp_path / "ours_b.mtx").read_bytes() == (tmp_path / "ref_b.mtx").read_bytes()
     if fmt == "matrix_market":
         assert (tmp_path / "ours.mtx").read_text().splitlines()[1] == f"25 25 {len(ci)}"
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="oracle/_ref not built")
+def test_reference_build_reproduces_its_golden_kernel_source():
+    """Pins the oracle/_ref build to the reference: its emit_source output for
+    the demo form hashes to the committed fixture, which is the hash of the
+    reference's own golden (proj/tests/data/demo_kernel.cu.golden,
+    test_codegen.cpp:199-206) when the reference tree is present."""
+    import hashlib
+    buf = po.C.create_string_buffer(1 << 20)
+    n = po.ref().ffref_emit_demo_source(buf, len(buf))
+    got = hashlib.sha256(buf.value[:n]).hexdigest()
+    with open(os.path.join(GOLDEN, "demo_kernel.cu.golden.sha256")) as f:
+        assert got == f.read().strip()
+    golden = "/root/reference/proj/tests/data/demo_kernel.cu.golden"
+    if os.path.exists(golden):
+        with open(golden, "rb") as f:
+            assert got == hashlib.sha256(f.read()).hexdigest()
