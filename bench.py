@@ -6,8 +6,8 @@ prebuilt pattern (the reference's criterion-9 protocol, acceptance.cpp:292-327)
 cube (12,582,912 tets, 16,974,593 DOFs, 484,609,025 nnz).
 
   python bench.py [--gpus N --steps K --warmup W] [--config ns|c1|c2|c3|c4]
-  torchrun --nproc-per-node N bench.py --gpus N ...   (weak scaling: one cell per GPU;
-                                                       --scaling strong: row blocks of one mesh)
+  torchrun --nproc-per-node N bench.py --gpus N ...   (strong scaling: row blocks of the one mesh;
+                                                       --scaling weak: one cell per GPU)
   python bench.py --impl reference ...                (reference CPU arm)
 
 One JSON line on rank 0. Multi-GPU: contiguous DOF row blocks, halo elements
@@ -62,6 +62,19 @@ def make_mesh(ff, cfg):
         coords, vconn = ff.kuhn_mesh(cfg["n"])
         dconn, n_dofs = (vconn, coords.shape[0]) if cfg["degree"] == 1 else ff.kuhn_p2_dofs(cfg["n"], vconn)
     return coords, vconn, dconn, n_dofs
+
+
+def workload_config(cfg, world, elements, dofs, nnz, weak=False):
+    """The `config` object of the JSON line: the workload only (mesh, form,
+    sizes, partitioning), identical in both arms; diagnostics go to `detail`."""
+    values_bytes = nnz * 8
+    return {"workload": cfg["workload"] + (f", stacked x{world} along the last axis (one cell per GPU)"
+                                           if weak else ""),
+            "n": cfg["n"], "elements": int(elements), "dofs": int(dofs), "nnz": int(nnz), "form": cfg["form"],
+            "quad_rule": cfg["quad"],
+            "parallelism": f"row-blocks x{world} (halo elements duplicated, no collective)",
+            "l2": "flushed (256 MiB write) between steps" if values_bytes < 2 * 126 * 2 ** 20 else
+                  f"inputs > L2 (CSR values {values_bytes / 1e9:.2f} GB)"}
 
 
 def measured_peaks():
@@ -154,71 +167,121 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 # reference CPU arm
 
-def cpu_reference_sample(cfg, target_s=2.0):
-    """Reference CPU assembly on the box's host cores (bounded sample).
+def host_info():
+    """always print nproc, the lscpu model, OMP_NUM_THREADS,
+    the compiler and flags with a CPU number."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    info = {"nproc": os.cpu_count(), "cpu_model": model, "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+    try:
+        import pyoracle as po
+        if po.ref_available():
+            info["reference_build"] = po.ref().ffref_build_info().decode()
+    except Exception:
+        pass
+    return info
 
-    oracle/_ref: the unmodified reference library (symbolic CAS + IR VM +
-    binary-search scatter + OpenMP/atomics, all host threads) driving a 3D
-    instantiation restated from fem.cpp:122-158 (2D configs run the reference
-    pipeline unchanged). Falls back to the C restatement (oracle/femoracle.c)
-    when the reference build is absent. Returns a callable step() and a
-    description."""
+
+def cpu_reference_sample(cfg, target_s=2.0):
+    """Reference CPU assembly on the box's host cores, ON THE CONFIGURED MESH.
+
+    oracle/_ref is the unmodified reference library (symbolic CAS + IR VM +
+    binary-search scatter + OpenMP atomics, all host threads):
+      2D P1 (C1): the reference pipeline unchanged -- build_sparsity, then
+        assemble_sparse(CompiledEvaluator) in parallel mode over the whole
+        512^2 mesh every step (criterion 9, acceptance.cpp:292-327).
+      3D scalar (C2/C3/C4/NS): the reference's CAS + IR VM through the 3D
+        restatement of instantiate/run_assembly_block (oracle/ref_harness.cpp)
+        over the full mesh and its full CSR (built once, outside the timer,
+        acceptance.cpp:295-296); each step is a bounded, strided sample of the
+        mesh's elements (every stride-th element, so the sample touches the
+        whole CSR like the full pass), sized to ~target_s.
+      Vector P2 (C5): no reference implementation; the C restatement on a
+        Kuhn 8^3 sample (same element type and form; not the same mesh).
+    Returns step() -> (elements, seconds), kind, workers, desc, same_mesh,
+    (elements, dofs, nnz) of the configured workload."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
 
     workers = os.cpu_count() or 1
-    n_s = (8 if cfg.get("ncomp", 1) > 1 else 24) if cfg["dim"] == 3 else 256   # sample mesh of the same element type
-    if cfg["dim"] == 2:
-        coords, vconn = po.unit_square_mesh(n_s)
-        dconn, nd = vconn, coords.shape[0]
-    else:
+    if cfg.get("ncomp", 1) > 1:
+        n_s = 8
         coords, vconn = po.kuhn_mesh(n_s)
-        dconn, nd = (vconn, coords.shape[0]) if cfg["degree"] == 1 else po.p2_dofs_kuhn(n_s, vconn)
-    E = vconn.shape[0]
-    if cfg.get("ncomp", 1) > 1:   # no reference implementation of vector forms: the C restatement
+        dconn, nd = po.p2_dofs_kuhn(n_s, vconn)
         rp, ci = po.build_pattern(dconn, nd)
         vrp, vci = po.block_pattern(rp, ci, cfg["ncomp"])
-        kind = "port"
+        E = vconn.shape[0]
 
-        def run(limit):
-            po.assemble_elasticity(cfg["dim"], cfg["degree"], cfg["quad"], coords, vconn[:limit], dconn[:limit],
-                                   vrp, vci)
-        workers = 1
-    elif po.ref_available() and not (cfg["dim"] == 2 and cfg["degree"] == 2):
-        h = po.RefHarness(cfg["dim"], cfg["degree"], coords, vconn, dconn, nd, cfg["form"], cfg["quad"])
-        kind = "reference"
+        def step():
+            t = time.perf_counter()
+            po.assemble_elasticity(cfg["dim"], cfg["degree"], cfg["quad"], coords, vconn, dconn, vrp, vci)
+            return E, time.perf_counter() - t
+        desc = (f"C restatement (oracle/femoracle.c, 1 thread): all {E} elements of a Kuhn {n_s}^3 vector P2 mesh "
+                f"(the reference has no vector forms; not the {cfg['n']}^3 mesh)")
+        n = cfg["n"]
+        nnz_node = 230 * n ** 3 + 138 * n ** 2 + 24 * n + 1   # SURVEY Appendix A (Kuhn P2)
+        sizes = (6 * n ** 3, (2 * n + 1) ** 3, cfg["ncomp"] ** 2 * nnz_node)
+        return step, "port", 1, desc, False, sizes
+    if not po.ref_available():
+        raise RuntimeError("oracle/_ref (the reference library) is not built")
+    n = cfg["n"]
+    if cfg["dim"] == 2:
+        if cfg["degree"] != 1:
+            raise RuntimeError("the reference implements 2D P1 only")
+        coords, vconn = po.unit_square_mesh(n)
+        h = po.RefHarness(2, 1, coords, vconn, vconn, coords.shape[0], cfg["form"], cfg["quad"])
+        E = vconn.shape[0]
 
-        def run(limit):
-            h.assemble(workers=workers, elem_limit=limit)
-    else:
-        rp, ci = po.build_pattern(dconn, nd)
-        kind = "port"
-
-        def run(limit):
-            po.assemble(cfg["form"], cfg["dim"], cfg["degree"], cfg["quad"], coords, vconn[:limit], dconn[:limit],
-                        rp, ci, workers=workers)
+        def step():
+            t = time.perf_counter()
+            h.assemble(workers=workers)
+            return E, time.perf_counter() - t
+        desc = (f"reference library (oracle/_ref): assemble_sparse(CompiledEvaluator), parallel mode, {workers} "
+                f"workers, the whole {n}^2 mesh ({E} elements) per step; build_sparsity outside the timer")
+        return step, "reference", workers, desc, True, (E, coords.shape[0], h.nnz)
+    coords, vconn = po.kuhn_mesh(n)
+    dconn, nd = (vconn, coords.shape[0]) if cfg["degree"] == 1 else po.p2_dofs_kuhn(n, vconn)
+    t = time.perf_counter()
+    rp, ci = po.build_pattern(dconn, nd)
+    pattern_s = time.perf_counter() - t
+    h = po.RefHarness(3, cfg["degree"], coords, vconn, dconn, nd, cfg["form"], cfg["quad"], pattern=(rp, ci))
+    E = vconn.shape[0]
+    values = np.zeros(h.nnz)
+    rhs = np.zeros(nd)
+    values[:] = 0.0   # touch every page outside the timer
+    rhs[:] = 0.0
     probe = min(E, 4 * workers * 64)
-    t0 = time.perf_counter()
-    run(probe)
-    rate = probe / max(time.perf_counter() - t0, 1e-6)
-    limit = int(min(E, max(probe, rate * target_s)))
-    desc = (f"{'reference lib (oracle/_ref)' if kind == 'reference' else 'C restatement (oracle/femoracle.c)'}: "
-            f"first {limit} of {E} elements of the same element type/form on a "
-            f"{'Kuhn ' + str(n_s) + '^3' if cfg['dim'] == 3 else str(n_s) + '^2'} mesh, "
-            f"{workers} OpenMP threads, pattern prebuilt (acceptance.cpp:295-296)")
+    h.assemble_sample(values, rhs, workers, 0, max(E // probe, 1), probe)   # warm (thread scratch, caches)
+    t = time.perf_counter()
+    h.assemble_sample(values, rhs, workers, 1 % max(E // probe, 1), max(E // probe, 1), probe)
+    rate = probe / max(time.perf_counter() - t, 1e-6)
+    count = int(min(E, max(probe, rate * target_s)))
+    stride = max(E // count, 1)
+    state = {"i": 0}
 
     def step():
+        first = state["i"] % stride
+        state["i"] += 1
         t = time.perf_counter()
-        run(limit)
-        return limit, time.perf_counter() - t
-
-    return step, kind, workers, desc
+        h.assemble_sample(values, rhs, workers, first, stride, count)
+        return count, time.perf_counter() - t
+    desc = (f"reference library (oracle/_ref: CAS + IR VM + binary-search scatter + atomic adds, "
+            f"{workers} OpenMP threads) on the full Kuhn {n}^3 mesh and its full CSR ({h.nnz} nnz, built in "
+            f"{pattern_s:.1f} s outside the timer): per step every {stride}-th element ({count} of {E})")
+    return step, "reference", workers, desc, True, (E, nd, h.nnz)
 
 
 def run_reference_arm(args, cfg, rank, world):
     if rank != 0:
         return
-    step, kind, workers, desc = cpu_reference_sample(cfg, target_s=args.ref_step_s)
+    step, kind, workers, desc, same, sizes = cpu_reference_sample(cfg, target_s=args.ref_step_s)
     for _ in range(args.warmup):
         step()
     elems, secs = 0, 0.0
@@ -229,10 +292,12 @@ def run_reference_arm(args, cfg, rank, world):
     value = elems / secs
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic structured mesh)",
-            "config": {"workload": cfg["workload"], "sample": desc},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": desc},
+            "config": workload_config(cfg, world, *sizes),
+            "sample": desc, "same_mesh": same,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": desc,
+                             "same_mesh": same, "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -254,9 +319,9 @@ def main():
     ap.add_argument("--block", type=int, default=256)
     ap.add_argument("--strategy", default="auto")
     ap.add_argument("--scatter", default="gather", choices=["gather", "atomic"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak = the 1-GPU workload stacked N times (one cell per GPU); "
-                         "strong = row blocks of the one 1-GPU mesh")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N>1: strong (default, SURVEY §8e) = contiguous DOF row blocks of the one configured "
+                         "mesh, halo elements duplicated; weak = the 1-GPU workload stacked N times")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.n:
@@ -435,25 +500,20 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            stepf, kind, workers, desc = cpu_reference_sample(cfg)
+            stepf, kind, workers, desc, same, _ = cpu_reference_sample(cfg)
             e, s = stepf()
-            cpu = {"value": e / s, "unit": UNIT, "cores": workers, "kind": kind, "sample": desc}
+            cpu = {"value": e / s, "unit": UNIT, "cores": workers, "kind": kind, "sample": desc,
+                   "same_mesh": same, "host": host_info()}
         except Exception as ex:  # never let the baseline hide the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
     value = E / (step_ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "strong" if world > 1 and not weak else "weak",
+        "scaling": "weak" if weak else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic structured mesh)",
-        "config": {"workload": cfg["workload"] + (f", stacked x{world} along the last axis (one cell per GPU)"
-                                                  if weak else ""),
-                   "n": cfg["n"], "elements": int(E), "dofs": int(dofs_tot),
-                   "nnz": int(nnz_tot), "form": cfg["form"], "quad_rule": cfg["quad"],
-                   "parallelism": f"row-blocks x{world} (halo elements duplicated, no collective)",
-                   "l2": "flushed (256 MiB write) between steps" if need_flush else
-                         f"inputs > L2 (CSR values {values.numel() * 8 / 1e9:.2f} GB)",
-                   "step": STEP_DESC[scatter] + ", inputs resident in HBM", "scatter": scatter,
+        "config": workload_config(cfg, world, E, dofs_tot, nnz_tot, weak),
+        "detail": {"step": STEP_DESC[scatter] + ", inputs resident in HBM", "scatter": scatter,
                    "k0_ms": k0_ms if scatter == "atomic" else 0.0,
                    "k2a_ms": k0_ms if scatter == "gather" else None,
                    "k2_ms": k2_ms, "pattern_build_ms": pattern_ms, "slot_plan_ms": plan_ms,

@@ -172,8 +172,13 @@ def ref():
         L.ffref_nnz.argtypes = [C.c_void_p]
         L.ffref_pattern.argtypes = [C.c_void_p, _i64p, _i32p]
         L.ffref_assemble.argtypes = [C.c_void_p, C.c_int, C.c_int64, _f64p, _f64p]
+        L.ffref_create3_on_pattern.restype = C.c_void_p
+        L.ffref_create3_on_pattern.argtypes = [C.c_int, _f64p, C.c_int64, _i32p, _i32p, C.c_int64, C.c_int64,
+                                               C.c_char_p, C.c_char_p, C.c_int, _i64p, _i32p]
+        L.ffref_assemble_sample.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, _f64p, _f64p]
         L.ffref_emit_demo_source.argtypes = [C.c_char_p, C.c_int64]
         L.ffref_max_threads.restype = C.c_int
+        L.ffref_build_info.restype = C.c_char_p
         L.ffref_export.argtypes = [C.c_void_p, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int]
         L.ffref_cg.argtypes = [C.c_void_p, _f64p, _f64p, C.c_double, C.c_int, _f64p, C.POINTER(C.c_int),
                                C.POINTER(C.c_double)]
@@ -209,15 +214,25 @@ class RefHarness:
     """The reference's own pipeline (2D P1) / CAS + IR VM (3D), see
     oracle/ref_harness.cpp."""
 
-    def __init__(self, dim, degree, coords, vconn, dconn, n_dofs, form, quad_id=4):
+    def __init__(self, dim, degree, coords, vconn, dconn, n_dofs, form, quad_id=4, pattern=None):
+        """pattern=(row_ptr, col_idx): 3D only -- search this prebuilt CSR
+        (kept alive here) instead of building the std::set pattern."""
         bil, lin = form_text(form, dim) if isinstance(form, str) else form
         self.L = ref()
         self.coords = np.ascontiguousarray(coords, np.float64)
         self.vconn = np.ascontiguousarray(vconn, np.int32)
         self.dconn = np.ascontiguousarray(dconn, np.int32)
         self.n_dofs = n_dofs
-        self.h = self.L.ffref_create(dim, degree, self.coords, coords.shape[0], self.vconn, self.dconn,
-                                     vconn.shape[0], n_dofs, bil.encode(), lin.encode(), quad_id)
+        self.n_elems = vconn.shape[0]
+        if pattern is not None:
+            self._rp = np.ascontiguousarray(pattern[0], np.int64)
+            self._ci = np.ascontiguousarray(pattern[1], np.int32)
+            self.h = self.L.ffref_create3_on_pattern(degree, self.coords, coords.shape[0], self.vconn, self.dconn,
+                                                     vconn.shape[0], n_dofs, bil.encode(), lin.encode(), quad_id,
+                                                     self._rp, self._ci)
+        else:
+            self.h = self.L.ffref_create(dim, degree, self.coords, coords.shape[0], self.vconn, self.dconn,
+                                         vconn.shape[0], n_dofs, bil.encode(), lin.encode(), quad_id)
         if not self.h:
             raise OracleError(self.L.ffref_last_error().decode())
         self.nnz = self.L.ffref_nnz(self.h)
@@ -233,6 +248,12 @@ class RefHarness:
             raise OracleError(self.L.ffref_last_error().decode())
         return vals, rhs
 
+
+    def assemble_sample(self, values, rhs, workers, first, stride, count):
+        """Accumulate elements first, first+stride, ... (count) into values/rhs
+        (no zero fill): a bounded timing sample of the full-mesh 3D loop."""
+        if self.L.ffref_assemble_sample(self.h, workers, first, stride, count, values, rhs) != 0:
+            raise OracleError(self.L.ffref_last_error().decode())
 
     def export(self, values, rhs, mpath, vpath, fmt=0):
         """The reference's export_matrix / export_vector of this 2D system."""

@@ -121,6 +121,12 @@ struct Harness {
   QuadRule3 quad;
   std::vector<std::int64_t> row_ptr;
   std::vector<std::int32_t> col_idx;
+  // CSR the scatter searches: the vectors above, or a caller-owned pattern
+  // (ffref_create3_on_pattern: full-size meshes whose std::set build would
+  // not fit the bench's time budget; the pattern is outside the timed
+  // region, acceptance.cpp:295-296)
+  const std::int64_t* rp = nullptr;
+  const std::int32_t* ci = nullptr;
 };
 
 // fem.cpp:68-71 generalised: Lagrange basis on the reference tet; P2 local
@@ -216,31 +222,95 @@ void pattern3(Harness& h) {
 
 inline std::int64_t find_slot(const Harness& h, int i, int j) {
   // binary search exactly as device.cpp:274-288
-  std::int64_t lo = h.row_ptr[i], hi = h.row_ptr[i + 1];
+  std::int64_t lo = h.rp[i], hi = h.rp[i + 1];
   while (lo < hi) {
     std::int64_t mid = (lo + hi) / 2;
-    if (h.col_idx[mid] < j)
+    if (h.ci[mid] < j)
       lo = mid + 1;
     else
       hi = mid;
   }
-  if (lo >= h.row_ptr[i + 1] || h.col_idx[lo] != j) return -1;
+  if (lo >= h.rp[i + 1] || h.ci[lo] != j) return -1;
   return lo;
 }
 
-}  // namespace
+// One element of the 3D device loop: IR-VM entries summed in ascending-q
+// order (device.cpp:147-205), binary-search scatter (device.cpp:265-305),
+// plain adds (det) or device::atomic_add (par, device.cpp:14-19).
+void element3(const Harness& h, std::int64_t e, double* values, double* rhs, bool par) {
+  thread_local std::vector<double> scratch;
+  const int nq = static_cast<int>(h.quad.w.size());
+  const int n = h.nloc;
+  const std::int32_t* vc = &h.vconn[4 * e];
+  const std::int32_t* dc = &h.dconn[n * e];
+  std::array<double, 15> a{};
+  for (int v = 0; v < 4; ++v)
+    for (int c = 0; c < 3; ++c) a[3 + 3 * v + c] = h.coords[3 * vc[v] + c];
+  double jm[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) jm[r][c] = a[3 + 3 * (c + 1) + r] - a[3 + r];
+  double det = jm[0][0] * (jm[1][1] * jm[2][2] - jm[1][2] * jm[2][1]) -
+               jm[0][1] * (jm[1][0] * jm[2][2] - jm[1][2] * jm[2][0]) +
+               jm[0][2] * (jm[1][0] * jm[2][1] - jm[1][1] * jm[2][0]);
+  if (std::abs(det) <= 1e-14)  // device.cpp:128, 180-186
+    throw std::runtime_error("degenerate element " + std::to_string(e) + " (|det J| <= 1e-14)");
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < n; ++j) {
+      double acc = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        a[0] = h.quad.p[q][0];
+        a[1] = h.quad.p[q][1];
+        a[2] = h.quad.p[q][2];
+        acc += h.quad.w[q] * h.bil[i * n + j].run(a, scratch);
+      }
+      std::int64_t s = find_slot(h, dc[i], dc[j]);
+      if (s < 0)
+        throw std::runtime_error("column " + std::to_string(dc[j]) + " not present in sparsity row " +
+                                 std::to_string(dc[i]));
+      if (par)
+        device::atomic_add(values[s], acc);
+      else
+        values[s] += acc;
+    }
+    double acc = 0.0;
+    for (int q = 0; q < nq; ++q) {
+      a[0] = h.quad.p[q][0];
+      a[1] = h.quad.p[q][1];
+      a[2] = h.quad.p[q][2];
+      acc += h.quad.w[q] * h.lin[i].run(a, scratch);
+    }
+    if (par)
+      device::atomic_add(rhs[dc[i]], acc);
+    else
+      rhs[dc[i]] += acc;
+  }
+}
 
-extern "C" {
+// Elements first, first+stride, ... (count of them) of the 3D loop: in order
+// (det mode) or OpenMP dynamic chunks with atomic adds (par mode).
+void run3(const Harness& h, std::int64_t first, std::int64_t stride, std::int64_t count, double* values, double* rhs,
+          int workers) {
+  const bool par = workers > 1;
+  if (!par) {
+    for (std::int64_t i = 0; i < count; ++i) element3(h, first + i * stride, values, rhs, false);
+    return;
+  }
+  std::string err;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(workers)
+  for (std::int64_t i = 0; i < count; ++i) {
+    try {
+      element3(h, first + i * stride, values, rhs, true);
+    } catch (const std::exception& ex) {
+#pragma omp critical(ffref_err)
+      if (err.empty()) err = ex.what();
+    }
+  }
+  if (!err.empty()) throw std::runtime_error(err);
+}
 
-const char* ffref_last_error() { return g_err.c_str(); }
-
-// Create a harness. coords: [nv][dim]; vconn: [ne][dim+1]; dconn: [ne][nloc]
-// (for P1, dconn == vconn). bilinear/linear: weak-form text over the reserved
-// symbols (u, u_x, u_y[, u_z], v, v_x, v_y[, v_z], x, y[, z]).
-// quad_id: 3D rule id (1, 4, 11, 14); ignored in 2D (reference rule, fem.cpp:43-48).
-void* ffref_create(int dim, int degree, const double* coords, std::int64_t nv,
-                   const std::int32_t* vconn, const std::int32_t* dconn, std::int64_t ne,
-                   std::int64_t n_dofs, const char* bilinear, const char* linear, int quad_id) {
+Harness* create(int dim, int degree, const double* coords, std::int64_t nv, const std::int32_t* vconn,
+                const std::int32_t* dconn, std::int64_t ne, std::int64_t n_dofs, const char* bilinear,
+                const char* linear, int quad_id, const std::int64_t* ext_row_ptr, const std::int32_t* ext_col_idx) {
   try {
     auto h = std::make_unique<Harness>();
     h->dim = dim;
@@ -271,6 +341,8 @@ void* ffref_create(int dim, int degree, const double* coords, std::int64_t nv,
       for (int i = 0; i < h->sp2.n; ++i)
         for (int k = 0; k < h->sp2.row_len[i]; ++k)
           h->col_idx[h->row_ptr[i] + k] = h->sp2.row_cols[static_cast<std::size_t>(i) * h->sp2.max_nz + k];
+      h->rp = h->row_ptr.data();
+      h->ci = h->col_idx.data();
       return h.release();
     }
     if (dim != 3 || (degree != 1 && degree != 2)) throw std::runtime_error("unsupported dim/degree");
@@ -281,11 +353,70 @@ void* ffref_create(int dim, int degree, const double* coords, std::int64_t nv,
     h->quad = tet_rule(quad_id);
     if (h->quad.w.empty()) throw std::runtime_error("unknown tet rule");
     instantiate3(*h, bl, li);
+    if (ext_row_ptr) {  // caller-owned pattern (ffref_create3_on_pattern)
+      h->rp = ext_row_ptr;
+      h->ci = ext_col_idx;
+      h->row_ptr.assign(1, ext_row_ptr[n_dofs]);  // ffref_nnz
+      return h.release();
+    }
     pattern3(*h);
+    h->rp = h->row_ptr.data();
+    h->ci = h->col_idx.data();
     return h.release();
   } catch (const std::exception& ex) {
     g_err = ex.what();
     return nullptr;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ffref_last_error() { return g_err.c_str(); }
+
+// Create a harness. coords: [nv][dim]; vconn: [ne][dim+1]; dconn: [ne][nloc]
+// (for P1, dconn == vconn). bilinear/linear: weak-form text over the reserved
+// symbols (u, u_x, u_y[, u_z], v, v_x, v_y[, v_z], x, y[, z]).
+// quad_id: 3D rule id (1, 4, 11, 14); ignored in 2D (reference rule, fem.cpp:43-48).
+void* ffref_create(int dim, int degree, const double* coords, std::int64_t nv,
+                   const std::int32_t* vconn, const std::int32_t* dconn, std::int64_t ne,
+                   std::int64_t n_dofs, const char* bilinear, const char* linear, int quad_id) {
+  return create(dim, degree, coords, nv, vconn, dconn, ne, n_dofs, bilinear, linear, quad_id, nullptr, nullptr);
+}
+
+
+// 3D harness over a caller-owned CSR (row_ptr [n_dofs+1], col_idx; must stay
+// alive with the harness): full-size meshes (Kuhn 128^3 P2: 485M nnz) whose
+// std::set pattern build (pattern3) would take minutes and tens of GB. The
+// pattern is built outside the timed region either way (acceptance.cpp:295-296).
+void* ffref_create3_on_pattern(int degree, const double* coords, std::int64_t nv, const std::int32_t* vconn,
+                               const std::int32_t* dconn, std::int64_t ne, std::int64_t n_dofs,
+                               const char* bilinear, const char* linear, int quad_id,
+                               const std::int64_t* row_ptr, const std::int32_t* col_idx) {
+  if (!row_ptr || !col_idx) {
+    g_err = "ffref_create3_on_pattern: null pattern";
+    return nullptr;
+  }
+  return create(3, degree, coords, nv, vconn, dconn, ne, n_dofs, bilinear, linear, quad_id, row_ptr, col_idx);
+}
+
+// Timing sample of the 3D parallel loop: elements first, first+stride, ...
+// (count of them), accumulated into values/rhs WITHOUT the zero fill (the
+// caller zeroes once). Used by bench.py's reference arm on the full mesh:
+// the stride spreads the sample over the whole CSR, like the full pass.
+int ffref_assemble_sample(void* p, int workers, std::int64_t first, std::int64_t stride, std::int64_t count,
+                          double* values, double* rhs) {
+  auto* h = static_cast<Harness*>(p);
+  try {
+    if (h->dim != 3) throw std::runtime_error("ffref_assemble_sample: 3D harness only");
+    if (first < 0 || stride < 1 || count < 0 || (count > 0 && first + (count - 1) * stride >= h->n_elems))
+      throw std::runtime_error("ffref_assemble_sample: element range outside the mesh");
+    run3(*h, first, stride, count, values, rhs, workers);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1;
   }
 }
 
@@ -332,70 +463,7 @@ int ffref_assemble(void* p, int workers, std::int64_t elem_limit, double* values
     std::fill(values, values + nnz, 0.0);
     std::fill(rhs, rhs + h->n_dofs, 0.0);
     const std::int64_t ne = elem_limit > 0 ? std::min(elem_limit, h->n_elems) : h->n_elems;
-    const int nq = static_cast<int>(h->quad.w.size());
-    const int n = h->nloc;
-    const bool par = workers > 1;
-    std::string err;
-    auto body = [&](std::int64_t e) {
-      thread_local std::vector<double> scratch;
-      const std::int32_t* vc = &h->vconn[4 * e];
-      const std::int32_t* dc = &h->dconn[n * e];
-      std::array<double, 15> a{};
-      for (int v = 0; v < 4; ++v)
-        for (int c = 0; c < 3; ++c) a[3 + 3 * v + c] = h->coords[3 * vc[v] + c];
-      double jm[3][3];
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) jm[r][c] = a[3 + 3 * (c + 1) + r] - a[3 + r];
-      double det = jm[0][0] * (jm[1][1] * jm[2][2] - jm[1][2] * jm[2][1]) -
-                   jm[0][1] * (jm[1][0] * jm[2][2] - jm[1][2] * jm[2][0]) +
-                   jm[0][2] * (jm[1][0] * jm[2][1] - jm[1][1] * jm[2][0]);
-      if (std::abs(det) <= 1e-14)  // device.cpp:128, 180-186
-        throw std::runtime_error("degenerate element " + std::to_string(e) + " (|det J| <= 1e-14)");
-      for (int i = 0; i < n; ++i) {
-        for (int j = 0; j < n; ++j) {
-          double acc = 0.0;
-          for (int q = 0; q < nq; ++q) {
-            a[0] = h->quad.p[q][0];
-            a[1] = h->quad.p[q][1];
-            a[2] = h->quad.p[q][2];
-            acc += h->quad.w[q] * h->bil[i * n + j].run(a, scratch);
-          }
-          std::int64_t s = find_slot(*h, dc[i], dc[j]);
-          if (s < 0)
-            throw std::runtime_error("column " + std::to_string(dc[j]) +
-                                     " not present in sparsity row " + std::to_string(dc[i]));
-          if (par)
-            device::atomic_add(values[s], acc);
-          else
-            values[s] += acc;
-        }
-        double acc = 0.0;
-        for (int q = 0; q < nq; ++q) {
-          a[0] = h->quad.p[q][0];
-          a[1] = h->quad.p[q][1];
-          a[2] = h->quad.p[q][2];
-          acc += h->quad.w[q] * h->lin[i].run(a, scratch);
-        }
-        if (par)
-          device::atomic_add(rhs[dc[i]], acc);
-        else
-          rhs[dc[i]] += acc;
-      }
-    };
-    if (!par) {
-      for (std::int64_t e = 0; e < ne; ++e) body(e);
-    } else {
-#pragma omp parallel for schedule(dynamic, 64) num_threads(workers)
-      for (std::int64_t e = 0; e < ne; ++e) {
-        try {
-          body(e);
-        } catch (const std::exception& ex) {
-#pragma omp critical(ffref_err)
-          if (err.empty()) err = ex.what();
-        }
-      }
-      if (!err.empty()) throw std::runtime_error(err);
-    }
+    run3(*h, 0, 1, ne, values, rhs, workers);
     return 0;
   } catch (const std::exception& ex) {
     g_err = ex.what();
@@ -418,6 +486,13 @@ int ffref_emit_demo_source(char* buf, std::int64_t cap) {
 }
 
 int ffref_max_threads() { return omp_get_max_threads(); }
+
+#ifndef FFREF_FLAGS
+#define FFREF_FLAGS "unknown"
+#endif
+// Compiler and flags the reference library was built with (bench.py prints
+// them with the CPU baseline).
+const char* ffref_build_info() { return "g++ " __VERSION__ " " FFREF_FLAGS; }
 
 // The reference's own export (linalg::export_matrix(EllMatrix) / export_vector,
 // linalg.cpp:148-210) of a 2D system given as CSR values over the harness's

@@ -503,8 +503,8 @@ def test_bench_two_ranks_on_one_gpu(ff):
            "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c3",
            "--size", "16", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
     n = 16
-    # strong scaling: row blocks of the one 16^3 mesh
-    out = subprocess.run(cmd + ["--scaling", "strong"], capture_output=True, text=True, env=env, timeout=600)
+    # strong scaling (default): row blocks of the one 16^3 mesh
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -512,8 +512,8 @@ def test_bench_two_ranks_on_one_gpu(ff):
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["config"]["nnz"] == 230 * n ** 3 + 138 * n ** 2 + 24 * n + 1
     assert d["value"] > 0 and d["e2e"]["value"] > 0
-    # weak scaling (default): the 16^3 cell stacked twice, one slab per rank
-    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+    # weak scaling: the 16^3 cell stacked twice, one slab per rank
+    out = subprocess.run(cmd + ["--scaling", "weak"], capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
     from paper_1802_03433_b200 import rowblocks

@@ -1,4 +1,4 @@
-"""Weak-scaling slabs (bench.py --gpus N, default): rank r of W meshes the r-th
+"""Weak-scaling slabs (bench.py --gpus N --scaling weak): rank r of W meshes the r-th
 cell of a box stacked W cells high, exactly as the library meshes one cell.
 Host logic only (CPU): the 1-rank slab is the library mesh itself, and the
 ranks' owned rows together are the pattern of the whole box, checked against
