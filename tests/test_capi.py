@@ -131,6 +131,19 @@ def test_cpp_host_suites():
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
 
 
+def test_integration_binding_is_the_documented_one():
+    """tests/cpp/ref_side/device_b200.cpp (compiled against the reference into
+    oracle/_ref/test_integration, run by the GPU suite) is INTEGRATION.md §2's
+    snippet verbatim, and it builds wherever the reference sources exist."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    a = doc.index("```cpp\n// src/device/device_b200.cpp") + len("```cpp\n")
+    snippet = doc[a:doc.index("```", a)]
+    src = open(os.path.join(ROOT, "tests", "cpp", "ref_side", "device_b200.cpp")).read()
+    assert src.endswith(snippet)
+    if os.path.isdir("/root/reference/proj/src"):
+        assert os.path.exists(os.path.join(ROOT, "oracle", "_ref", "test_integration"))
+
+
 def _row_classes(dconn, n_dofs, row_ptr, col_idx, min_rows):
     """Row classes as the gather plan defines them: rows whose incidences,
     sorted by (local index, slot bytes, element), and lengths coincide."""

@@ -137,7 +137,7 @@ class _DevArray:
     """A device allocation owned by the library, seen by torch (no copy)."""
 
     def __init__(self, ptr, n, typestr):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, True), "version": 3}
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
 
 
 def test_c5_elasticity_160_offsets_past_2_31_vs_oracle(ff, ctx):

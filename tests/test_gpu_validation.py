@@ -162,3 +162,19 @@ def test_pattern_of_scalar_mesh_rejected_for_vector_form(ff, ctx):
     m2 = ff.Mesh(ctx, 3, xyz, vc, dc, nd, ncomp=3)
     with pytest.raises(ff.DeviceError, match="components per node"):
         ff.assemble(f, m2, p)
+
+
+def test_reference_side_binding_matches_reference_assemble_sparse():
+    """INTEGRATION.md §2 compiled for real (oracle/_ref/test_integration: the
+    unmodified reference objects + the documented binding + libfemforge_b200.so):
+    assemble_sparse_b200 == the reference's assemble_sparse on 2D n=64 (demo
+    Helmholtz and Poisson): identical ELL columns, values/RHS <= 1e-12."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "test_integration")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/test_integration not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert r.stdout.count("-> ok") == 2 and "integration ok" in r.stdout
