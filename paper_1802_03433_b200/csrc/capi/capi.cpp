@@ -215,6 +215,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
+  if (const char* v = std::getenv("FF_PIPE")) src = "#define FF_PIPE " + std::to_string(std::atoi(v)) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
   bind(p->ctx);
   ffb::cuda_check(cudaLibraryLoadData(&p->class_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
@@ -287,11 +288,22 @@ int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w)
   return mode;
 }
 
+// K2a/class pipeline depth: chunks of the pipelined launch (0 = K2a, then the
+// row kernels); needs the plan's first-touch chunk boundaries
+int k2a_chunks(const ffb::kernels::GatherPlan& gp, unsigned flags) {
+  if (flags & (FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) return 0;
+  if (gp.chunk_rec.size() != ffb::kernels::GatherPlan::kChunks + 1 || gp.n_citems == 0) return 0;
+  int c = 8;
+  if (const char* v = std::getenv("FF_K2A_CHUNKS")) c = std::atoi(v);  // tuning knob
+  if (c <= 0) return 0;
+  while (ffb::kernels::GatherPlan::kChunks % c) --c;  // a divisor of kChunks
+  return c;
+}
+
 void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
                    unsigned flags, int w) {
   ff_ctx* ctx = f->ctx;
   ensure_gather_plan(p, m);
-  unsigned long long* wstatus = ctx->d_status;
   const int gs = ((f->plan.n_kinv + 3) / 4) * 4;  // FF_GS: invariants [E][gs] + load vectors [k][E]
   const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * (gs + f->n_local);
   if (p->ginv_cap < ng) {
@@ -301,34 +313,29 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     p->ginv_cap = ng;
   }
   unsigned long long* status = ctx->d_status;
+  // K2a over records [t0, t1)
+  auto launch_k2a = [&](int64_t t0, int64_t t1, cudaStream_t st) {
+    if (t1 <= t0) return;
+    const double* coords = m->coords;
+    const int32_t* vconn = p->gather.vconn_m;  // vertex ids in record order
+    const int32_t* dconn = m->dconn;
+    long long ne = m->ne, a = t0, b = t1;
+    double* ginv = p->ginv;
+    const int32_t* eorder = p->gather.eorder;
+    void* args[] = {&coords, &vconn, &dconn, &eorder, &ne, &ginv, &status, &a, &b};
+    const unsigned grid = static_cast<unsigned>((t1 - t0 + f->block - 1) / f->block);
+    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_ginv[w]), dim3(grid), dim3(f->block),
+                                     args, 0, st),
+                    "K2a (element invariants) launch");
+  };
+  const ffb::kernels::GatherPlan& gp = p->gather;
+  const int nchunks = k2a_chunks(gp, flags);
   if (!(flags & FF_GATHER_ROWS_ONLY)) {
     ffb::cuda_check(cudaMemsetAsync(status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
-    if (m->ne > 0) {
-      const double* coords = m->coords;
-      const int32_t* vconn = p->gather.vconn_m;  // vertex ids in record order
-      const int32_t* dconn = m->dconn;
-      long long ne = m->ne;
-      double* ginv = p->ginv;
-      const int32_t* eorder = p->gather.eorder;
-      void* args[] = {&coords, &vconn, &dconn, &eorder, &ne, &ginv, &status};
-      const unsigned grid = static_cast<unsigned>((m->ne + f->block - 1) / f->block);
-      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(f->kernel_ginv[w]), dim3(grid), dim3(f->block),
-                                       args, 0, s),
-                      "K2a (element invariants) launch");
-    }
+    if (nchunks == 0) launch_k2a(0, m->ne, s);
   }
   if (flags & FF_GATHER_INVARIANTS_ONLY) return;
-  const ffb::kernels::GatherPlan& gp = p->gather;
-  // the generic rows run on the side stream, concurrently with the class
-  // kernel (disjoint rows, both only read the element records): 2.861 ->
-  // 2.846 ms at the north star (run 34)
-  const bool generic_side = gp.n_citems > 0 && gp.n_items > 0 && !std::getenv("FF_GENERIC_SERIAL");
-  if (generic_side) {
-    ffb::cuda_check(cudaEventRecord(ctx->fork, s), "fork");
-    ffb::cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
-  }
-  const cudaStream_t sg = generic_side ? ctx->side : s;
-  auto launch_generic = [&]() {
+  auto launch_generic = [&](cudaStream_t sg) {
     // K2b for the remaining rows in two launches: short-pitch items, then long-pitch items
     // vector forms: FF_BS^2 sub-items (component pairs) per item
     const int64_t nb = static_cast<int64_t>(f->ncomp) * f->ncomp;
@@ -363,50 +370,78 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
                       "K2b (row gather) launch");
     }
   };
-  if (generic_side) launch_generic();
-  // K2b for the row classes: specialised kernels (rows in registers)
-  if (gp.n_citems > 0) {
-    ensure_class_module(f, p);
-    const int64_t cr[2][2] = {{0, gp.n_citems_short}, {gp.n_citems_short, gp.n_citems}};
-    // the long-row kernel runs on the context's side stream, concurrently with
-    // the short-row one (disjoint rows): the two register budgets share the SMs
-    // and the element records they both read stay in L2
-    const bool both = !generic_side && gp.n_citems_short > 0 && gp.n_citems > gp.n_citems_short &&
-                      !std::getenv("FF_SERIAL_CLASSES");
-    if (both) {
-      ffb::cuda_check(cudaEventRecord(ctx->fork, s), "fork");
-      ffb::cuda_check(cudaStreamWaitEvent(ctx->side, ctx->fork, 0), "fork");
-    }
-    for (int c = 1; c >= 0; --c) {
-      cudaStream_t sc = (both && c == 1) ? ctx->side : s;
-      long long i0 = cr[c][0], i1 = cr[c][1];
-      if (i1 <= i0) continue;
-      const int64_t ipw = class_ipw(f);
-      // 4 warps x FF_IPW items per CTA; vector forms: one CTA per component pair
-      const int cw = class_cwarps(f);
-      const unsigned grid = static_cast<unsigned>((i1 - i0 + cw * ipw - 1) / (cw * ipw) * f->ncomp * f->ncomp);
-      const double* ginv = p->ginv;
-      long long ne_arg = m->ne;
-      const int64_t* row_ptr = p->row_ptr;
-      const int32_t* icls = gp.citem_class;
-      const int32_t* irows = gp.citem_rows;
-      const int64_t* irec = gp.citem_rec;
-      const int32_t* crec = gp.crec;
-      void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
-      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(32 * cw), args,
-                                       p->class_smem[c], sc),
-                      "K2b (class row gather) launch");
-    }
-    if (both) {
-      ffb::cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
-      ffb::cuda_check(cudaStreamWaitEvent(s, ctx->join, 0), "join");
-    }
-  }
-  if (!generic_side) launch_generic();
-  if (generic_side) {
-    ffb::cuda_check(cudaEventRecord(ctx->join, ctx->side), "join");
+  // class items [a, b) with kernel c (0: short rows, 1: long rows)
+  auto launch_class = [&](int c, int64_t a, int64_t b, cudaStream_t sc) {
+    long long i0 = a, i1 = b;
+    if (i1 <= i0) return;
+    const int64_t ipw = class_ipw(f);
+    // FF_CWARPS warps x FF_IPW items per CTA; vector forms: one CTA per component pair
+    const int cw = class_cwarps(f);
+    const unsigned grid = static_cast<unsigned>((i1 - i0 + cw * ipw - 1) / (cw * ipw) * f->ncomp * f->ncomp);
+    const double* ginv = p->ginv;
+    long long ne_arg = m->ne;
+    const int64_t* row_ptr = p->row_ptr;
+    const int32_t* icls = gp.citem_class;
+    const int32_t* irows = gp.citem_rows;
+    const int64_t* irec = gp.citem_rec;
+    const int32_t* crec = gp.crec;
+    void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
+    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(32 * cw), args,
+                                     p->class_smem[c], sc),
+                    "K2b (class row gather) launch");
+  };
+  auto fork = [&](cudaStream_t to) {
+    ffb::cuda_check(cudaEventRecord(ctx->fork, s), "fork");
+    ffb::cuda_check(cudaStreamWaitEvent(to, ctx->fork, 0), "fork");
+  };
+  auto join = [&](cudaStream_t from) {
+    ffb::cuda_check(cudaEventRecord(ctx->join, from), "join");
     ffb::cuda_check(cudaStreamWaitEvent(s, ctx->join, 0), "join");
+  };
+  if (gp.n_citems > 0) ensure_class_module(f, p);
+  const int64_t ns = gp.n_citems_short;
+  if (nchunks > 0) {
+    // pipelined: K2a chunk c on the high-priority stream, then (side stream)
+    // the class items that read only records of chunks <= c, concurrently with
+    // K2a chunk c+1 -- K2a is HBM-bound, the class kernel latency-bound; the
+    // generic rows (any record) follow the last K2a chunk
+    fork(ctx->hi);
+    fork(ctx->side);
+    const int step = ffb::kernels::GatherPlan::kChunks / nchunks;
+    for (int c = 0; c < ffb::kernels::GatherPlan::kChunks; c += step) {
+      launch_k2a(gp.chunk_rec[c], gp.chunk_rec[c + step], ctx->hi);
+      ffb::cuda_check(cudaEventRecord(ctx->chunk, ctx->hi), "chunk");
+      ffb::cuda_check(cudaStreamWaitEvent(ctx->side, ctx->chunk, 0), "chunk");
+      const int64_t a = gp.chunk_item[c], b = gp.chunk_item[c + step];
+      launch_class(0, a, std::min(b, ns), ctx->side);
+      launch_class(1, std::max(a, ns), b, ctx->side);
+    }
+    launch_generic(ctx->hi);
+    join(ctx->hi);
+    join(ctx->side);
+    return;
   }
+  // the generic rows run on the side stream, concurrently with the class
+  // kernel (disjoint rows, both only read the element records): 2.861 ->
+  // 2.846 ms at the north star (run 34)
+  const bool generic_side = gp.n_citems > 0 && gp.n_items > 0 && !std::getenv("FF_GENERIC_SERIAL");
+  if (generic_side) {
+    fork(ctx->side);
+    launch_generic(ctx->side);
+  }
+  // K2b for the row classes: specialised kernels (rows in registers); the
+  // long-row kernel runs on the side stream, concurrently with the short-row
+  // one (disjoint rows): the two register budgets share the SMs and the
+  // element records they both read stay in L2
+  if (gp.n_citems > 0) {
+    const bool both = !generic_side && ns > 0 && gp.n_citems > ns && !std::getenv("FF_SERIAL_CLASSES");
+    if (both) fork(ctx->side);
+    launch_class(1, ns, gp.n_citems, both ? ctx->side : s);
+    launch_class(0, 0, ns, s);
+    if (both) join(ctx->side);
+  }
+  if (!generic_side) launch_generic(s);
+  if (generic_side) join(ctx->side);
 }
 
 void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
@@ -573,6 +608,10 @@ int ff_init(int device, ff_ctx** out) {
     ffb::cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attribute");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    int lo_prio = 0, hi_prio = 0;
+    ffb::cuda_check(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio), "stream priorities");
+    ffb::cuda_check(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
+    ffb::cuda_check(cudaEventCreateWithFlags(&c->chunk, cudaEventDisableTiming), "cudaEventCreate");
     ffb::cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
     ffb::cuda_check(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming), "cudaEventCreate");
     c->d_status = device_alloc<unsigned long long>(3, "status");  // [bad_elem, bad_row, scratch]
@@ -590,8 +629,11 @@ int ff_ctx_destroy(ff_ctx* ctx) {
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
     cudaStreamSynchronize(ctx->side);
+    cudaStreamSynchronize(ctx->hi);
     cudaEventDestroy(ctx->fork);
     cudaEventDestroy(ctx->join);
+    cudaEventDestroy(ctx->chunk);
+    cudaStreamDestroy(ctx->hi);
     cudaStreamDestroy(ctx->side);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1045,8 +1087,19 @@ int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* m, ff_gather_info* out)
     // what launch_gather issues: K2a + the class kernel(s) + the non-empty
     // generic ranges
     const auto& g = p->gather;
-    out->launches = (m->ne > 0 ? 1 : 0) + (g.n_citems_short > 0) + (g.n_citems > g.n_citems_short) +
-                    (g.n_short > 0) + (g.n_items > g.n_short);
+    const int nchunks = k2a_chunks(g, 0);
+    if (nchunks > 0) {  // pipelined: per chunk K2a + the non-empty class ranges
+      const int step = ffb::kernels::GatherPlan::kChunks / nchunks;
+      out->launches = (g.n_short > 0) + (g.n_items > g.n_short);
+      for (int c = 0; c < ffb::kernels::GatherPlan::kChunks; c += step) {
+        const int64_t a = g.chunk_item[c], b = g.chunk_item[c + step];
+        out->launches += (g.chunk_rec[c + step] > g.chunk_rec[c]) + (std::min(b, g.n_citems_short) > a) +
+                         (b > std::max(a, g.n_citems_short));
+      }
+    } else {
+      out->launches = (m->ne > 0 ? 1 : 0) + (g.n_citems_short > 0) + (g.n_citems > g.n_citems_short) +
+                      (g.n_short > 0) + (g.n_items > g.n_short);
+    }
   });
 }
 

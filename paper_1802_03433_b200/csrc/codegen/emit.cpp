@@ -288,6 +288,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
 #ifndef FF_IPW
 #define FF_IPW 2  // consecutive items per warp
 #endif
+#ifndef FF_PIPE
+#define FF_PIPE 1  // two-stage item prefetch (0: next item's header and records only)
+#endif
 #ifndef FF_CWARPS
 #define FF_CWARPS 4  // warps per CTA
 #endif
@@ -444,7 +447,36 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  int ep[FF_PRE];\n"
           "#pragma unroll\n"
           "  for (int u = 0; u < FF_PRE; ++u) ep[u] = u < ff_csteps[c] ? __ldcs(rec + u * 32) : -1;\n"
+          "#if FF_PIPE\n"
+          "  // two-stage item pipeline: while item w computes, the records and row\n"
+          "  // start of item w+1 load (addresses known one iteration ahead) and the\n"
+          "  // header of item w+2 loads -- no load waits on another at an item start\n"
+          "  ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
+          "  int c1 = 0, row1 = -1;\n"
+          "  ff_i64 r1 = 0;\n"
+          "  if (first + 1 < last) {\n"
+          "    c1 = __ldg(citem_class + first + 1);\n"
+          "    row1 = __ldg(citem_rows + (first + 1) * 32 + lane);\n"
+          "    r1 = __ldg(citem_rec + first + 1);\n"
+          "  }\n"
+          "#endif\n"
           "  for (ff_i64 w = first; w < last; ++w) {\n"
+          "#if FF_PIPE\n"
+          "    const int cn = c1, rown = row1;\n"
+          "    const ff_i32* recn = crec + r1 * 32 + lane;\n"
+          "    int epn[FF_PRE];\n"
+          "    ff_i64 rbegn = 0;\n"
+          "    if (w + 1 < last) {\n"
+          "#pragma unroll\n"
+          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = u < ff_csteps[cn] ? __ldcs(recn + u * 32) : -1;\n"
+          "      rbegn = rown >= 0 ? __ldg(row_ptr + rown) : 0;\n"
+          "    }\n"
+          "    if (w + 2 < last) {\n"
+          "      c1 = __ldg(citem_class + w + 2);\n"
+          "      row1 = __ldg(citem_rows + (w + 2) * 32 + lane);\n"
+          "      r1 = __ldg(citem_rec + w + 2);\n"
+          "    }\n"
+          "#else\n"
           "    int cn = 0, rown = -1, epn[FF_PRE];\n"
           "    const ff_i32* recn = rec;\n"
           "    if (w + 1 < last) {\n"
@@ -455,6 +487,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "      for (int u = 0; u < FF_PRE; ++u) epn[u] = u < ff_csteps[cn] ? __ldcs(recn + u * 32) : -1;\n"
           "    }\n"
           "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
+          "#endif\n"
           "    switch (c * FF_NB + cd) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
@@ -463,6 +496,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
              << "(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
     os << "      default: break;\n    }\n"
           "    c = cn;\n    row = rown;\n    rec = recn;\n"
+          "#if FF_PIPE\n    rbeg = rbegn;\n#endif\n"
           "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
           "  }\n}\n";
   };
