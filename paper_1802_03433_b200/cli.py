@@ -1,11 +1,10 @@
 """femforge-b200 command line: the reference CLI (tools/femforge.cpp) on the GPU
 path.
 
-  python -m paper_1802_03433_b200.cli assemble [--n N | --mesh-file F] [--out-matrix A.mtx] [--out-vector b.mtx]
+  python -m paper_1802_03433_b200.cli assemble [--n N] [--out-matrix A.mtx] [--out-vector b.mtx]
   python -m paper_1802_03433_b200.cli solve    [...] [--tol 1e-10] [--max-iter 10000] [--exact EXPR]
   python -m paper_1802_03433_b200.cli bench    [--sizes 64,128,256] [--repeats 3] [--csv PATH]
   python -m paper_1802_03433_b200.cli codegen  [--out-source kernel.cu] [--out-ir kernel.ir]
-  python -m paper_1802_03433_b200.cli mesh N   [--out mesh.txt]
 
 Same subcommands, options, output lines, files and exit codes as the
 reference (usage errors 2, runtime errors 1; femforge.cpp:368-374): the 2D
@@ -19,6 +18,10 @@ for option parity; the GPU launch shape does not depend on them. The bench
 CSV keeps the reference's columns (femforge.cpp:296-303) with one GPU row
 per size: evaluator `nvrtc`, mode `gpu`, workers = GPUs used; the GPU path
 has no interpreted evaluator, so `speedup_vs_interpreted` is `nan`.
+
+Outside the hot-path scope and not provided:
+the `mesh` subcommand and `--mesh-file` (mesh-file I/O, meshgen.cpp:50-119)
+and `--layout dense` (assemble_dense, the paper's dense toy).
 """
 from __future__ import annotations
 
@@ -27,8 +30,6 @@ import sys
 import time
 
 import numpy as np
-
-K_DEFAULT_MEM_CAP = 2 * 1024 * 1024 * 1024   # femforge.cpp:22
 
 
 class UsageError(Exception):
@@ -47,15 +48,14 @@ def add_problem_options(p):
     p.add_argument("--lambda", dest="lam", type=float, default=1.0, help="reaction coefficient")
     p.add_argument("--f", default="-2*(x^2+y^2)+36", help="right hand side expression over x,y")
     p.add_argument("--n", type=int, default=16, help="structured unit-square mesh subdivisions per side")
-    p.add_argument("--mesh-file", default="", help="mesh file path (overrides --n)")
-    p.add_argument("--layout", default="ell", choices=["dense", "ell"], help="matrix layout: dense|ell")
+    p.add_argument("--layout", default="ell", choices=["ell"],
+                   help="matrix layout: ell (CSR on the device; the dense toy layout, assemble_dense, is out of scope)")
     p.add_argument("--mode", default="det", choices=["det", "par"], help="execution mode: det|par")
     p.add_argument("--workers", type=int, default=0, help="worker count for parallel mode (option parity)")
     p.add_argument("--elems-per-block", type=int, default=4, help="elements per thread block (option parity)")
     p.add_argument("--evaluator", default="compiled", choices=["compiled", "interpreted", "nvrtc"],
                    help="integrand evaluator: compiled|nvrtc (NVRTC element kernels)")
     p.add_argument("--seed", type=int, default=0, help="seed for the parallel block schedule (option parity)")
-    p.add_argument("--mem-cap-bytes", type=int, default=K_DEFAULT_MEM_CAP, help="dense layout memory cap in bytes")
     p.add_argument("--device", type=int, default=0, help="CUDA device")
 
 
@@ -78,86 +78,10 @@ def build_form(cfg):
     return ff.helmholtz_text(2, [[sigma[0], sigma[1]], [sigma[2], sigma[3]]], repr(float(cfg.lam)), cfg.f)
 
 
-# ---- mesh files (meshgen.cpp:50-119) ----------------------------------------
-
-def write_mesh(coords, conn, path):
-    with open(path, "w") as f:
-        f.write(f"nodes {coords.shape[0]}\n")
-        for x, y in coords:
-            f.write("%.17g %.17g\n" % (x, y))
-        f.write(f"elements {conn.shape[0]}\n")
-        for a, b, c in conn:
-            f.write(f"{a} {b} {c}\n")
-
-
-def read_mesh(path):
-    """`nodes N`, N lines `x y`, `elements M`, M lines `i j k`; '#' comments
-    and blank lines skipped; clockwise elements reoriented (nodes 1 and 2
-    swapped) and counted. Errors name path:line (MeshError, exit 1)."""
-    ff = _ff()
-    try:
-        lines = open(path).read().split("\n")
-    except OSError:
-        raise ff.MeshError(ff.FF_E_MESH, f"cannot open '{path}'") from None
-    it = iter(enumerate(lines, 1))
-    state = {"lineno": 0}
-
-    def fail(msg):
-        raise ff.MeshError(ff.FF_E_MESH, f"{path}:{state['lineno']}: {msg}")
-
-    def next_content(what):
-        for lineno, raw in it:
-            state["lineno"] = lineno
-            s = raw.split("#", 1)[0]
-            if s.strip():
-                return s.split()
-        fail(f"unexpected end of file, expected {what}")
-
-    def header(tag):
-        t = next_content(f"'{tag} <N>'")
-        try:
-            n = int(t[1]) if len(t) >= 2 and t[0] == tag else -1
-        except ValueError:
-            n = -1
-        if n < 0:
-            fail(f"expected '{tag} <{'N' if tag == 'nodes' else 'M'}>'")
-        return n
-
-    nn = header("nodes")
-    coords = np.empty((nn, 2))
-    for k in range(nn):
-        t = next_content("node coordinates")
-        try:
-            coords[k] = float(t[0]), float(t[1])
-        except (ValueError, IndexError):
-            fail("malformed node line")
-    ne = header("elements")
-    conn = np.empty((ne, 3), np.int32)
-    reoriented = 0
-    for k in range(ne):
-        t = next_content("element indices")
-        try:
-            e = [int(t[0]), int(t[1]), int(t[2])]
-        except (ValueError, IndexError):
-            fail("malformed element line")
-        for idx in e:
-            if idx < 0 or idx >= nn:
-                fail(f"node index {idx} out of range")
-        p0, p1, p2 = coords[e[0]], coords[e[1]], coords[e[2]]
-        if (p1[0] - p0[0]) * (p2[1] - p0[1]) - (p2[0] - p0[0]) * (p1[1] - p0[1]) < 0.0:
-            e[1], e[2] = e[2], e[1]
-            reoriented += 1
-        conn[k] = e
-    return coords, conn, reoriented
-
-
 def load_mesh(cfg):
+    """The structured unit-square mesh (meshgen.cpp:13-33). Mesh files
+    (meshgen.cpp:50-119) are outside the hot-path scope."""
     ff = _ff()
-    if cfg.mesh_file:
-        coords, conn, reoriented = read_mesh(cfg.mesh_file)
-        if reoriented > 0:
-            print(f"note: reoriented {reoriented} element(s) to CCW", file=sys.stderr)
-        return coords, conn
     if cfg.n < 1:
         raise ff.MeshError(ff.FF_E_MESH, "unit_square_mesh: n must be >= 1")
     return ff.unit_square_mesh(cfg.n)
@@ -175,11 +99,6 @@ def run_assembly(cfg, coords, conn, ctx=None):
         raise UsageError("the GPU path has no interpreted evaluator (use --evaluator compiled|nvrtc)")
     bil, lin = build_form(cfg)
     n = coords.shape[0]
-    if cfg.layout == "dense":
-        need = n * n * 8
-        if need > cfg.mem_cap_bytes:
-            raise UsageError(f"dense matrix needs {need} bytes, over the memory cap of {cfg.mem_cap_bytes} "
-                             "(use --layout ell or raise --mem-cap-bytes)")
     ctx = ctx or ff.Context(cfg.device)
     ctx.set_scatter("gather" if cfg.mode == "det" else "atomic")
     form = ff.Form(ctx, 2, 1, bil, lin, quad_rule=3)
@@ -188,22 +107,9 @@ def run_assembly(cfg, coords, conn, ctx=None):
     values, rhs = ff.assemble(form, mesh, pat)
     s = System()
     s.ctx, s.form, s.mesh, s.pattern, s.values, s.rhs, s.n = ctx, form, mesh, pat, values, rhs, n
-    s.is_dense = cfg.layout == "dense"
-    s.nnz = n * n if s.is_dense else pat.nnz
-    s.max_nz = n if s.is_dense else pat.max_row_len
+    s.nnz = pat.nnz
+    s.max_nz = pat.max_row_len
     return s
-
-
-def export_dense(s, path):
-    """linalg.cpp:148-167 (array format, column-major, %.17g)."""
-    rp, ci = s.pattern.export()
-    a = np.zeros((s.n, s.n))
-    rows = np.repeat(np.arange(s.n), np.diff(rp))
-    a[rows, ci] = s.values
-    with open(path, "w") as f:
-        f.write(f"%%MatrixMarket matrix array real general\n{s.n} {s.n}\n")
-        for v in a.T.ravel():
-            f.write("%.17g\n" % v)
 
 
 def cmd_assemble(cfg):
@@ -212,10 +118,7 @@ def cmd_assemble(cfg):
     t0 = time.perf_counter()
     s = run_assembly(cfg, coords, conn)
     elapsed = 1e3 * (time.perf_counter() - t0)
-    if s.is_dense:
-        export_dense(s, cfg.out_matrix)
-    else:
-        ff.export_matrix(s.pattern, s.values, cfg.out_matrix)
+    ff.export_matrix(s.pattern, s.values, cfg.out_matrix)
     ff.export_vector(s.rhs, cfg.out_vector)
     print(f"N: {s.n}\nnnz: {s.nnz}\nMAX_NZ: {s.max_nz}\nwall_ms: {elapsed:.3f}")
     print(f"matrix: {cfg.out_matrix}\nvector: {cfg.out_vector}")
@@ -302,7 +205,7 @@ def cmd_bench(cfg):
     ctx = ff.Context(cfg.device)
     for n in cfg.sizes:
         c = argparse.Namespace(**vars(cfg))
-        c.n, c.layout, c.mesh_file = n, "ell", ""
+        c.n, c.layout = n, "ell"
         coords, conn = ff.unit_square_mesh(n)
         times = []
         for _ in range(cfg.repeats):
@@ -325,17 +228,6 @@ def cmd_bench(cfg):
             f.write("n,nodes,elements,evaluator,mode,workers,median_ms,speedup_vs_interpreted\n")
             for r in rows:
                 f.write(",".join(str(v) for v in r) + "\n")
-    return 0
-
-
-def cmd_mesh(cfg):
-    ff = _ff()
-    if cfg.mesh_n < 1:
-        print("error: n must be >= 1", file=sys.stderr)
-        return 2
-    coords, conn = ff.unit_square_mesh(cfg.mesh_n)
-    write_mesh(coords, conn, cfg.out)
-    print(f"mesh: {cfg.out}")
     return 0
 
 
@@ -367,9 +259,6 @@ def main(argv=None):
     add_problem_options(c)
     c.add_argument("--out-source", default="kernel.cu")
     c.add_argument("--out-ir", default="kernel.ir")
-    m = sub.add_parser("mesh", help="generate a structured unit-square mesh")
-    m.add_argument("mesh_n", type=int)
-    m.add_argument("--out", default="mesh.txt")
     try:
         cfg = ap.parse_args(argv)
         if cfg.cmd == "bench":
@@ -377,8 +266,7 @@ def main(argv=None):
                 cfg.sizes = [int(v) for v in cfg.sizes.split(",") if v]
             except ValueError:
                 raise UsageError("--sizes: comma-separated integers") from None
-        return {"assemble": cmd_assemble, "solve": cmd_solve, "bench": cmd_bench, "codegen": cmd_codegen,
-                "mesh": cmd_mesh}[cfg.cmd](cfg)
+        return {"assemble": cmd_assemble, "solve": cmd_solve, "bench": cmd_bench, "codegen": cmd_codegen}[cfg.cmd](cfg)
     except UsageError as e:
         print(f"error: {e}", file=sys.stderr)
         return 2
