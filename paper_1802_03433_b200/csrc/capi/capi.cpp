@@ -215,7 +215,6 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
-  if (const char* v = std::getenv("FF_PIPE")) src = "#define FF_PIPE " + std::to_string(std::atoi(v)) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
   bind(p->ctx);
   ffb::cuda_check(cudaLibraryLoadData(&p->class_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
@@ -288,18 +287,6 @@ int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w)
   return mode;
 }
 
-// K2a/class pipeline depth: chunks of the pipelined launch (0 = K2a, then the
-// row kernels); needs the plan's first-touch chunk boundaries
-int k2a_chunks(const ffb::kernels::GatherPlan& gp, unsigned flags) {
-  if (flags & (FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) return 0;
-  if (gp.chunk_rec.size() != ffb::kernels::GatherPlan::kChunks + 1 || gp.n_citems == 0) return 0;
-  int c = 8;
-  if (const char* v = std::getenv("FF_K2A_CHUNKS")) c = std::atoi(v);  // tuning knob
-  if (c <= 0) return 0;
-  while (ffb::kernels::GatherPlan::kChunks % c) --c;  // a divisor of kChunks
-  return c;
-}
-
 void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
                    unsigned flags, int w) {
   ff_ctx* ctx = f->ctx;
@@ -329,10 +316,9 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
                     "K2a (element invariants) launch");
   };
   const ffb::kernels::GatherPlan& gp = p->gather;
-  const int nchunks = k2a_chunks(gp, flags);
   if (!(flags & FF_GATHER_ROWS_ONLY)) {
     ffb::cuda_check(cudaMemsetAsync(status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
-    if (nchunks == 0) launch_k2a(0, m->ne, s);
+    launch_k2a(0, m->ne, s);
   }
   if (flags & FF_GATHER_INVARIANTS_ONLY) return;
   auto launch_generic = [&](cudaStream_t sg) {
@@ -377,7 +363,18 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     const int64_t ipw = class_ipw(f);
     // FF_CWARPS warps x FF_IPW items per CTA; vector forms: one CTA per component pair
     const int cw = class_cwarps(f);
-    const unsigned grid = static_cast<unsigned>((i1 - i0 + cw * ipw - 1) / (cw * ipw) * f->ncomp * f->ncomp);
+    const int nb = f->ncomp * f->ncomp;
+    int64_t ctas = (i1 - i0 + cw * ipw - 1) / (cw * ipw);
+    // FF_PERSIST=k (tuning knob): at most k waves of resident CTAs; each warp
+    // then loops over rounds of items with its item pipeline running across them
+    if (const char* v = std::getenv("FF_PERSIST")) {
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(p->class_kernel[c]),
+                                                        32 * cw, p->class_smem[c]) == cudaSuccess && occ > 0)
+        ctas = std::min<int64_t>(ctas, int64_t(std::max(1, std::atoi(v))) * occ * ctx->sm_count / nb);
+      cudaGetLastError();
+    }
+    const unsigned grid = static_cast<unsigned>(ctas * nb);
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;
     const int64_t* row_ptr = p->row_ptr;
@@ -400,27 +397,6 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   };
   if (gp.n_citems > 0) ensure_class_module(f, p);
   const int64_t ns = gp.n_citems_short;
-  if (nchunks > 0) {
-    // pipelined: K2a chunk c on the high-priority stream, then (side stream)
-    // the class items that read only records of chunks <= c, concurrently with
-    // K2a chunk c+1 -- K2a is HBM-bound, the class kernel latency-bound; the
-    // generic rows (any record) follow the last K2a chunk
-    fork(ctx->hi);
-    fork(ctx->side);
-    const int step = ffb::kernels::GatherPlan::kChunks / nchunks;
-    for (int c = 0; c < ffb::kernels::GatherPlan::kChunks; c += step) {
-      launch_k2a(gp.chunk_rec[c], gp.chunk_rec[c + step], ctx->hi);
-      ffb::cuda_check(cudaEventRecord(ctx->chunk, ctx->hi), "chunk");
-      ffb::cuda_check(cudaStreamWaitEvent(ctx->side, ctx->chunk, 0), "chunk");
-      const int64_t a = gp.chunk_item[c], b = gp.chunk_item[c + step];
-      launch_class(0, a, std::min(b, ns), ctx->side);
-      launch_class(1, std::max(a, ns), b, ctx->side);
-    }
-    launch_generic(ctx->hi);
-    join(ctx->hi);
-    join(ctx->side);
-    return;
-  }
   // the generic rows run on the side stream, concurrently with the class
   // kernel (disjoint rows, both only read the element records): 2.861 ->
   // 2.846 ms at the north star (run 34)
@@ -608,10 +584,7 @@ int ff_init(int device, ff_ctx** out) {
     ffb::cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attribute");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "cudaStreamCreate");
-    int lo_prio = 0, hi_prio = 0;
-    ffb::cuda_check(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio), "stream priorities");
-    ffb::cuda_check(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, hi_prio), "cudaStreamCreate");
-    ffb::cuda_check(cudaEventCreateWithFlags(&c->chunk, cudaEventDisableTiming), "cudaEventCreate");
+
     ffb::cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
     ffb::cuda_check(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming), "cudaEventCreate");
     c->d_status = device_alloc<unsigned long long>(3, "status");  // [bad_elem, bad_row, scratch]
@@ -629,11 +602,8 @@ int ff_ctx_destroy(ff_ctx* ctx) {
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
     cudaStreamSynchronize(ctx->side);
-    cudaStreamSynchronize(ctx->hi);
     cudaEventDestroy(ctx->fork);
     cudaEventDestroy(ctx->join);
-    cudaEventDestroy(ctx->chunk);
-    cudaStreamDestroy(ctx->hi);
     cudaStreamDestroy(ctx->side);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1087,19 +1057,8 @@ int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* m, ff_gather_info* out)
     // what launch_gather issues: K2a + the class kernel(s) + the non-empty
     // generic ranges
     const auto& g = p->gather;
-    const int nchunks = k2a_chunks(g, 0);
-    if (nchunks > 0) {  // pipelined: per chunk K2a + the non-empty class ranges
-      const int step = ffb::kernels::GatherPlan::kChunks / nchunks;
-      out->launches = (g.n_short > 0) + (g.n_items > g.n_short);
-      for (int c = 0; c < ffb::kernels::GatherPlan::kChunks; c += step) {
-        const int64_t a = g.chunk_item[c], b = g.chunk_item[c + step];
-        out->launches += (g.chunk_rec[c + step] > g.chunk_rec[c]) + (std::min(b, g.n_citems_short) > a) +
-                         (b > std::max(a, g.n_citems_short));
-      }
-    } else {
-      out->launches = (m->ne > 0 ? 1 : 0) + (g.n_citems_short > 0) + (g.n_citems > g.n_citems_short) +
-                      (g.n_short > 0) + (g.n_items > g.n_short);
-    }
+    out->launches = (m->ne > 0 ? 1 : 0) + (g.n_citems_short > 0) + (g.n_citems > g.n_citems_short) +
+                    (g.n_short > 0) + (g.n_items > g.n_short);
   });
 }
 

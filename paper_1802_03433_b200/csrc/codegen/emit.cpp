@@ -288,9 +288,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
 #ifndef FF_IPW
 #define FF_IPW 2  // consecutive items per warp
 #endif
-#ifndef FF_PIPE
-#define FF_PIPE 1  // two-stage item prefetch (0: next item's header and records only)
-#endif
+
 #ifndef FF_CWARPS
 #define FF_CWARPS 4  // warps per CTA
 #endif
@@ -436,10 +434,16 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  // vector forms: FF_NB consecutive CTAs run the same items, one component\n"
           "  // pair each (one code path per CTA; the items' records shared in L2)\n"
           "  const int cd = (int)(blockIdx.x % FF_NB);\n"
+          "  // items of this warp: FF_IPW consecutive ones per round, rounds one grid\n"
+          "  // apart (one round when the grid covers the range; a persistent grid\n"
+          "  // loops, and the item pipeline below runs across rounds)\n"
+          "  const ff_i64 stride = (ff_i64)(gridDim.x / FF_NB) * FF_CWARPS * FF_IPW;\n"
           "  const ff_i64 first = i0 + ((ff_i64)(blockIdx.x / FF_NB) * FF_CWARPS + wid) * FF_IPW;\n"
-          "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
-          "  if (first >= last) return;\n"
-          "  // the next item's header and first records load while this item computes\n"
+          "#define FF_ITEM(k) (first + ((k) / FF_IPW) * stride + ((k) % FF_IPW))\n"
+          "  if (first >= i1) return;\n"
+          "  // two-stage item pipeline: while item k computes, the records and row\n"
+          "  // start of item k+1 load (addresses known one iteration ahead) and the\n"
+          "  // header of item k+2 loads -- no load waits on another at an item start\n"
           "  // (the record array is padded by FF_PRE steps, so the loads need no bound)\n"
           "  int c = __ldg(citem_class + first);\n"
           "  int row = __ldg(citem_rows + first * 32 + lane);\n"
@@ -447,47 +451,31 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  int ep[FF_PRE];\n"
           "#pragma unroll\n"
           "  for (int u = 0; u < FF_PRE; ++u) ep[u] = u < ff_csteps[c] ? __ldcs(rec + u * 32) : -1;\n"
-          "#if FF_PIPE\n"
-          "  // two-stage item pipeline: while item w computes, the records and row\n"
-          "  // start of item w+1 load (addresses known one iteration ahead) and the\n"
-          "  // header of item w+2 loads -- no load waits on another at an item start\n"
           "  ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
           "  int c1 = 0, row1 = -1;\n"
           "  ff_i64 r1 = 0;\n"
-          "  if (first + 1 < last) {\n"
-          "    c1 = __ldg(citem_class + first + 1);\n"
-          "    row1 = __ldg(citem_rows + (first + 1) * 32 + lane);\n"
-          "    r1 = __ldg(citem_rec + first + 1);\n"
+          "  if (FF_ITEM(1) < i1) {\n"
+          "    const ff_i64 w1 = FF_ITEM(1);\n"
+          "    c1 = __ldg(citem_class + w1);\n"
+          "    row1 = __ldg(citem_rows + w1 * 32 + lane);\n"
+          "    r1 = __ldg(citem_rec + w1);\n"
           "  }\n"
-          "#endif\n"
-          "  for (ff_i64 w = first; w < last; ++w) {\n"
-          "#if FF_PIPE\n"
+          "  for (ff_i64 k = 0; FF_ITEM(k) < i1; ++k) {\n"
           "    const int cn = c1, rown = row1;\n"
           "    const ff_i32* recn = crec + r1 * 32 + lane;\n"
           "    int epn[FF_PRE];\n"
           "    ff_i64 rbegn = 0;\n"
-          "    if (w + 1 < last) {\n"
+          "    if (FF_ITEM(k + 1) < i1) {\n"
           "#pragma unroll\n"
           "      for (int u = 0; u < FF_PRE; ++u) epn[u] = u < ff_csteps[cn] ? __ldcs(recn + u * 32) : -1;\n"
           "      rbegn = rown >= 0 ? __ldg(row_ptr + rown) : 0;\n"
           "    }\n"
-          "    if (w + 2 < last) {\n"
-          "      c1 = __ldg(citem_class + w + 2);\n"
-          "      row1 = __ldg(citem_rows + (w + 2) * 32 + lane);\n"
-          "      r1 = __ldg(citem_rec + w + 2);\n"
+          "    if (FF_ITEM(k + 2) < i1) {\n"
+          "      const ff_i64 w2 = FF_ITEM(k + 2);\n"
+          "      c1 = __ldg(citem_class + w2);\n"
+          "      row1 = __ldg(citem_rows + w2 * 32 + lane);\n"
+          "      r1 = __ldg(citem_rec + w2);\n"
           "    }\n"
-          "#else\n"
-          "    int cn = 0, rown = -1, epn[FF_PRE];\n"
-          "    const ff_i32* recn = rec;\n"
-          "    if (w + 1 < last) {\n"
-          "      cn = __ldg(citem_class + w + 1);\n"
-          "      rown = __ldg(citem_rows + (w + 1) * 32 + lane);\n"
-          "      recn = crec + __ldg(citem_rec + w + 1) * 32 + lane;\n"
-          "#pragma unroll\n"
-          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = u < ff_csteps[cn] ? __ldcs(recn + u * 32) : -1;\n"
-          "    }\n"
-          "    const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
-          "#endif\n"
           "    switch (c * FF_NB + cd) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
@@ -495,10 +483,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           os << "      case " << c * nb + cd << ": ff_cls_" << c << "_" << cd
              << "(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
     os << "      default: break;\n    }\n"
-          "    c = cn;\n    row = rown;\n    rec = recn;\n"
-          "#if FF_PIPE\n    rbeg = rbegn;\n#endif\n"
+          "    c = cn;\n    row = rown;\n    rec = recn;\n    rbeg = rbegn;\n"
           "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
-          "  }\n}\n";
+          "  }\n#undef FF_ITEM\n}\n";
   };
   kernel("ff_gather_classes_s", false);
   kernel("ff_gather_classes_l", true);

@@ -52,10 +52,6 @@ struct GatherPlan {
   // eorder[t]; records (rec, crec) hold erank[e]
   int32_t* eorder = nullptr;
   int32_t* erank = nullptr;
-  // pipelined K2a/class launch (first-touch record order only): class items
-  // [chunk_item[c], chunk_item[c+1]) read records below chunk_rec[c+1]
-  static constexpr int kChunks = 32;
-  std::vector<int64_t> chunk_item, chunk_rec;  // kChunks + 1 boundaries each, or empty
 };
 // bbox: {min x, min y, min z, max x, max y, max z} of the mesh coordinates.
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,

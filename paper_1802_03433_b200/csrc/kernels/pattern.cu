@@ -460,22 +460,6 @@ __global__ void touch_keys(const unsigned long long* __restrict__ first, const i
   }
 }
 
-// out[c] = number of sorted keys below bound[c] (lower_bound on the device)
-__global__ void count_below(const uint64_t* __restrict__ sorted, int64_t n, const uint64_t* __restrict__ bound,
-                            int nb, int64_t* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nb) return;
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (sorted[mid] < bound[c])
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  out[c] = lo;
-}
-
 // record ranks of the old order -> ranks of the new one
 __global__ void remap_ranks(int32_t* __restrict__ crec, int64_t n, const int32_t* __restrict__ eorder_old,
                             const int32_t* __restrict__ erank_new) {
@@ -962,34 +946,6 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
         if ((err = need_temp(te)) != cudaSuccess) return tfree(), done(err);
         err = cub::DeviceRadixSort::SortPairs(temp, te, ek, ek2, eid, eorder_new, ne, 0, 64, s);
         if (err == cudaSuccess) {
-          // K2a/class overlap: with records in first-touch order, class items
-          // [0, P) read only records [0, R(P)), R(P) = elements first touched
-          // before item P -- chunk boundaries for the pipelined launch
-          const int nbd = GatherPlan::kChunks + 1;
-          std::vector<uint64_t> bnd(nbd);
-          out->chunk_item.resize(nbd);
-          out->chunk_rec.resize(nbd);
-          for (int c = 0; c < nbd; ++c) {
-            out->chunk_item[c] = nci * c / GatherPlan::kChunks;
-            bnd[c] = static_cast<uint64_t>(irec[out->chunk_item[c]]) * 32;
-          }
-          uint64_t* d_bnd = nullptr;
-          int64_t* d_cnt = nullptr;
-          err = cudaMalloc(&d_bnd, nbd * (sizeof(uint64_t) + sizeof(int64_t)));
-          if (err == cudaSuccess) {
-            d_cnt = reinterpret_cast<int64_t*>(d_bnd + nbd);
-            cudaMemcpyAsync(d_bnd, bnd.data(), nbd * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
-            count_below<<<1, 64, 0, s>>>(ek2, ne, d_bnd, nbd, d_cnt);
-            cudaMemcpyAsync(out->chunk_rec.data(), d_cnt, nbd * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-            err = cudaStreamSynchronize(s);
-            cudaFree(d_bnd);
-          }
-          if (err != cudaSuccess) {
-            out->chunk_item.clear();
-            out->chunk_rec.clear();
-            return tfree(), done(err);
-          }
-          out->chunk_rec[nbd - 1] = ne;  // the last chunk also computes the generic-only records
           invert_perm<<<grid_for(ne, cap), kThreads, 0, s>>>(eorder_new, ne, out->erank);
           remap_ranks<<<grid_for(out->n_crec, cap), kThreads, 0, s>>>(out->crec, out->n_crec, out->eorder,
                                                                        out->erank);

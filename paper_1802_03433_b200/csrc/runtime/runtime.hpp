@@ -41,8 +41,7 @@ struct ff_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;             // second stream: concurrent gather launches
-  cudaStream_t hi = nullptr;               // high priority: K2a chunks of the pipelined gather
-  cudaEvent_t fork = nullptr, join = nullptr, chunk = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   unsigned long long* d_status = nullptr;  // [bad_elem, bad_row]
   unsigned long long* h_status = nullptr;  // pinned mirror
   int scatter = 2;                          // FF_SCATTER_*_MODE (default: row gather)
