@@ -291,11 +291,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
                    unsigned flags, int w) {
   ff_ctx* ctx = f->ctx;
   ensure_gather_plan(p, m);
-  // FF_GS record values per element (invariants + point-value load factors)
-  // + the load vectors [k][E] when the record has no point-value factors
-  const int gs = ((f->plan.n_kinv + f->plan.n_bq + 3) / 4) * 4;
-  const std::size_t ng =
-      static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * (gs + (f->plan.n_bq > 0 ? 0 : f->n_local));
+  const int gs = ((f->plan.n_kinv + 3) / 4) * 4;  // FF_GS: invariants [E][gs] + load vectors [k][E]
+  const std::size_t ng = static_cast<std::size_t>(std::max<int64_t>(m->ne, 1)) * (gs + f->n_local);
   if (p->ginv_cap < ng) {
     cudaFree(p->ginv);
     p->ginv = nullptr;

@@ -21,7 +21,6 @@
 //    subexpressions are computed once per element).
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 #include <map>
 #include <optional>
 #include <set>
@@ -212,38 +211,10 @@ std::string emit_call(const Entry& en, const std::string& v) {
 // ---------------------------------------------------------------------------
 // ReferenceTensor
 
-// Point-value load vector: when l(v) = f(x) v, every load entry is
-// geo_linear[i] = phi_i(xi) * h with h = l(1) det J, so
-//   b_i = sum_q w_q phi_i(xi_q) h(xi_q) = sum_q phi_i(xi_q) F_q,  F_q = w_q h(xi_q).
-// With fewer points than local DOFs (P2, 4-point rule: 4 < 10) the element
-// record stores the F_q instead of the b_i, and the row kernels form b_i.
-// Returns H (h as a polynomial) when the identity holds for every i.
-std::optional<Poly> point_load_factor(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule, PolyBuilder& pb) {
-  if (f.ncomp != 1 || !f.geo_linear_unit.valid() || rule.size() >= f.n_local || std::getenv("FF_NO_POINT_LOAD"))
-    return std::nullopt;
-  const std::vector<Expr> phi = fem::reference_shape_functions(f.dim, f.degree);
-  if (static_cast<int>(phi.size()) != f.n_local) return std::nullopt;
-  auto h = pb.build(f.geo_linear_unit);
-  if (!h) return std::nullopt;
-  for (int i = 0; i < f.n_local; ++i) {
-    auto li = pb.build(f.geo_linear[i]);
-    auto pi = pb.build(phi[i]);
-    if (!li || !pi) return std::nullopt;
-    Poly d = poly_mul(*pi, *h);
-    long double scale = 0.0L;
-    for (const auto& [m, c] : *li) scale = std::max(scale, std::fabs(c));
-    poly_add(d, *li, -1.0L);
-    for (const auto& [m, c] : d)
-      if (std::fabs(c) > 1e-13L * (scale > 0 ? scale : 1.0L)) return std::nullopt;
-  }
-  return h;
-}
-
 std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
   PolyBuilder pb;
-  const std::optional<Poly> point_h = point_load_factor(f, rule, pb);
   std::vector<Expr> integrands = f.geo_bilinear;
-  if (!point_h) integrands.insert(integrands.end(), f.geo_linear.begin(), f.geo_linear.end());
+  integrands.insert(integrands.end(), f.geo_linear.begin(), f.geo_linear.end());
   std::vector<Poly> polys;
   for (const Expr& e : integrands) {
     auto p = pb.build(e);
@@ -408,18 +379,6 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
     for (const auto& [blk, t] : keyed) kq[t] = q++;
   }
   plan.n_kinv = static_cast<int>(kq.size());
-  // point-value load: phi_i at the rule's points (exact rationals evaluated in double)
-  std::vector<std::vector<double>> point_phi;
-  if (point_h) {
-    const std::vector<Expr> phi = fem::reference_shape_functions(f.dim, f.degree);
-    for (int i = 0; i < f.n_local; ++i) {
-      point_phi.emplace_back();
-      for (int q = 0; q < rule.size(); ++q)
-        point_phi[i].push_back(eval(phi[i], {{"xi", rule.points[q][0]}, {"eta", rule.points[q][1]},
-                                             {"zeta", f.dim == 3 ? rule.points[q][2] : 0.0}}));
-    }
-    plan.n_bq = rule.size();
-  }
   {
     std::vector<std::pair<int, int>> by_q;
     for (const auto& [t, q] : kq) by_q.push_back({q, t});
@@ -462,17 +421,6 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
     rc << "__constant__ double ff_kc[" << std::max<std::size_t>(coefs.size(), 1) << "] = {";
     for (std::size_t q = 0; q < coefs.size(); ++q) rc << (q ? ", " : "") << double_literal(coefs[q]);
     if (coefs.empty()) rc << "0.0";
-    if (point_h) {
-      // ff_brow<i>: b_i = sum_q phi_i(xi_q) g[FF_NKINV + q] (same terms and
-      // order as the element body's FF_EMIT_B)
-      for (int i = 0; i < f.n_local; ++i) {
-        body << "template <> __device__ __forceinline__ double ff_brow<" << i
-             << ">(const double* __restrict__ g) {\n  return ";
-        for (int q = 0; q < rule.size(); ++q)
-          body << (q ? " + " : "") << cref(point_phi[i][q]) << " * g[" << plan.n_kinv + q << "]";
-        body << ";\n}\n";
-      }
-    }
     rc << "};\n" << body.str();
     plan.row_code = rc.str();
   }
@@ -503,50 +451,6 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
     os << "  { const double " << name << " = " << v << ";";
     for (int r : members) os << " " << emit_call(entries[r], name);
     os << " }\n";
-  }
-  if (point_h) {
-    // F_q = w_q h(xi_q): h's polynomial in the reference coordinates,
-    // evaluated at each point over its geometry monomials
-    std::map<Mono, std::vector<long double>> by_geo;  // geometry monomial -> coefficient at each point
-    for (const auto& [m, c] : *point_h) {
-      Mono geo;
-      std::array<int, 3> ex{0, 0, 0};
-      for (const auto& [a, p] : m) {
-        if (a < 3)
-          ex[a] = p;
-        else
-          geo.push_back({a, p});
-      }
-      auto& v = by_geo[geo];
-      v.resize(rule.size(), 0.0L);
-      for (int q = 0; q < rule.size(); ++q) {
-        long double t = c * static_cast<long double>(rule.weights[q]);
-        for (int k = 0; k < 3; ++k)
-          for (int e = 0; e < ex[k]; ++e) t *= static_cast<long double>(rule.points[q][k]);
-        v[q] += t;
-      }
-    }
-    os << "  // point-value load vector: F_q = w_q l(1) det at the " << rule.size() << " points\n";
-    for (int q = 0; q < rule.size(); ++q) {
-      std::string expr;
-      for (const auto& [geo, v] : by_geo) {
-        const double c = static_cast<double>(v[q]);
-        if (c == 0.0) continue;
-        const std::string t = product(geo);
-        expr += (expr.empty() ? "" : " + ") + (t == "1.0" ? double_literal(c) : double_literal(c) + " * " + t);
-        flops += 2;
-      }
-      os << "  const double ff_F" << q << " = " << (expr.empty() ? "0.0" : expr) << ";\n";
-      os << "  FF_KBQ(" << q << ", ff_F" << q << ");\n";
-    }
-    for (int i = 0; i < f.n_local; ++i) {
-      std::string v;
-      for (int q = 0; q < rule.size(); ++q) {
-        v += (q ? " + " : "") + double_literal(point_phi[i][q]) + " * ff_F" + std::to_string(q);
-        flops += 2;
-      }
-      os << "  FF_EMIT_B(" << i << ", " << v << ");\n";
-    }
   }
   plan.n_unique_entries = static_cast<int>(ordered.size());
   plan.flops = flops;

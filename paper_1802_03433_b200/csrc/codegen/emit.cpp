@@ -79,8 +79,6 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   const bool gather = gather_capable(plan, f.n_local, f.ncomp, cfg.block_size);
   fill(text, "INVARIANT_LOAD", gather ? kInvariantLoad : "");
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));
-  fill(text, "NBQ", std::to_string(gather ? plan.n_bq : 0));
-  fill(text, "PAIR_TAIL", std::to_string(record_pair_tail(f.n_local, gather ? plan.n_bq : 0)));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
   {
     std::string d =
@@ -89,12 +87,6 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
     for (int i = 0; i < f.n_local; ++i)
       d += "    case " + std::to_string(i) + ": ff_gather_apply<" + std::to_string(i) + ">(r, g, d, arow); break;\n";
     d += "    default: break;\n  }\n}\n";
-    if (plan.n_bq > 0) {  // b_i from the record's point-value factors
-      d += "__device__ __forceinline__ double ff_bload_dispatch(int i, const double (&g)[FF_NKP]) {\n  switch (i) {\n";
-      for (int i = 0; i < f.n_local; ++i)
-        d += "    case " + std::to_string(i) + ": return ff_brow<" + std::to_string(i) + ">(g);\n";
-      d += "    default: return 0.0;\n  }\n}\n";
-    }
     fill(text, "ROW_DISPATCH", gather ? d : std::string());
   }
   if (text.find("{{") != std::string::npos) throw CodegenError("unresolved placeholder");
@@ -108,17 +100,7 @@ bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_s
   // vector forms)
   (void)block_size;
   return plan.n_kinv > 0 && ncomp >= 1 && n_local / ncomp <= 12 &&
-         (ncomp == 1 ? plan.n_kinv + (plan.n_bq > 0 ? plan.n_bq : n_local) <= 24 : plan.n_kinv <= 64);
-}
-
-// Tail of a scalar element record (FF_NREC % 4 values): a pair array [E][2]
-// when it holds <= 2 values and this returns 1, else a chunk array [E][4].
-// P1 records: pairs (eight elements per line, C2 0.81 -> 0.80 ms); P2
-// invariant-only tails measured slower as pairs (NS 2.57 -> 2.61 ms).
-// FF_PAIR_TAIL=0/1 overrides (read by both modules of a process).
-int record_pair_tail(int n_local, int n_bq) {
-  if (const char* v = std::getenv("FF_PAIR_TAIL")) return std::atoi(v) != 0 ? 1 : 0;
-  return n_local <= 4 || n_bq > 0 ? 1 : 0;
+         (ncomp == 1 ? plan.n_kinv + n_local <= 24 : plan.n_kinv <= 64);
 }
 
 namespace {
@@ -207,24 +189,21 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
   // gather each (test c, trial d) component pair as its own sub-row
   const int nsc = n_local / bs, nb = bs * bs;
   std::ostringstream os;
-  const int nrec = plan.n_kinv + plan.n_bq;
-  const int nkp = nrec + (nrec & 1);
-  const int erec = plan.n_bq > 0 ? (nrec + 1) & ~1 : (plan.n_kinv + n_local + 1) & ~1;
+  const int nkp = plan.n_kinv + (plan.n_kinv & 1);
+  const int erec = (plan.n_kinv + n_local + 1) & ~1;
   os << "// femforge-b200 class-specialised row gather (generated per (form, gather plan));\n"
         "// every class row stays in registers, indexed by compile-time slots.\n"
         "typedef long long ff_i64;\ntypedef int ff_i32;\n"
      << "#define FF_NLOC " << n_local << "\n#define FF_BS " << bs << "\n#define FF_NB " << nb
-     << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NBQ " << (bs == 1 ? plan.n_bq : 0)
-     << "\n#define FF_NREC (FF_NKINV + FF_NBQ)\n#define FF_NKP " << nkp
-     << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((nrec + 3) / 4) * 4 << "\n"
-     << "#define FF_NFULL (FF_NREC / 4)\n#define FF_PAIR_TAIL " << record_pair_tail(n_local, plan.n_bq) << "\n"
-     << "#define FF_GTAIL (FF_NREC % 4 == 0 ? 0 : ((FF_NREC % 4 <= 2 && FF_PAIR_TAIL) ? 2 : 4))\n"
+     << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
+     << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((plan.n_kinv + 3) / 4) * 4 << "\n"
+     << "#define FF_NFULL (FF_NKINV / 4)\n"
+     << "#define FF_GTAIL (FF_NKINV % 4 == 0 ? 0 : ((FF_NKINV % 4 <= 2 && FF_NLOC <= 4) ? 2 : 4))\n"
      << "#if FF_BS == 1\n#define FF_GSTORE (4 * FF_NFULL + FF_GTAIL)\n#else\n#define FF_GSTORE FF_GS\n#endif\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
      << class_stage_pitch(classes, 1, fused) << "\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
-     << "template <int I>\n__device__ __forceinline__ double ff_brow(const double* __restrict__ g);\n"
      << plan.row_code
      << R"(
 #ifdef FF_EINV_NA  // element records streamed past L1 (no allocation)
@@ -258,12 +237,7 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   ff_load_inv(einv, n_elems, ee, t);
 #pragma unroll
   for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
-#if FF_NBQ > 0
-  b = 0.0;  // formed from the record's point-value factors (ff_brow)
-  (void)i;
-#else
   b = ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)i * n_elems + ee);
-#endif
 }
 #define FF_PRE 8  // records of the next item prefetched while this item computes
 #ifndef FF_WUNROLL
@@ -422,12 +396,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           }
         }
         os << " }\n";
-        if (dd == 0) {
-          if (plan.n_bq > 0 && bs == 1)
-            os << "    bs += ff_brow<" << k.local[q] << ">(g" << q << ");\n";
-          else
-            os << "    bs += b" << q << ";\n";
-        }
+        if (dd == 0) os << "    bs += b" << q << ";\n";
       }
       os << "  }\n";
     }

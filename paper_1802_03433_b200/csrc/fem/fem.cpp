@@ -464,12 +464,6 @@ InstantiatedForm instantiate(const WeakForm& wf) {
         g.g[a][r] = s;
       }
     fill_entries(dim, phi, g, wf, out.geo_bilinear, out.geo_linear);
-    // the linear integrand at v = 1 (times det J): the load vector's
-    // point-value factor when l(v) = f(x) v (geo_linear[i] = phi_i * this)
-    const FormSymbols& fs = form_symbols();
-    std::vector<std::pair<Expr, Expr>> b{{fs.v, integer(1)}, {fs.x, g.x[0]}, {fs.y, g.x[1]}};
-    if (dim == 3) b.push_back({fs.z, g.x[2]});
-    out.geo_linear_unit = substitute(wf.linear, b) * g.det;
   }
   return out;
 }

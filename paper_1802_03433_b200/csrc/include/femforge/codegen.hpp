@@ -104,10 +104,6 @@ struct ElementPlan {
   // FF_KINV(q, ff_tT)), and per local row i the static code computing
   // v[j] = K_ij from g[q] (ff_row<i> specialisations).
   int n_kinv = 0;
-  // point-value load vector (l(v) = f(x) v, fewer points than local DOFs):
-  // the record holds n_bq = n_quad factors F_q after the invariants (body
-  // lines FF_KBQ(q, F_q)); row_code adds ff_brow<i>(g) = b_i
-  int n_bq = 0;
   std::string row_code;
   std::int64_t row_flops = 0;  // fp64 operations of all n_local rows
 };
@@ -152,7 +148,6 @@ struct RowClass {
 };
 
 // Whether the plan's kernels include the row gather (K2a + generic K2b).
-int record_pair_tail(int n_local, int n_bq);
 bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size);
 
 // Incidence order of a row class that minimises the number of row slots whose

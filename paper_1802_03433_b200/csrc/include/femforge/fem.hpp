@@ -149,9 +149,6 @@ struct InstantiatedForm {
   std::vector<Expr> linear;    // n_local
   std::vector<Expr> geo_bilinear;
   std::vector<Expr> geo_linear;
-  // scalar forms: the linear integrand with v = 1, times det J (geometry
-  // symbols); null for blocked forms
-  Expr geo_linear_unit;
 };
 
 // Geometry symbols of the GPU element prologue: gJrc (Jacobian dx_r/dxi_c),
