@@ -318,7 +318,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=2.0)
     ap.add_argument("--block", type=int, default=256)
     ap.add_argument("--strategy", default="auto")
-    ap.add_argument("--scatter", default="gather", choices=["gather", "atomic"])
+    ap.add_argument("--scatter", default="auto", choices=["auto", "gather", "atomic"],
+                    help="auto: both scatters timed on this config before the run, the faster one kept")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N>1: strong (default, SURVEY §8e) = contiguous DOF row blocks of the one configured "
                          "mesh, halo elements duplicated; weak = the 1-GPU workload stacked N times")
@@ -387,12 +388,15 @@ def main():
     t = time.perf_counter()
     pat.prepare(mesh)
     plan_ms = 1e3 * (time.perf_counter() - t)
-    scatter = pat.scatter_for(form)   # what actually runs (gather falls back to atomic for pointwise forms)
-    gather_info = pat.gather_info(mesh) if scatter == "gather" else None
     values = torch.empty(pat.nnz, dtype=torch.float64, device="cuda")
     rhs = torch.empty(pat.n_rows, dtype=torch.float64, device="cuda")
     stream = torch.cuda.Stream()       # every launch and every event on this one stream
     sp = stream.cuda_stream
+    calibration = None
+    if args.scatter == "auto":         # north star (3): the scatter chosen from measured times on this config
+        calibration = pat.calibrate_scatter(form, mesh, values.data_ptr(), rhs.data_ptr(), sp)
+    scatter = pat.scatter_for(form)   # what actually runs (gather falls back to atomic for pointwise forms)
+    gather_info = pat.gather_info(mesh) if scatter == "gather" else None
     l2_bytes = 126 * 2 ** 20
     need_flush = values.numel() * 8 < 2 * l2_bytes
     flush = torch.empty(2 * l2_bytes // 4, dtype=torch.int32, device="cuda") if need_flush else None
@@ -517,6 +521,7 @@ def main():
                    "k0_ms": k0_ms if scatter == "atomic" else 0.0,
                    "k2a_ms": k0_ms if scatter == "gather" else None,
                    "k2_ms": k2_ms, "pattern_build_ms": pattern_ms, "slot_plan_ms": plan_ms,
+                   "scatter_calibration": calibration,
                    "gather_plan": gather_info,
                    "nvrtc_compile_ms": compile_ms, "strategy": info["strategy"], "registers": info["registers"],
                    "flops_per_element": info["flops_per_element"],

@@ -100,8 +100,12 @@ void* ff_ctx_stream(ff_ctx* ctx); /* cudaStream_t of the context */
  *     (atomic-free, deterministic; needs a reference-tensor form, <= 12 DOFs
  *     per element and rows of <= 221 entries, else the atomic kernel runs);
  *   FF_SCATTER_ATOMIC_MODE: element-parallel fp64 RED after a zero-fill (the
- *     reference's parallel mode, device.cpp:193-200). */
-enum { FF_SCATTER_ATOMIC_MODE = 1, FF_SCATTER_GATHER_MODE = 2 };
+ *     reference's parallel mode, device.cpp:193-200);
+ *   FF_SCATTER_AUTO_MODE: measured choice -- the first device assembly of a
+ *     (form, pattern, mesh) times both scatters on the caller's buffers and
+ *     keeps the faster (ff_scatter_calibrate; the atomic scatter alone when
+ *     the form/pattern cannot gather). */
+enum { FF_SCATTER_ATOMIC_MODE = 1, FF_SCATTER_GATHER_MODE = 2, FF_SCATTER_AUTO_MODE = 3 };
 int ff_ctx_set_scatter(ff_ctx* ctx, int mode);
 
 /* ---- forms: weak form text -> symbolic -> CUDA source -> NVRTC (sm_100a) - */
@@ -174,6 +178,17 @@ int ff_class_source(const ff_form* form, int n, const int32_t* len, const int32_
 int ff_pattern_gather_info(ff_pattern* p, const ff_mesh* mesh, ff_gather_info* out);
 /* Which scatter the next assembly of (form, pattern) runs: FF_SCATTER_*_MODE. */
 int ff_scatter_selected(const ff_form* form, const ff_pattern* p, unsigned flags, int* mode);
+/* Times the row gather and the atomic scatter of (form, mesh, pattern) on the
+ * given device buffers (CUDA events on `stream`: one warm-up run, then the
+ * mean of 3 runs each; gather_ms < 0 when the gather cannot run), records the
+ * faster as the pattern's choice for FF_SCATTER_AUTO_MODE and returns it.
+ * Blocking; leaves a valid assembly in the buffers. */
+typedef struct ff_scatter_timing {
+  double gather_ms, atomic_ms;
+  int chosen;            /* FF_SCATTER_GATHER_MODE or FF_SCATTER_ATOMIC_MODE */
+} ff_scatter_timing;
+int ff_scatter_calibrate(ff_form* form, const ff_mesh* mesh, ff_pattern* p, double* d_values, double* d_rhs,
+                         void* stream, ff_scatter_timing* out);
 
 /* ---- numeric assembly (K0 zero-fill + K2 element kernel with scatter) ---- */
 /* Device-resident, asynchronous on `stream` (NULL: the context stream).

@@ -276,14 +276,20 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
 }
 
 // The scatter a (form, pattern, flags) assembly runs (FF_SCATTER_*_MODE).
+bool gather_possible(const ff_form* f, const ff_pattern* p, int w) {
+  return f->kernel_grows[w] && p->max_row_len <= 255 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax;
+}
+
 int select_scatter(const ff_form* f, const ff_pattern* p, unsigned flags, int w) {
   int mode = f->ctx ? f->ctx->scatter : FF_SCATTER_GATHER_MODE;
+  if (mode == FF_SCATTER_AUTO_MODE)  // the measured choice, else the row gather where it can run
+    mode = (p->auto_form == f->id && p->auto_generation == p->plan_generation && p->auto_mode)
+               ? p->auto_mode
+               : FF_SCATTER_GATHER_MODE;
   if (flags & FF_SCATTER_ATOMIC) mode = FF_SCATTER_ATOMIC_MODE;
   if (flags & (FF_SCATTER_GATHER | FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY)) mode = FF_SCATTER_GATHER_MODE;
   if (flags & (FF_ZERO_ONLY | FF_SKIP_ZERO)) mode = FF_SCATTER_ATOMIC_MODE;
-  if (mode == FF_SCATTER_GATHER_MODE &&
-      !(f->kernel_grows[w] && p->max_row_len <= 255 && gather_smem(gather_pitch(p->max_row_len)) <= kGatherSmemMax))
-    mode = FF_SCATTER_ATOMIC_MODE;
+  if (mode == FF_SCATTER_GATHER_MODE && !gather_possible(f, p, w)) mode = FF_SCATTER_ATOMIC_MODE;
   return mode;
 }
 
@@ -415,7 +421,49 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
 }
 
 void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
-                     unsigned flags = 0) {
+                     unsigned flags = 0);
+
+// FF_SCATTER_AUTO_MODE: times both scatters (CUDA events on s, one warm-up
+// then the mean of 3 runs each) and records the faster for (form, plan).
+void calibrate_scatter(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s) {
+  ensure_plan(p, m);
+  const int w = p->slot_bytes;
+  build_variant(f, w);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ffb::cuda_check(cudaEventCreate(&e0), "cudaEventCreate");
+  ffb::cuda_check(cudaEventCreate(&e1), "cudaEventCreate");
+  double ms[2] = {-1.0, -1.0};
+  const unsigned fl[2] = {FF_SCATTER_GATHER, FF_SCATTER_ATOMIC};
+  try {
+    for (int v = 0; v < 2; ++v) {
+      if (v == 0 && !gather_possible(f, p, w)) continue;
+      launch_assembly(f, m, p, d_values, d_rhs, s, fl[v]);  // warm-up: plans, modules
+      ffb::cuda_check(cudaEventRecord(e0, s), "event");
+      for (int r = 0; r < 3; ++r) launch_assembly(f, m, p, d_values, d_rhs, s, fl[v]);
+      ffb::cuda_check(cudaEventRecord(e1, s), "event");
+      ffb::cuda_check(cudaEventSynchronize(e1), "calibration");
+      float t = 0.f;
+      ffb::cuda_check(cudaEventElapsedTime(&t, e0, e1), "event");
+      ms[v] = t / 3.0;
+    }
+  } catch (...) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    throw;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  p->auto_ms[0] = ms[0];
+  p->auto_ms[1] = ms[1];
+  p->auto_mode = (ms[0] >= 0.0 && ms[0] <= ms[1]) ? FF_SCATTER_GATHER_MODE : FF_SCATTER_ATOMIC_MODE;
+  p->auto_form = f->id;
+  p->auto_generation = p->plan_generation;
+  if (p->auto_mode == FF_SCATTER_GATHER_MODE)  // leave the chosen scatter's result in the buffers
+    launch_assembly(f, m, p, d_values, d_rhs, s, FF_SCATTER_GATHER);
+}
+
+void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, cudaStream_t s,
+                     unsigned flags) {
   require(f->ctx && f->ctx == m->ctx && m->ctx == p->ctx, "form, mesh and pattern must share one context");
   require(f->dim == m->dim, "form and mesh dimensions differ");
   require(f->ncomp == m->bs && f->n_local == m->k * m->bs, "form and mesh have different DOFs per element");
@@ -425,6 +473,14 @@ void launch_assembly(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_valu
   build_variant(f, w);
   ff_ctx* ctx = f->ctx;
   const int64_t n_rows = p->re - p->rb;
+  if (ctx->scatter == FF_SCATTER_AUTO_MODE && flags == 0 &&
+      !(p->auto_form == f->id && p->auto_generation == p->plan_generation && p->auto_mode)) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+      calibrate_scatter(f, m, p, d_values, d_rhs, s);
+      return;  // the buffers hold the chosen scatter's assembly
+    }
+  }
   const int mode = select_scatter(f, p, flags, w);
   if (mode == FF_SCATTER_GATHER_MODE) {
     launch_gather(f, m, p, d_values, d_rhs, s, flags, w);
@@ -617,7 +673,7 @@ void* ff_ctx_stream(ff_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) 
 int ff_ctx_set_scatter(ff_ctx* ctx, int mode) {
   return guarded([&] {
     require(ctx, "null context");
-    require(mode == FF_SCATTER_ATOMIC_MODE || mode == FF_SCATTER_GATHER_MODE,
+    require(mode == FF_SCATTER_ATOMIC_MODE || mode == FF_SCATTER_GATHER_MODE || mode == FF_SCATTER_AUTO_MODE,
             "unknown scatter mode");
     ctx->scatter = mode;
   });
@@ -1115,6 +1171,22 @@ int ff_assemble_device(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_va
     ffb::cuda_check(e, "cudaGraphInstantiate");
     p->graph_key = key;
     ffb::cuda_check(cudaGraphLaunch(p->graph_exec, s), "cudaGraphLaunch");
+  });
+}
+
+int ff_scatter_calibrate(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values, double* d_rhs, void* stream,
+                         ff_scatter_timing* out) {
+  return guarded([&] {
+    require(f && m && p && d_values && d_rhs, "ff_scatter_calibrate: null argument");
+    require(f->ctx && f->ctx == m->ctx && m->ctx == p->ctx, "form, mesh and pattern must share one context");
+    bind(f->ctx);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : f->ctx->stream;
+    calibrate_scatter(f, m, p, d_values, d_rhs, s);
+    if (out) {
+      out->gather_ms = p->auto_ms[0];
+      out->atomic_ms = p->auto_ms[1];
+      out->chosen = p->auto_mode;
+    }
   });
 }
 

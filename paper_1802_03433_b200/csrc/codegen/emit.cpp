@@ -79,6 +79,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   const bool gather = gather_capable(plan, f.n_local, f.ncomp, cfg.block_size);
   fill(text, "INVARIANT_LOAD", gather ? kInvariantLoad : "");
   fill(text, "NKINV", std::to_string(gather ? plan.n_kinv : 0));
+  fill(text, "PAIR_TAIL", std::to_string(record_pair_tail(f.n_local)));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
   {
     std::string d =
@@ -90,10 +91,21 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
     fill(text, "ROW_DISPATCH", gather ? d : std::string());
   }
   if (text.find("{{") != std::string::npos) throw CodegenError("unresolved placeholder");
+  if (const char* v = std::getenv("FF_WAGG")) text = "#define FF_WAGG " + std::to_string(std::atoi(v) != 0) + "\n" + text;
   if (plan_out) *plan_out = std::move(plan);
   return text;
 }
 
+
+// Tail of a scalar element record (n_kinv % 4 invariants): a pair array
+// [E][2] when it holds <= 2 values and this returns 1, else a chunk array
+// [E][4]. Pairs for P1 records (eight elements per line, C2 0.81 -> 0.80 ms);
+// chunks for P2 (NS 2.57 -> 2.61 ms with pairs). FF_PAIR_TAIL=0/1 overrides
+// (read by both modules of a process, so K2a and the class kernels agree).
+int record_pair_tail(int n_local) {
+  if (const char* v = std::getenv("FF_PAIR_TAIL")) return std::atoi(v) != 0 ? 1 : 0;
+  return n_local <= 4 ? 1 : 0;
+}
 
 bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size) {
   // a reference-tensor plan and <= 12 slot bytes per record (node rows for
@@ -173,22 +185,12 @@ std::vector<int> class_step_order(const RowClass& k, int n_local) {
   return best;
 }
 
-// Rows of <= 33 entries leave the staging tile by one asynchronous bulk copy
-// (cp.async.bulk shared -> global, the TMA engine) per row instead of the
-// warp's store loop; FF_BULK=0 keeps the store loop.
-bool class_bulk_rows() {
-  const char* v = std::getenv("FF_BULK");
-  return !v || std::atoi(v) != 0;
-}
-
 int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused) {
   int m = 1;
   for (const auto& c : classes)
     if (fused || (c.len > 33) == (kernel == 1)) m = std::max(m, c.len);
-  // rows longer than 33 are staged in chunks of 32 in finalisation order;
-  // bulk-copied rows start one double later when that aligns them with
-  // their CSR position (16-byte copies)
-  return (std::min(m, 33) + (class_bulk_rows() ? 1 : 0)) | 1;  // odd: conflict-free lane-row stores
+  // rows longer than 33 are staged in chunks of 32 in finalisation order
+  return std::min(m, 33) | 1;  // odd: conflict-free lane-row stores
 }
 
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes, bool fused,
@@ -207,8 +209,8 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "#define FF_NLOC " << n_local << "\n#define FF_BS " << bs << "\n#define FF_NB " << nb
      << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
      << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((plan.n_kinv + 3) / 4) * 4 << "\n"
-     << "#define FF_NFULL (FF_NKINV / 4)\n"
-     << "#define FF_GTAIL (FF_NKINV % 4 == 0 ? 0 : ((FF_NKINV % 4 <= 2 && FF_NLOC <= 4) ? 2 : 4))\n"
+     << "#define FF_NFULL (FF_NKINV / 4)\n#define FF_PAIR_TAIL " << record_pair_tail(n_local) << "\n"
+     << "#define FF_GTAIL (FF_NKINV % 4 == 0 ? 0 : ((FF_NKINV % 4 <= 2 && FF_PAIR_TAIL) ? 2 : 4))\n"
      << "#if FF_BS == 1\n#define FF_GSTORE (4 * FF_NFULL + FF_GTAIL)\n#else\n#define FF_GSTORE FF_GS\n#endif\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
@@ -295,29 +297,6 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   }
   __syncwarp();
 }
-// bulk write-out of one staged row (rows <= 33 entries): the 16-byte aligned
-// middle by an asynchronous bulk copy (TMA engine), an odd head / tail double
-// by plain stores; the staging row's parity matches the CSR row's, so the
-// middle is aligned at both ends
-__device__ __forceinline__ void ff_bulk_wait() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void ff_bulk_row(const double* s, double* g, int n) {
-  if (n <= 0) return;
-  if ((reinterpret_cast<unsigned long long>(g) & 15ull) != 0) {
-    __stcs(g, s[0]);
-    ++g;
-    ++s;
-    --n;
-  }
-  const int nb = n & ~1;
-  if (nb > 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(sa), "r"(nb * 8)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  }
-  if (n & 1) __stcs(g + nb, s[nb]);
-}
 #ifndef FF_IPW
 #define FF_IPW 2  // consecutive items per warp
 #endif
@@ -388,13 +367,10 @@ __device__ __forceinline__ void ff_bulk_row(const double* s, double* g, int n) {
       else
         os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
     }
-    const bool bulk = !chunked && bs == 1 && class_bulk_rows();
-    if (bulk) os << "  double* stl = st + lane * " << sp << " + (int)((rbeg ^ lane) & 1);\n";
     if (dd == 0) os << "  double bs = 0.0;\n";
     for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
     os << ";\n";
-    if (!bulk)
-      os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
+    os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
     const int depth = bs == 1 ? 8 : (std::getenv("FF_VDEPTH") ? std::max(1, std::atoi(std::getenv("FF_VDEPTH"))) : 2);
     for (int t0 = 0; t0 < k.steps; t0 += depth) {
       const int t1 = std::min(k.steps, t0 + depth);
@@ -404,9 +380,6 @@ __device__ __forceinline__ void ff_bulk_row(const double* s, double* g, int n) {
         os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] * bs + cc
            << ", einv, n_elems, g" << q << ", b" << q << ");\n";
       }
-      // the previous item's bulk copies have read the staging tile (waited
-      // for after this item's first loads are in flight)
-      if (bulk && t0 == 0) os << "    ff_bulk_wait();\n";
       for (int t = t0; t < t1; ++t) {
         const int q = order[t];
         os << "    { double v[FF_NLOC]; ff_row<" << k.local[q] * bs + cc << ">(g" << q << ", v);";
@@ -417,12 +390,7 @@ __device__ __forceinline__ void ff_bulk_row(const double* s, double* g, int n) {
         if (!chunked) {
           for (int j = 0; j < n_local; ++j) {
             const int sl = k.slots[q * n_local + j];
-            if (last[sl] == t) {
-              if (bulk)
-                os << " stl[" << sl << "] = a" << sl << ";";
-              else
-                os << " st[lane * " << sp << " + " << sl << "] = a" << sl << ";";
-            }
+            if (last[sl] == t) os << " st[lane * " << sp << " + " << sl << "] = a" << sl << ";";
           }
         } else {
           std::vector<int> closing;  // finalisation ranks closing at step t
@@ -446,9 +414,7 @@ __device__ __forceinline__ void ff_bulk_row(const double* s, double* g, int n) {
     }
     // write-out through the staging rows (consecutive lanes = consecutive CSR
     // values of one row)
-    if (bulk)
-      os << "  ff_bulk_row(stl, values + rbeg, row >= 0 ? " << k.len << " : 0);\n";
-    else if (!chunked)
+    if (!chunked)
       for (int q0 = 0; q0 < k.len; q0 += 32)
         os << "  ff_writeout(st + " << q0 << ", " << sp << ", sr, lane, " << std::min(32, k.len - q0) << ", " << q0
            << ", values);\n";
@@ -473,7 +439,7 @@ __device__ __forceinline__ void ff_bulk_row(const double* s, double* g, int n) {
           "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
           "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
           "  // dynamic shared memory: 4 staging tiles [32][FF_SP] + 4 x 32 row offsets\n"
-          "  extern __shared__ __align__(16) double ff_dsm[];\n"
+          "  extern __shared__ double ff_dsm[];\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
           "  double* st = ff_dsm + wid * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ";\n"
           "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ") + wid * 32;\n"
@@ -531,9 +497,7 @@ __device__ __forceinline__ void ff_bulk_row(const double* s, double* g, int n) {
     os << "      default: break;\n    }\n"
           "    c = cn;\n    row = rown;\n    rec = recn;\n    rbeg = rbegn;\n"
           "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
-          "  }\n"
-          "  asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");  // staging tiles live until copied\n"
-          "#undef FF_ITEM\n}\n";
+          "  }\n#undef FF_ITEM\n}\n";
   };
   kernel("ff_gather_classes_s", false);
   kernel("ff_gather_classes_l", true);

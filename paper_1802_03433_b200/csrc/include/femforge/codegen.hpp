@@ -148,6 +148,7 @@ struct RowClass {
 };
 
 // Whether the plan's kernels include the row gather (K2a + generic K2b).
+int record_pair_tail(int n_local);
 bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size);
 
 // Incidence order of a row class that minimises the number of row slots whose

@@ -118,6 +118,10 @@ struct ff_pattern {
   double* ginv = nullptr;   // [ne][nkp]
   double* bvec = nullptr;   // [ne][k]
   std::size_t ginv_cap = 0, bvec_cap = 0;
+  // FF_SCATTER_AUTO_MODE: the measured choice for (form id, slot-plan generation)
+  std::uint64_t auto_form = 0, auto_generation = ~0ull;
+  int auto_mode = 0;
+  double auto_ms[2] = {-1.0, -1.0};  // gather, atomic
   // device scratch of the host-buffer (end-to-end) entry point
   double* e2e_values = nullptr;
   double* e2e_rhs = nullptr;

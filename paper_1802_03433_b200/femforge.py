@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libfemforge_b200.so")
 FF_OK, FF_E_ARG, FF_E_DEGENERATE, FF_E_PATTERN, FF_E_NVRTC, FF_E_CUDA, FF_E_FORM, FF_E_MESH, FF_E_SYMBOLIC, FF_E_NOMEM = \
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9
 STRATEGY = {"auto": 0, "tensor": 1, "pointwise": 2}
-SCATTER_MODE = {"atomic": 1, "gather": 2}
+SCATTER_MODE = {"atomic": 1, "gather": 2, "auto": 3}
 SCATTER_NAME = {v: k for k, v in SCATTER_MODE.items()}
 
 
@@ -89,6 +89,10 @@ class Stats(C.Structure):
     _fields_ = [("bad_element", C.c_int64), ("bad_row", C.c_int64), ("ms", C.c_double)]
 
 
+class ScatterTiming(C.Structure):
+    _fields_ = [("gather_ms", C.c_double), ("atomic_ms", C.c_double), ("chosen", C.c_int)]
+
+
 _P = C.c_void_p
 _i64 = C.c_int64
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
@@ -130,6 +134,7 @@ SIGNATURES = [
     ("ff_pattern_prepare", C.c_int, [_P, _P]),
     ("ff_pattern_gather_info", C.c_int, [_P, _P, C.POINTER(GatherInfo)]),
     ("ff_scatter_selected", C.c_int, [_P, _P, C.c_uint, C.POINTER(C.c_int)]),
+    ("ff_scatter_calibrate", C.c_int, [_P, _P, _P, _P, _P, _P, C.POINTER(ScatterTiming)]),
     ("ff_assemble_device", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("ff_assemble_device_ex", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint]),
     ("ff_check", C.c_int, [_P, C.POINTER(Stats)]),
@@ -196,8 +201,9 @@ class Context:
         _ok(lib().ff_ctx_synchronize(self.h))
 
     def set_scatter(self, mode):
-        """'gather' (row gather, atomic-free, default) or 'atomic' (fp64 RED
-        after a zero-fill)."""
+        """'gather' (row gather, atomic-free, default), 'atomic' (fp64 RED
+        after a zero-fill) or 'auto' (the first device assembly of a (form,
+        pattern, mesh) times both and keeps the faster)."""
         _ok(lib().ff_ctx_set_scatter(self.h, SCATTER_MODE[mode]))
         self.scatter = mode
 
@@ -387,6 +393,15 @@ class Pattern:
         m = C.c_int(0)
         _ok(lib().ff_scatter_selected(form.h, self.h, flags, C.byref(m)))
         return SCATTER_NAME[m.value]
+
+    def calibrate_scatter(self, form, mesh, values_ptr, rhs_ptr, stream=None):
+        """Times the row gather and the atomic scatter on device buffers and
+        records the faster for 'auto': {gather_ms, atomic_ms, chosen}."""
+        t = ScatterTiming()
+        _ok(lib().ff_scatter_calibrate(form.h, mesh.h, self.h, C.c_void_p(values_ptr), C.c_void_p(rhs_ptr),
+                                       _stream(stream), C.byref(t)))
+        return {"gather_ms": t.gather_ms if t.gather_ms >= 0 else None, "atomic_ms": t.atomic_ms,
+                "chosen": SCATTER_NAME[t.chosen]}
 
     def close(self):
         if getattr(self, "h", None):

@@ -548,3 +548,38 @@ def test_jittered_permuted_mesh(ff, ctx, deg):
     assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
     ov, ob = po.assemble("helmholtz", 3, deg, 4, c, v, d, orp, oci, workers=8)
     assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
+
+
+@pytest.mark.parametrize("form,quad,gather_ok", [("poisson", 4, True), ("varcoef", 14, False)])
+def test_auto_scatter_is_the_measured_faster_one(ff, ctx, form, quad, gather_ok):
+    """North star (3): FF_SCATTER_AUTO_MODE times the row gather and the fp64
+    RED scatter on the caller's buffers and keeps the faster; the assembly it
+    leaves (and every later one) matches the oracle."""
+    import torch
+    n = 10
+    c, v, d, nd = _mesh(ff, 3, 2, n)
+    b, l = ff.named_form(form, 3)
+    f = ff.Form(ctx, 3, 2, b, l, quad_rule=quad)
+    m = ff.Mesh(ctx, 3, c, v, d, nd)
+    p = ff.Pattern(ctx, m)
+    ctx.set_scatter("auto")
+    try:
+        vals = torch.empty(p.nnz, dtype=torch.float64, device="cuda")
+        rhs = torch.empty(p.n_rows, dtype=torch.float64, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+        t = p.calibrate_scatter(f, m, vals.data_ptr(), rhs.data_ptr(), s)
+        assert t["atomic_ms"] > 0
+        if gather_ok:
+            assert t["gather_ms"] > 0
+            assert t["chosen"] == ("gather" if t["gather_ms"] <= t["atomic_ms"] else "atomic")
+        else:
+            assert t["gather_ms"] is None and t["chosen"] == "atomic"
+        assert p.scatter_for(f) == t["chosen"]
+        orp, oci = po.build_pattern(d, nd)
+        ov, ob = po.assemble(form, 3, 2, quad, c, v, d, orp, oci, workers=8)
+        torch.cuda.synchronize()
+        assert normwise(vals.cpu().numpy(), ov) <= TOL and normwise(rhs.cpu().numpy(), ob) <= TOL
+        v2, b2 = ff.assemble(f, m, p)  # later calls run the choice
+        assert normwise(v2, ov) <= TOL and normwise(b2, ob) <= TOL
+    finally:
+        ctx.set_scatter("gather")
