@@ -209,9 +209,11 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // 82.6 ms at config 5, run 43)
   if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
-  // element records bypass L1 allocation (streamed once per lane; -6 %, run 27)
-  // (vector forms read each record once per component pair: keep L1)
-  if (!std::getenv("FF_EINV_L1") && f->ncomp == 1) src = "#define FF_EINV_NA 1\n" + src;
+  // element records through L1: with records in first-touch order the lanes of
+  // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
+  // FF_EINV_NA=1 streams them past L1 (the round-1 default, -6 % before the
+  // first-touch order)
+  if (std::getenv("FF_EINV_NA") && f->ncomp == 1) src = "#define FF_EINV_NA 1\n" + src;
   for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
