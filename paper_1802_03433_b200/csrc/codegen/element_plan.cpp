@@ -459,9 +459,242 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
 }
 
 // ---------------------------------------------------------------------------
+// Pointwise, bilinear structure (scalar forms)
+//
+// The weak form is bilinear: a(u, v) = sum_{a,b} C_ab(x) U_a V_b with
+// U = (u, u_x, u_y[, u_z]) and V = (v, v_x, v_y[, v_z]), l(v) = L(x) v, the
+// C_ab = d2a / dU_a dV_b and L = dl/dv found symbolically (and checked at
+// random points). Per quadrature point (runtime loop, ascending q):
+//   x_q = X0 + J xi_q;  W_ab = w_q det J C_ab(x_q)  (only the nonzero C_ab)
+//   U_a(j): phi_j and the physical gradient G grad_ref phi_j (tables of the
+//           reference basis at the points, __constant__)
+//   P_b(j) = sum_a W_ab U_a(j);  K_ij += sum_b V_b(i) P_b(j);  b_i += w det L phi_i
+// i.e. per point a rank-(dim+1) update of the element matrix instead of every
+// entry's expanded integrand (config 4: ~10k instead of ~38k flops per
+// element). Rows go in blocks of <= 5 (accumulators in registers); P is
+// recomputed per block.
+
+namespace {
+
+bool is_zero_expr(const Expr& e) { return e.is_zero(); }
+
+void render_program(std::ostringstream& os, const MultiProgram& p, const std::string& prefix, const std::string& indent,
+                    std::int64_t& ops) {
+  auto r = [&](int k) { return prefix + std::to_string(k); };
+  for (std::size_t k = 0; k < p.code.size(); ++k) {
+    const Instr& in = p.code[k];
+    std::string rhs;
+    switch (in.op) {
+      case Op::LoadArg: rhs = p.arg_names[in.imm]; break;
+      case Op::LoadConst: rhs = double_literal(p.consts[in.imm]); break;
+      case Op::Add: rhs = r(in.a) + " + " + r(in.b); ++ops; break;
+      case Op::Sub: rhs = r(in.a) + " - " + r(in.b); ++ops; break;
+      case Op::Mul: rhs = r(in.a) + " * " + r(in.b); ++ops; break;
+      case Op::Div: rhs = r(in.a) + " / " + r(in.b); ops += 4; break;
+      case Op::Neg: rhs = "-" + r(in.a); break;
+      case Op::PowInt: rhs = "ff_powi(" + r(in.a) + ", " + std::to_string(in.imm) + ")"; ops += 8; break;
+      case Op::Sin: rhs = "sin(" + r(in.a) + ")"; ops += 20; break;
+      case Op::Cos: rhs = "cos(" + r(in.a) + ")"; ops += 20; break;
+      case Op::Sqrt: rhs = "sqrt(" + r(in.a) + ")"; ops += 4; break;
+    }
+    os << indent << "const double " << r(static_cast<int>(k)) << " = " << rhs << ";\n";
+  }
+}
+
+}  // namespace
+
+std::optional<ElementPlan> plan_point_bilinear(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
+  if (f.ncomp != 1 || !f.form_bilinear.valid() || !f.form_linear.valid() || std::getenv("FF_POINT_GENERIC"))
+    return std::nullopt;
+  const int dim = f.dim, n = f.n_local, nq = rule.size(), nu = dim + 1;
+  const char* un[4] = {"u", "u_x", "u_y", "u_z"};
+  const char* vn[4] = {"v", "v_x", "v_y", "v_z"};
+  const char* xn[3] = {"x", "y", "z"};
+  const std::set<std::string> coords(xn, xn + dim);
+  Expr C[4][4];
+  bool nz[4][4] = {};
+  std::vector<Expr> outs;
+  int idx[4][4];
+  for (int a = 0; a < nu; ++a)
+    for (int b = 0; b < nu; ++b) {
+      C[a][b] = diff(diff(f.form_bilinear, sym(un[a])), sym(vn[b]));
+      for (const std::string& s : free_symbols(C[a][b]))
+        if (!coords.count(s)) return std::nullopt;  // not bilinear in (U, V)
+      nz[a][b] = !is_zero_expr(C[a][b]);
+      idx[a][b] = -1;
+      if (nz[a][b]) {
+        idx[a][b] = static_cast<int>(outs.size());
+        outs.push_back(C[a][b]);
+      }
+    }
+  const Expr L = diff(f.form_linear, sym("v"));
+  for (const std::string& s : free_symbols(L))
+    if (!coords.count(s)) return std::nullopt;
+  const int iL = static_cast<int>(outs.size());
+  outs.push_back(L);
+  // the decomposition must reproduce the form (random points; exact for
+  // bilinear / linear forms up to rounding)
+  {
+    std::uint64_t rng = 0x2545F4914F6CDD1Dull;
+    auto rnd = [&]() {
+      rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+      return 0.25 + 0.5 * static_cast<double>(rng >> 11) / 9007199254740992.0;
+    };
+    for (int t = 0; t < 4; ++t) {
+      std::map<std::string, double> val;
+      for (int c = 0; c < 3; ++c) val[xn[c]] = rnd();
+      for (int a = 0; a < 4; ++a) val[un[a]] = rnd(), val[vn[a]] = rnd();
+      double ref = eval(f.form_bilinear, val), got = 0.0, scale = std::fabs(ref);
+      for (int a = 0; a < nu; ++a)
+        for (int b = 0; b < nu; ++b)
+          if (nz[a][b]) {
+            const double term = eval(C[a][b], val) * val[un[a]] * val[vn[b]];
+            got += term;
+            scale = std::max(scale, std::fabs(term));
+          }
+      if (std::fabs(got - ref) > 1e-12 * std::max(scale, 1e-300)) return std::nullopt;
+      const double lref = eval(f.form_linear, val), lgot = eval(L, val) * val["v"];
+      if (std::fabs(lgot - lref) > 1e-12 * std::max(std::fabs(lref), 1e-300)) return std::nullopt;
+    }
+  }
+  bool use_u[4] = {}, use_v[4] = {};
+  for (int a = 0; a < nu; ++a)
+    for (int b = 0; b < nu; ++b)
+      if (nz[a][b]) use_u[a] = use_v[b] = true;
+  // reference basis and gradients at the points
+  const std::vector<Expr> phi = fem::reference_shape_functions(dim, f.degree);
+  const Expr ref[3] = {sym("xi"), sym("eta"), sym("zeta")};
+  std::ostringstream pre;
+  pre << "__constant__ double ff_qp[" << nq << "][3] = { ";
+  for (int q = 0; q < nq; ++q)
+    pre << (q ? ", " : "") << "{" << double_literal(rule.points[q][0]) << ", " << double_literal(rule.points[q][1])
+        << ", " << double_literal(dim == 3 ? rule.points[q][2] : 0.0) << "}";
+  pre << "};\n__constant__ double ff_qw[" << nq << "] = {";
+  for (int q = 0; q < nq; ++q) pre << (q ? ", " : "") << double_literal(rule.weights[q]);
+  pre << "};\n__constant__ double ff_bphi[" << nq << "][" << n << "] = {";
+  std::vector<std::array<Expr, 3>> dphi(n);
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < dim; ++c) dphi[i][c] = diff(phi[i], ref[c]);
+  auto at = [&](int q) {
+    return std::map<std::string, double>{
+        {"xi", rule.points[q][0]}, {"eta", rule.points[q][1]}, {"zeta", dim == 3 ? rule.points[q][2] : 0.0}};
+  };
+  for (int q = 0; q < nq; ++q)
+    for (int i = 0; i < n; ++i) pre << (q || i ? ", " : "") << double_literal(eval(phi[i], at(q)));
+  pre << "};\n__constant__ double ff_bdphi[" << nq << "][" << n << "][" << dim << "] = {";
+  for (int q = 0; q < nq; ++q)
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < dim; ++c) pre << (q || i || c ? ", " : "") << double_literal(eval(dphi[i][c], at(q)));
+  pre << "};\n";
+
+  SymbolTable args;
+  for (int c = 0; c < dim; ++c) args.add(xn[c]);
+  const MultiProgram prog = lower_many(outs, args);
+  ElementPlan plan;
+  plan.strategy = Strategy::Pointwise;
+  plan.prelude = pre.str();
+  std::ostringstream os;
+  std::int64_t flops = 0;
+  const int nblk = (n + 4) / 5, R = (n + nblk - 1) / nblk;
+  const char* refname[3] = {"xi", "eta", "zeta"};
+  auto grad = [&](const std::string& base, int r) {  // (G grad_ref phi)_r from the table row `base`
+    std::string e;
+    for (int c = 0; c < dim; ++c)
+      e += (c ? " + " : "") + std::string("gG") + std::to_string(r) + std::to_string(c) + " * " + base + "[" +
+           std::to_string(c) + "]";
+    return e;
+  };
+  os << "  // element body: bilinear point updates, " << nq << "-point rule, rows in " << nblk << " block(s)\n";
+  for (int i0 = 0; i0 < n; i0 += R) {
+    const int i1 = std::min(n, i0 + R);
+    os << "  {  // rows [" << i0 << ", " << i1 << ")\n";
+    for (int i = i0; i < i1; ++i) {
+      os << "    double ff_b" << i << " = 0.0";
+      for (int j = 0; j < n; ++j) os << ", ff_a" << i << "_" << j << " = 0.0";
+      os << ";\n";
+    }
+    os << "#pragma unroll 1\n    for (int ff_q = 0; ff_q < " << nq << "; ++ff_q) {\n";
+    for (int c = 0; c < dim; ++c) os << "      const double " << refname[c] << " = ff_qp[ff_q][" << c << "];\n";
+    os << "      const double ff_w = ff_qw[ff_q] * gdet;\n";
+    for (int r = 0; r < dim; ++r) {
+      os << "      const double " << xn[r] << " = gX" << r;
+      for (int c = 0; c < dim; ++c) os << " + gJ" << r << c << " * " << refname[c];
+      os << ";\n";
+      flops += 2 * dim;
+    }
+    render_program(os, prog, "ff_c", "      ", flops);
+    for (int a = 0; a < nu; ++a)
+      for (int b = 0; b < nu; ++b)
+        if (nz[a][b]) {
+          os << "      const double ff_W" << a << b << " = ff_w * ff_c" << prog.results[idx[a][b]] << ";\n";
+          ++flops;
+        }
+    os << "      const double ff_L = ff_w * ff_c" << prog.results[iL] << ";\n";
+    ++flops;
+    // test side of the block's rows
+    for (int i = i0; i < i1; ++i) {
+      os << "      const double ff_v" << i << "_0 = ff_bphi[ff_q][" << i << "];\n";
+      for (int r = 0; r < dim; ++r)
+        if (use_v[r + 1]) {
+          os << "      const double ff_v" << i << "_" << r + 1 << " = " << grad("ff_bdphi[ff_q][" + std::to_string(i) + "]", r)
+             << ";\n";
+          flops += 2 * dim;
+        }
+    }
+    for (int j = 0; j < n; ++j) {
+      os << "      {\n        const double ff_u0 = ff_bphi[ff_q][" << j << "];\n";
+      for (int r = 0; r < dim; ++r)
+        if (use_u[r + 1]) {
+          os << "        const double ff_u" << r + 1 << " = " << grad("ff_bdphi[ff_q][" + std::to_string(j) + "]", r)
+             << ";\n";
+          flops += 2 * dim;
+        }
+      for (int b = 0; b < nu; ++b) {
+        if (!use_v[b]) continue;
+        std::string e;
+        for (int a = 0; a < nu; ++a)
+          if (nz[a][b]) {
+            e += (e.empty() ? "" : " + ") + std::string("ff_W") + std::to_string(a) + std::to_string(b) + " * ff_u" +
+                 std::to_string(a);
+            flops += 2;
+          }
+        os << "        const double ff_P" << b << " = " << e << ";\n";
+      }
+      for (int i = i0; i < i1; ++i) {
+        os << "        ff_a" << i << "_" << j << " += ";
+        bool first = true;
+        for (int b = 0; b < nu; ++b)
+          if (use_v[b]) {
+            os << (first ? "" : " + ") << "ff_v" << i << "_" << b << " * ff_P" << b;
+            first = false;
+            flops += 2;
+          }
+        os << ";\n";
+      }
+      os << "      }\n";
+    }
+    for (int i = i0; i < i1; ++i) {
+      os << "      ff_b" << i << " += ff_L * ff_v" << i << "_0;\n";
+      flops += 2;
+    }
+    os << "    }\n";
+    for (int i = i0; i < i1; ++i) {
+      for (int j = 0; j < n; ++j) os << "    FF_EMIT_A(" << i << ", " << j << ", ff_a" << i << "_" << j << ");\n";
+      os << "    FF_EMIT_B(" << i << ", ff_b" << i << ");\n";
+    }
+    os << "  }\n";
+  }
+  plan.n_unique_entries = n * n + n;
+  plan.flops = flops * nq;  // counted once per point inside the loop body
+  plan.body = os.str();
+  return plan;
+}
+
+// ---------------------------------------------------------------------------
 // Pointwise
 
 ElementPlan plan_pointwise(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
+  if (auto p = plan_point_bilinear(f, rule)) return *p;
   // A runtime quadrature loop per block of kRows element rows: the block's
   // integrands are lowered once with the reference coordinates as symbols
   // (CSE inside the block), evaluated at every point in ascending order, and

@@ -92,6 +92,7 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   }
   if (text.find("{{") != std::string::npos) throw CodegenError("unresolved placeholder");
   if (const char* v = std::getenv("FF_WAGG")) text = "#define FF_WAGG " + std::to_string(std::atoi(v) != 0) + "\n" + text;
+  if (std::getenv("FF_NO_BPAD")) text = "#define FF_NO_BPAD 1\n" + text;  // tuning knob (both modules)
   if (plan_out) *plan_out = std::move(plan);
   return text;
 }
@@ -203,6 +204,7 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
   std::ostringstream os;
   const int nkp = plan.n_kinv + (plan.n_kinv & 1);
   const int erec = (plan.n_kinv + n_local + 1) & ~1;
+  if (std::getenv("FF_NO_BPAD")) os << "#define FF_NO_BPAD 1\n";  // tuning knob (both modules)
   os << "// femforge-b200 class-specialised row gather (generated per (form, gather plan));\n"
         "// every class row stays in registers, indexed by compile-time slots.\n"
         "typedef long long ff_i64;\ntypedef int ff_i32;\n"
@@ -212,6 +214,8 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "#define FF_NFULL (FF_NKINV / 4)\n#define FF_PAIR_TAIL " << record_pair_tail(n_local) << "\n"
      << "#define FF_GTAIL (FF_NKINV % 4 == 0 ? 0 : ((FF_NKINV % 4 <= 2 && FF_PAIR_TAIL) ? 2 : 4))\n"
      << "#if FF_BS == 1\n#define FF_GSTORE (4 * FF_NFULL + FF_GTAIL)\n#else\n#define FF_GSTORE FF_GS\n#endif\n"
+     << "#if FF_BS == 1 && FF_GTAIL == 4 && !defined(FF_NO_BPAD)\n"
+        "#define FF_NBPAD ((4 - FF_NKINV % 4) < FF_NLOC ? (4 - FF_NKINV % 4) : FF_NLOC)\n#else\n#define FF_NBPAD 0\n#endif\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
      << class_stage_pitch(classes, 1, fused) << "\n"
@@ -249,7 +253,9 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   ff_load_inv(einv, n_elems, ee, t);
 #pragma unroll
   for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
-  b = ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)i * n_elems + ee);
+  // entries b_0 .. b_{FF_NBPAD-1} came with the invariants (chunk-tail padding)
+  b = i < FF_NBPAD ? t[FF_NKINV + (i < FF_NBPAD ? i : 0)]
+                   : ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)(i - FF_NBPAD) * n_elems + ee);
 }
 #define FF_PRE 8  // records of the next item prefetched while this item computes
 #ifndef FF_WUNROLL

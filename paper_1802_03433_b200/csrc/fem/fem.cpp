@@ -465,6 +465,8 @@ InstantiatedForm instantiate(const WeakForm& wf) {
       }
     fill_entries(dim, phi, g, wf, out.geo_bilinear, out.geo_linear);
   }
+  out.form_bilinear = wf.bilinear;
+  out.form_linear = wf.linear;
   return out;
 }
 

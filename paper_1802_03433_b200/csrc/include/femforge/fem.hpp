@@ -149,6 +149,9 @@ struct InstantiatedForm {
   std::vector<Expr> linear;    // n_local
   std::vector<Expr> geo_bilinear;
   std::vector<Expr> geo_linear;
+  // scalar forms: the weak form itself (over u, u_x.., v, v_x.., x, y, z),
+  // for the per-point bilinear planner; null for blocked forms
+  Expr form_bilinear, form_linear;
 };
 
 // Geometry symbols of the GPU element prologue: gJrc (Jacobian dx_r/dxi_c),
