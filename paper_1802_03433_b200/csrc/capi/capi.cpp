@@ -385,8 +385,21 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     const int64_t* irec = gp.citem_rec;
     const int32_t* crec = gp.crec;
     void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
-    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(32 * cw), args,
-                                     p->class_smem[c], sc),
+    // programmatic dependent launch after K2a on the same stream: the class
+    // CTAs fill K2a's last wave and load their item headers, then wait in
+    // griddepcontrol.wait for K2a (FF_PDL=0: plain stream order)
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(32 * cw);
+    lc.dynamicSmemBytes = p->class_smem[c];
+    lc.stream = sc;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    const char* pdl = std::getenv("FF_PDL");
+    lc.attrs = attr;
+    lc.numAttrs = (sc == s && !(pdl && std::atoi(pdl) == 0)) ? 1 : 0;
+    ffb::cuda_check(cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(p->class_kernel[c]), args),
                     "K2b (class row gather) launch");
   };
   auto fork = [&](cudaStream_t to) {

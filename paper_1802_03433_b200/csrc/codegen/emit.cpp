@@ -478,6 +478,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "    row1 = __ldg(citem_rows + w1 * 32 + lane);\n"
           "    r1 = __ldg(citem_rec + w1);\n"
           "  }\n"
+          "  // programmatic dependent launch: everything above reads only the plan;\n"
+          "  // the element records below are K2a's output (no-op without PDL)\n"
+          "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
           "  for (ff_i64 k = 0; FF_ITEM(k) < i1; ++k) {\n"
           "    const int cn = c1, rown = row1;\n"
           "    const ff_i32* recn = crec + r1 * 32 + lane;\n"
