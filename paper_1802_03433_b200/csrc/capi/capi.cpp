@@ -175,6 +175,13 @@ int class_cwarps(const ff_form* f) {
   return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
 }
 
+// Vector forms: item-CTAs per component-pair slab of the class grid (FF_CDWIN
+// knob; 1 = the pairs of one item on consecutive CTAs).
+int class_cdwin(const ff_form* f) {
+  const char* v = std::getenv("FF_CDWIN");
+  return f->ncomp > 1 && v ? std::max(1, std::atoi(v)) : 1;
+}
+
 // Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
 int class_ipw(const ff_form* f) {
   const char* v = std::getenv("FF_IPW");
@@ -208,6 +215,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
   // 82.6 ms at config 5, run 43)
   if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
+  src = "#define FF_CDWIN " + std::to_string(class_cdwin(f)) + "\n" + src;
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
   // element records through L1: with records in first-touch order the lanes of
   // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
@@ -372,10 +380,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     // FF_CWARPS warps x FF_IPW items per CTA; vector forms: one CTA per component pair
     const int cw = class_cwarps(f);
     const int nb = f->ncomp * f->ncomp;
-    const int64_t ctas = (i1 - i0 + cw * ipw - 1) / (cw * ipw);
-    // one round of items per warp: CTAs launch in item order, so the items in
-    // flight stay contiguous (a persistent grid looping over rounds measured
-    // 3.2-3.6 vs 2.09 ms at the north star: the warps drift apart)
+    const int cdwin = class_cdwin(f);
+    const int64_t ctas = ((i1 - i0 + cw * ipw - 1) / (cw * ipw) + cdwin - 1) / cdwin * cdwin;
     const unsigned grid = static_cast<unsigned>(ctas * nb);
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;
@@ -385,21 +391,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     const int64_t* irec = gp.citem_rec;
     const int32_t* crec = gp.crec;
     void* args[] = {&ginv, &ne_arg, &row_ptr, &d_values, &d_rhs, &icls, &irows, &irec, &crec, &i0, &i1};
-    // programmatic dependent launch after K2a on the same stream: the class
-    // CTAs fill K2a's last wave and load their item headers, then wait in
-    // griddepcontrol.wait for K2a (FF_PDL=0: plain stream order)
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(32 * cw);
-    lc.dynamicSmemBytes = p->class_smem[c];
-    lc.stream = sc;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    const char* pdl = std::getenv("FF_PDL");
-    lc.attrs = attr;
-    lc.numAttrs = (sc == s && !(pdl && std::atoi(pdl) == 0)) ? 1 : 0;
-    ffb::cuda_check(cudaLaunchKernelExC(&lc, reinterpret_cast<const void*>(p->class_kernel[c]), args),
+    ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->class_kernel[c]), dim3(grid), dim3(32 * cw), args,
+                                     p->class_smem[c], sc),
                     "K2b (class row gather) launch");
   };
   auto fork = [&](cudaStream_t to) {
