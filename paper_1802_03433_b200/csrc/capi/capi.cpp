@@ -175,13 +175,6 @@ int class_cwarps(const ff_form* f) {
   return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
 }
 
-// Vector forms: item-CTAs per component-pair slab of the class grid (FF_CDWIN
-// knob; 1 = the pairs of one item on consecutive CTAs).
-int class_cdwin(const ff_form* f) {
-  const char* v = std::getenv("FF_CDWIN");
-  return f->ncomp > 1 && v ? std::max(1, std::atoi(v)) : 1;
-}
-
 // Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
 int class_ipw(const ff_form* f) {
   const char* v = std::getenv("FF_IPW");
@@ -215,7 +208,6 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
   // 82.6 ms at config 5, run 43)
   if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
-  src = "#define FF_CDWIN " + std::to_string(class_cdwin(f)) + "\n" + src;
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
   // element records through L1: with records in first-touch order the lanes of
   // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
@@ -380,8 +372,7 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     // FF_CWARPS warps x FF_IPW items per CTA; vector forms: one CTA per component pair
     const int cw = class_cwarps(f);
     const int nb = f->ncomp * f->ncomp;
-    const int cdwin = class_cdwin(f);
-    const int64_t ctas = ((i1 - i0 + cw * ipw - 1) / (cw * ipw) + cdwin - 1) / cdwin * cdwin;
+    const int64_t ctas = (i1 - i0 + cw * ipw - 1) / (cw * ipw);
     const unsigned grid = static_cast<unsigned>(ctas * nb);
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;

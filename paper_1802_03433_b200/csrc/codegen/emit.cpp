@@ -310,9 +310,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
 #ifndef FF_CWARPS
 #define FF_CWARPS 4  // warps per CTA
 #endif
-#ifndef FF_CDWIN
-#define FF_CDWIN 1  // vector forms: item-CTAs per component-pair slab (1: pairs interleaved)
-#endif
+
 #ifndef FF_MINB_S
 #define FF_MINB_S 4  // CTAs per SM the register budgets are sized for
 #endif
@@ -452,14 +450,12 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
           "  double* st = ff_dsm + wid * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ";\n"
           "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ") + wid * 32;\n"
-          "  // vector forms: the grid is slabs of FF_CDWIN item-CTAs per component pair,\n"
-          "  // FF_NB slabs (one per pair) over the same items in a row: one code path per\n"
-          "  // CTA, consecutive CTAs on an SM run the same function (instruction cache),\n"
-          "  // and the pairs' stride-FF_BS writes to one CSR line meet in L2 within a\n"
-          "  // few waves; scalar forms: FF_NB = 1\n"
-          "  const unsigned ff_slab = blockIdx.x / (FF_CDWIN * FF_NB), ff_rem = blockIdx.x % (FF_CDWIN * FF_NB);\n"
-          "  const int cd = (int)(ff_rem / FF_CDWIN);\n"
-          "  const ff_i64 ff_cta = (ff_i64)ff_slab * FF_CDWIN + ff_rem % FF_CDWIN;\n"
+          "  // vector forms: FF_NB consecutive CTAs run the same items, one component\n"
+          "  // pair each (one code path per CTA; the items' records shared in L2, and\n"
+          "  // the pairs' stride-FF_BS writes to one CSR line meet in L2 -- slabs of\n"
+          "  // 16/64/256 CTAs per pair measured 62.5/63.4/71.7 vs 62.5 ms at config 5)\n"
+          "  const int cd = (int)(blockIdx.x % FF_NB);\n"
+          "  const ff_i64 ff_cta = blockIdx.x / FF_NB;\n"
           "  // items [first, last) of this warp (CTAs launch in item order, so the\n"
           "  // items in flight stay contiguous; a persistent grid measured 3.2-3.6 vs\n"
           "  // 2.09 ms at the north star)\n"

@@ -958,6 +958,20 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
         tfree();
         if (err != cudaSuccess) return done(err);
       }
+      // FF_PLAN_DUMP=<path> (analysis only): class items + element records
+      if (const char* dump = std::getenv("FF_PLAN_DUMP")) {
+        std::vector<int32_t> crec_h(out->n_crec);
+        cudaMemcpy(crec_h.data(), out->crec, out->n_crec * sizeof(int32_t), cudaMemcpyDeviceToHost);
+        if (FILE* fp = std::fopen(dump, "wb")) {
+          const int64_t hdr[3] = {nci, out->n_crec, ne};
+          std::fwrite(hdr, sizeof hdr, 1, fp);
+          std::fwrite(ic.data(), sizeof(int32_t), nci, fp);
+          std::fwrite(ir.data(), sizeof(int32_t), nci * 32, fp);
+          std::fwrite(irec.data(), sizeof(int64_t), nci + 1, fp);
+          std::fwrite(crec_h.data(), sizeof(int32_t), out->n_crec, fp);
+          std::fclose(fp);
+        }
+      }
     }
   }
   phase("class items");
