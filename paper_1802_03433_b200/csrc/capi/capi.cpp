@@ -172,7 +172,9 @@ void free_gather(ff_pattern* p) {
 
 int class_cwarps(const ff_form* f) {
   const char* v = std::getenv("FF_CWARPS");
-  return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
+  // vector forms: one warp per trial component (the CTA shares whole vector rows)
+  if (f->ncomp > 1) return f->ncomp;
+  return v ? std::max(1, std::min(8, std::atoi(v))) : 2;
 }
 
 // Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
@@ -224,7 +226,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[0], p->class_lib, "ff_gather_classes_s"), "class kernel");
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[1], p->class_lib, "ff_gather_classes_l"), "class kernel");
   for (int c = 0; c < 2; ++c) {
-    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused, class_cwarps(f));
+    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused, class_cwarps(f), f->ncomp);
     ffb::cuda_check(cudaKernelSetAttributeForDevice(p->class_kernel[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     p->class_smem[c], p->ctx->device),
                     "class kernel shared memory attribute");
@@ -369,11 +371,11 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     long long i0 = a, i1 = b;
     if (i1 <= i0) return;
     const int64_t ipw = class_ipw(f);
-    // FF_CWARPS warps x FF_IPW items per CTA; vector forms: one CTA per component pair
     const int cw = class_cwarps(f);
-    const int nb = f->ncomp * f->ncomp;
-    const int64_t ctas = (i1 - i0 + cw * ipw - 1) / (cw * ipw);
-    const unsigned grid = static_cast<unsigned>(ctas * nb);
+    // scalar: FF_CWARPS warps x FF_IPW items per CTA; vector: one item per CTA
+    // and test component (its warps are the trial components)
+    const unsigned grid = static_cast<unsigned>(f->ncomp > 1 ? (i1 - i0) * f->ncomp
+                                                               : (i1 - i0 + cw * ipw - 1) / (cw * ipw));
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;
     const int64_t* row_ptr = p->row_ptr;
