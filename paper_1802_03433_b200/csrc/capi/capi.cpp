@@ -177,6 +177,12 @@ int class_cwarps(const ff_form* f) {
   return v ? std::max(1, std::min(8, std::atoi(v))) : 2;
 }
 
+// Vector forms: CTAs per test-component slab of the class grid (FF_CCWIN knob).
+int class_ccwin() {
+  const char* v = std::getenv("FF_CCWIN");
+  return v ? std::max(1, std::atoi(v)) : 1024;
+}
+
 // Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
 int class_ipw(const ff_form* f) {
   const char* v = std::getenv("FF_IPW");
@@ -210,6 +216,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
   // 82.6 ms at config 5, run 43)
   if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
+  src = "#define FF_CCWIN " + std::to_string(class_ccwin()) + "\n" + src;
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
   // element records through L1: with records in first-touch order the lanes of
   // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
@@ -374,7 +381,8 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     const int cw = class_cwarps(f);
     // scalar: FF_CWARPS warps x FF_IPW items per CTA; vector: one item per CTA
     // and test component (its warps are the trial components)
-    const unsigned grid = static_cast<unsigned>(f->ncomp > 1 ? (i1 - i0) * f->ncomp
+    const int64_t ccwin = class_ccwin();
+    const unsigned grid = static_cast<unsigned>(f->ncomp > 1 ? (i1 - i0 + ccwin - 1) / ccwin * ccwin * f->ncomp
                                                                : (i1 - i0 + cw * ipw - 1) / (cw * ipw));
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;

@@ -314,6 +314,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   }
   __syncwarp();
 }
+#ifndef FF_CCWIN
+#define FF_CCWIN 1024  // vector forms: CTAs per test-component slab of the class grid
+#endif
 // vector forms: barrier of the CTA's FF_BS warps (one per trial component)
 __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"(32 * FF_BS) : "memory"); }
 #ifndef FF_IPW
@@ -397,7 +400,9 @@ __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"
       os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
     else if (dd == 0)  // the CTA's FF_BS warps share the item's rows: vector row FF_BS * row + cc
       os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len << " : -1;\n";
-    const int depth = bs == 1 ? 8 : (std::getenv("FF_VDEPTH") ? std::max(1, std::atoi(std::getenv("FF_VDEPTH"))) : 2);
+    // record loads in flight per batch (registers: depth x the record size)
+    const char* dk = bs == 1 ? std::getenv("FF_SDEPTH") : std::getenv("FF_VDEPTH");
+    const int depth = dk ? std::max(1, std::atoi(dk)) : (bs == 1 ? 8 : 2);
     for (int t0 = 0; t0 < k.steps; t0 += depth) {
       const int t1 = std::min(k.steps, t0 + depth);
       os << "  {\n";
@@ -490,8 +495,11 @@ __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"
           "  // shared tile of whole vector rows, written out together\n"
           "  st = ff_dsm;\n"
           "  sr = (ff_i64*)(ff_dsm + 32 * FF_VP);\n"
-          "  const int cd = (int)(blockIdx.x % FF_BS) * FF_BS + wid;\n"
-          "  const ff_i64 ff_cta = blockIdx.x / FF_BS;\n"
+          "  // slabs of FF_CCWIN consecutive CTAs share the test component, so an\n"
+          "  // SM's resident CTAs run FF_BS class functions, not FF_BS^2\n"
+          "  const unsigned ff_slab = blockIdx.x / (FF_CCWIN * FF_BS), ff_rem = blockIdx.x % (FF_CCWIN * FF_BS);\n"
+          "  const int cd = (int)(ff_rem / FF_CCWIN) * FF_BS + wid;\n"
+          "  const ff_i64 ff_cta = (ff_i64)ff_slab * FF_CCWIN + ff_rem % FF_CCWIN;\n"
           "#else\n"
           "  const int cd = 0;\n"
           "  const ff_i64 ff_cta = blockIdx.x;\n"
