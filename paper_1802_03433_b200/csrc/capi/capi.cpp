@@ -172,15 +172,7 @@ void free_gather(ff_pattern* p) {
 
 int class_cwarps(const ff_form* f) {
   const char* v = std::getenv("FF_CWARPS");
-  // vector forms: one warp per trial component (the CTA shares whole vector rows)
-  if (f->ncomp > 1) return f->ncomp;
-  return v ? std::max(1, std::min(8, std::atoi(v))) : 2;
-}
-
-// Vector forms: CTAs per test-component slab of the class grid (FF_CCWIN knob).
-int class_ccwin() {
-  const char* v = std::getenv("FF_CCWIN");
-  return v ? std::max(1, std::atoi(v)) : 1024;
+  return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
 }
 
 // Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
@@ -216,7 +208,6 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
   // 82.6 ms at config 5, run 43)
   if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
-  src = "#define FF_CCWIN " + std::to_string(class_ccwin()) + "\n" + src;
   // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
   // element records through L1: with records in first-touch order the lanes of
   // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
@@ -233,7 +224,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[0], p->class_lib, "ff_gather_classes_s"), "class kernel");
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[1], p->class_lib, "ff_gather_classes_l"), "class kernel");
   for (int c = 0; c < 2; ++c) {
-    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused, class_cwarps(f), f->ncomp);
+    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused, class_cwarps(f));
     ffb::cuda_check(cudaKernelSetAttributeForDevice(p->class_kernel[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     p->class_smem[c], p->ctx->device),
                     "class kernel shared memory attribute");
@@ -378,12 +369,11 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
     long long i0 = a, i1 = b;
     if (i1 <= i0) return;
     const int64_t ipw = class_ipw(f);
+    // FF_CWARPS warps x FF_IPW items per CTA; vector forms: one CTA per component pair
     const int cw = class_cwarps(f);
-    // scalar: FF_CWARPS warps x FF_IPW items per CTA; vector: one item per CTA
-    // and test component (its warps are the trial components)
-    const int64_t ccwin = class_ccwin();
-    const unsigned grid = static_cast<unsigned>(f->ncomp > 1 ? (i1 - i0 + ccwin - 1) / ccwin * ccwin * f->ncomp
-                                                               : (i1 - i0 + cw * ipw - 1) / (cw * ipw));
+    const int nb = f->ncomp * f->ncomp;
+    const int64_t ctas = (i1 - i0 + cw * ipw - 1) / (cw * ipw);
+    const unsigned grid = static_cast<unsigned>(ctas * nb);
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;
     const int64_t* row_ptr = p->row_ptr;

@@ -186,15 +186,6 @@ std::vector<int> class_step_order(const RowClass& k, int n_local) {
   return best;
 }
 
-// Vector forms: pitch of the shared tile of whole vector rows (FF_BS x the
-// longest class row, odd: conflict-free lane-row stores).
-int class_vector_pitch(const std::vector<RowClass>& classes, int bs) {
-  if (bs <= 1) return 1;
-  int m = 1;
-  for (const auto& c : classes) m = std::max(m, c.len);
-  return (bs * m) | 1;
-}
-
 int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused) {
   int m = 1;
   for (const auto& c : classes)
@@ -228,8 +219,6 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
      << class_stage_pitch(classes, 1, fused) << "\n"
-     << "// vector forms: staging pitch of a whole vector row (odd)\n#define FF_VP " << class_vector_pitch(classes, bs)
-     << "\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
@@ -314,11 +303,6 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   }
   __syncwarp();
 }
-#ifndef FF_CCWIN
-#define FF_CCWIN 1024  // vector forms: CTAs per test-component slab of the class grid
-#endif
-// vector forms: barrier of the CTA's FF_BS warps (one per trial component)
-__device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"(32 * FF_BS) : "memory"); }
 #ifndef FF_IPW
 #define FF_IPW 2  // consecutive items per warp
 #endif
@@ -355,10 +339,7 @@ __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"
     // staging position of every slot: the slot index when the row fits one
     // staging row, else its finalisation rank (chunks of 32 written out as
     // soon as they are complete, lanes in ascending slot order inside a chunk)
-    // vector forms stage whole vector rows (FF_BS x len values, the CTA's
-    // FF_BS warps each fill one trial component) -- never chunked
-    const bool vrow = bs > 1;
-    const bool chunked = !vrow && k.len > 33;
+    const bool chunked = k.len > 33;
     // fin: finalisation rank (chunk = fin / 32); pos: position inside the
     // chunk's staging row (ascending slot order)
     std::vector<int> pos(k.len), fin(k.len), slot_at(k.len);
@@ -396,13 +377,8 @@ __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"
     if (dd == 0) os << "  double bs = 0.0;\n";
     for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
     os << ";\n";
-    if (!vrow)
-      os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
-    else if (dd == 0)  // the CTA's FF_BS warps share the item's rows: vector row FF_BS * row + cc
-      os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len << " : -1;\n";
-    // record loads in flight per batch (registers: depth x the record size)
-    const char* dk = bs == 1 ? std::getenv("FF_SDEPTH") : std::getenv("FF_VDEPTH");
-    const int depth = dk ? std::max(1, std::atoi(dk)) : (bs == 1 ? 8 : 2);
+    os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
+    const int depth = bs == 1 ? 8 : (std::getenv("FF_VDEPTH") ? std::max(1, std::atoi(std::getenv("FF_VDEPTH"))) : 2);
     for (int t0 = 0; t0 < k.steps; t0 += depth) {
       const int t1 = std::min(k.steps, t0 + depth);
       os << "  {\n";
@@ -418,12 +394,7 @@ __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"
           const int sl = k.slots[q * n_local + j];
           os << " a" << sl << (first[sl] == t ? " = v[" : " += v[") << j * bs + dd << "];";
         }
-        if (vrow) {
-          for (int j = 0; j < n_local; ++j) {
-            const int sl = k.slots[q * n_local + j];
-            if (last[sl] == t) os << " st[lane * FF_VP + " << bs * sl + dd << "] = a" << sl << ";";
-          }
-        } else if (!chunked) {
+        if (!chunked) {
           for (int j = 0; j < n_local; ++j) {
             const int sl = k.slots[q * n_local + j];
             if (last[sl] == t) os << " st[lane * " << sp << " + " << sl << "] = a" << sl << ";";
@@ -450,17 +421,7 @@ __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"
     }
     // write-out through the staging rows (consecutive lanes = consecutive CSR
     // values of one row)
-    if (vrow) {
-      // all FF_BS trial components staged: the CTA writes the 32 vector rows,
-      // each FF_BS x len contiguous values (full lines, no partial-sector merges)
-      os << "  ff_vbar();\n"
-         << "  for (int m = 0; m < 32; ++m) {\n"
-         << "    const ff_i64 rb = sr[m];\n"
-         << "    if (rb >= 0)\n"
-         << "      for (int t = threadIdx.x; t < " << bs * k.len << "; t += 32 * FF_BS) __stcs(values + rb + t, st[m * FF_VP + t]);\n"
-         << "  }\n"
-         << "  ff_vbar();\n";
-    } else if (!chunked)
+    if (!chunked)
       for (int q0 = 0; q0 < k.len; q0 += 32)
         os << "  ff_writeout(st + " << q0 << ", " << sp << ", sr, lane, " << std::min(32, k.len - q0) << ", " << q0
            << ", values);\n";
@@ -489,29 +450,16 @@ __device__ __forceinline__ void ff_vbar() { asm volatile("bar.sync 1, %0;" ::"r"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
           "  double* st = ff_dsm + wid * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ";\n"
           "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * 32 * " << (longrows ? "FF_SP_L" : "FF_SP_S") << ") + wid * 32;\n"
-          "#if FF_BS > 1\n"
-          "  // vector forms: one item per CTA of FF_BS warps -- test component cc =\n"
-          "  // blockIdx % FF_BS, trial component dd = warp; the warps fill one\n"
-          "  // shared tile of whole vector rows, written out together\n"
-          "  st = ff_dsm;\n"
-          "  sr = (ff_i64*)(ff_dsm + 32 * FF_VP);\n"
-          "  // slabs of FF_CCWIN consecutive CTAs share the test component, so an\n"
-          "  // SM's resident CTAs run FF_BS class functions, not FF_BS^2\n"
-          "  const unsigned ff_slab = blockIdx.x / (FF_CCWIN * FF_BS), ff_rem = blockIdx.x % (FF_CCWIN * FF_BS);\n"
-          "  const int cd = (int)(ff_rem / FF_CCWIN) * FF_BS + wid;\n"
-          "  const ff_i64 ff_cta = (ff_i64)ff_slab * FF_CCWIN + ff_rem % FF_CCWIN;\n"
-          "#else\n"
-          "  const int cd = 0;\n"
-          "  const ff_i64 ff_cta = blockIdx.x;\n"
-          "#endif\n"
+          "  // vector forms: FF_NB consecutive CTAs run the same items, one component\n"
+          "  // pair each (one code path per CTA; the items' records shared in L2, and\n"
+          "  // the pairs' stride-FF_BS writes to one CSR line meet in L2 -- slabs of\n"
+          "  // 16/64/256 CTAs per pair measured 62.5/63.4/71.7 vs 62.5 ms at config 5)\n"
+          "  const int cd = (int)(blockIdx.x % FF_NB);\n"
+          "  const ff_i64 ff_cta = blockIdx.x / FF_NB;\n"
           "  // items [first, last) of this warp (CTAs launch in item order, so the\n"
           "  // items in flight stay contiguous; a persistent grid measured 3.2-3.6 vs\n"
           "  // 2.09 ms at the north star)\n"
-          "#if FF_BS > 1\n"
-          "  const ff_i64 first = i0 + ff_cta;  // FF_IPW = 1\n"
-          "#else\n"
           "  const ff_i64 first = i0 + (ff_cta * FF_CWARPS + wid) * FF_IPW;\n"
-          "#endif\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
           "  // (the record array is padded by FF_PRE steps, so the loads need no bound)\n"

@@ -158,13 +158,7 @@ std::vector<int> class_step_order(const RowClass& k, int n_local);
 // longest class row).
 int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused);
 // Dynamic shared memory of class kernel `kernel` (4 warps).
-int class_vector_pitch(const std::vector<RowClass>& classes, int bs);
-// Dynamic shared memory of a class kernel: scalar forms, one staging tile
-// [32][pitch] + 32 row offsets per warp; vector forms (bs > 1), one tile of
-// whole vector rows [32][bs * longest row] + 32 row offsets per CTA.
-inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused, int warps = 4,
-                              int bs = 1) {
-  if (bs > 1) return 32 * class_vector_pitch(classes, bs) * 8 + 32 * 8;
+inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused, int warps = 4) {
   return warps * 32 * class_stage_pitch(classes, kernel, fused) * 8 + warps * 32 * 8;
 }
 
