@@ -86,7 +86,17 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-FP64_PEAK_TFLOPS = 37.0   # nominal HGX B200 fp64
+def fp64_peak():
+    """Measured fp64 FMA peak (tools/microbench/fp64_peak.cu on a B200,
+    profiles/r2_fp64_peak.json), else the nominal 37 TFLOP/s."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_fp64_peak.json")) as f:
+            return float(json.load(f)["fp64_tflops"]), "measured (profiles/r2_fp64_peak.json, DFMA microbench)"
+    except Exception:
+        return 37.0, "nominal B200 fp64"
+
+
+FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = fp64_peak()
 
 
 def model_flops(cfg):
@@ -526,13 +536,18 @@ def main():
                    "nvrtc_compile_ms": compile_ms, "strategy": info["strategy"], "registers": info["registers"],
                    "flops_per_element": info["flops_per_element"],
                    "hbm_gbs_step": B / (step_ms * 1e-3) / 1e9},
-        "roofline": ({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak}
+        # the binding roofline, and (C3/NS sit at the ridge) the
+        # other fraction beside it; flops = the SURVEY §8d model
+        "roofline": ({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                      "fp64": {"achieved_tflops": F / (kern_ms * 1e-3) / 1e12, "peak_tflops": FP64_PEAK_TFLOPS,
+                               "frac": F / (kern_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                               "flops_per_element_model": model_flops(cfg), "peak_source": FP64_PEAK_SOURCE}}
                      if info["flops_per_element"] * vconn_l.shape[0] / B <= FP64_PEAK_TFLOPS * 1e3 / peak else
                      {"bound": "fp64", "achieved": F / (kern_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
                       "unit": "TFLOP/s", "frac": F / (kern_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                      "peak_note": "nominal B200 fp64 (no measured fp64 peak in MEASURED_PEAKS.json); "
-                                   "flops = SURVEY.md §8d model", "flops_per_element_model": model_flops(cfg),
-                      "hbm_gbs": achieved}) | {
+                      "peak_note": FP64_PEAK_SOURCE + "; flops = SURVEY.md §8d model",
+                      "flops_per_element_model": model_flops(cfg),
+                      "hbm": {"achieved_gbs": achieved, "peak_gbs": peak, "frac": achieved / peak}}) | {
                      "traffic": traffic,
                      "kernel": KERNEL_DESC[scatter],
                      "bytes_per_launch": int(B), "peak_source": peak_src},

@@ -823,7 +823,7 @@ int ff_mesh_set_components(ff_mesh* m, int ncomp) {
   return guarded([&] {
     require(m && ncomp >= 1 && ncomp <= 3, "invalid argument");
     m->bs = ncomp;
-    ++m->generation;
+    m->generation = next_generation();  // process-wide: no plan keyed on an old value can match
   });
 }
 
