@@ -430,10 +430,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
     }  // component pairs
   };
   for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
-  os << "__constant__ int ff_csteps[" << std::max<std::size_t>(classes.size(), 1) << "] = {";
-  for (std::size_t c = 0; c < classes.size(); ++c) os << (c ? ", " : "") << classes[c].steps;
-  if (classes.empty()) os << "0";
-  os << "};\n";
+
   auto kernel = [&](const char* name, bool longrows) {
     os << "// items of one launch: FF_IPW consecutive items per warp, CTAs in item order;\n"
           "// items are sorted by (Morton window, class): a CTA runs one class (small\n"
@@ -462,13 +459,15 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  const ff_i64 first = i0 + (ff_cta * FF_CWARPS + wid) * FF_IPW;\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
-          "  // (the record array is padded by FF_PRE steps, so the loads need no bound)\n"
+          "  // (the record array is padded by FF_PRE steps, so the loads need no bound;\n"
+          "  // they do not wait for the item's class either: a class function reads\n"
+          "  // only its own steps)\n"
           "  int c = __ldg(citem_class + first);\n"
           "  int row = __ldg(citem_rows + first * 32 + lane);\n"
           "  const ff_i32* rec = crec + __ldg(citem_rec + first) * 32 + lane;\n"
           "  int ep[FF_PRE];\n"
           "#pragma unroll\n"
-          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = u < ff_csteps[c] ? __ldcs(rec + u * 32) : -1;\n"
+          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(rec + u * 32);  // (steps past the item's: unused)\n"
           "  ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
           "#if FF_IPW > 1\n"
           "  // two-stage item pipeline: while item w computes, the records and row\n"
@@ -492,7 +491,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "    ff_i64 rbegn = 0;\n"
           "    if (w + 1 < last) {\n"
           "#pragma unroll\n"
-          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = u < ff_csteps[cn] ? __ldcs(recn + u * 32) : -1;\n"
+          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = __ldcs(recn + u * 32);\n"
           "      rbegn = rown >= 0 ? __ldg(row_ptr + rown) : 0;\n"
           "    }\n"
           "    if (w + 2 < last) {\n"
