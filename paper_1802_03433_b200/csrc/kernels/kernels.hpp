@@ -72,9 +72,6 @@ cudaError_t validate_mesh(const double* d_coords, int dim, int64_t nv, const int
 cudaError_t copy_compare(const int32_t* d_src, int32_t* d_dst, int64_t n, unsigned long long* d_diff, int sm_count,
                          cudaStream_t s);
 
-// Order-independent 64-bit content hash of n int32 values (sum of mixed
-// (index, value) pairs), written to *d_out.
-cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_out, int sm_count, cudaStream_t s);
 
 // Block expansion of a scalar CSR: row bs*n + c holds columns bs*m + d of every
 // scalar column m of row n (d = 0..bs-1), sorted. rp_v [bs*n_rows + 1].

@@ -502,23 +502,6 @@ __global__ void fill_records(const int32_t* __restrict__ erank, const int32_t* _
   }
 }
 
-__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
-  x ^= x >> 33;
-  x *= 0xff51afd7ed558ccdull;
-  x ^= x >> 33;
-  x *= 0xc4ceb9fe1a85ec53ull;
-  return x ^ (x >> 33);
-}
-
-__global__ void hash_kernel(const int32_t* __restrict__ a, int64_t n, unsigned long long* __restrict__ out) {
-  unsigned long long h = 0;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    h += mix64((static_cast<unsigned long long>(t) << 32) ^ static_cast<uint32_t>(a[t]));
-  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
-}
-
 int grid_for(int64_t n, int sm_blocks) {
   const int64_t g = (n + kThreads - 1) / kThreads;
   return static_cast<int>(g < sm_blocks ? (g < 1 ? 1 : g) : sm_blocks);
@@ -1074,12 +1057,6 @@ cudaError_t expand_block_pattern(const int64_t* rp_s, const int32_t* ci_s, int64
                                  int32_t* ci_v, int sm_count, cudaStream_t s) {
   if (n_rows == 0) return cudaMemsetAsync(rp_v, 0, sizeof(int64_t), s);
   expand_block_kernel<<<grid_for(n_rows, sm_count * 8), kThreads, 0, s>>>(rp_s, ci_s, n_rows, bs, rp_v, ci_v);
-  return cudaGetLastError();
-}
-
-cudaError_t content_hash(const int32_t* d_a, int64_t n, unsigned long long* d_out, int sm_count, cudaStream_t s) {
-  cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s);
-  if (n > 0) hash_kernel<<<grid_for(n, sm_count * 8), kThreads, 0, s>>>(d_a, n, d_out);
   return cudaGetLastError();
 }
 
