@@ -175,10 +175,11 @@ int class_cwarps(const ff_form* f) {
   return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
 }
 
-// Items per warp of the class kernels (FF_IPW knob; 2 scalar, 1 vector forms).
+// Items per warp of the class kernels (FF_IPW knob; 1: measured best for
+// scalar and vector forms).
 int class_ipw(const ff_form* f) {
   const char* v = std::getenv("FF_IPW");
-  return v ? std::max(1, std::atoi(v)) : (f->ncomp > 1 ? 1 : 2);
+  return v ? std::max(1, std::atoi(v)) : 1;
 }
 
 // NVRTC-compiles the class-specialised gather kernels of (form, plan).
@@ -203,7 +204,11 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp);
   // register budget: 12 warps/SM (168 registers) whatever the CTA size
-  if (fused && !std::getenv("FF_MINB_S")) src = "#define FF_MINB_S " + std::to_string(12 / class_cwarps(f)) + "\n" + src;
+  // register budget: 14 warps/SM for scalar forms (one item per warp: no
+  // carried item state; NS 2.013 vs 2.038 ms at 12 warps, 2.053 with two items
+  // per warp), 12 for vector forms
+  if (fused && !std::getenv("FF_MINB_S"))
+    src = "#define FF_MINB_S " + std::to_string((f->ncomp > 1 ? 12 : 14) / class_cwarps(f)) + "\n" + src;
   if (!std::getenv("FF_CWARPS")) src = "#define FF_CWARPS " + std::to_string(class_cwarps(f)) + "\n" + src;
   // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
   // 82.6 ms at config 5, run 43)
