@@ -177,7 +177,7 @@ int class_cwarps(const ff_form* f) {
 
 // Items per warp of the class kernels (FF_IPW knob; 1: measured best for
 // scalar and vector forms).
-int class_ipw(const ff_form* f) {
+int class_ipw(const ff_form*) {
   const char* v = std::getenv("FF_IPW");
   return v ? std::max(1, std::atoi(v)) : 1;
 }
@@ -203,7 +203,6 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
   const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp);
-  // register budget: 12 warps/SM (168 registers) whatever the CTA size
   // register budget: 14 warps/SM for scalar forms (one item per warp: no
   // carried item state; NS 2.013 vs 2.038 ms at 12 warps, 2.053 with two items
   // per warp), 12 for vector forms
