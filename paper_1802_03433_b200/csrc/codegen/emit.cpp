@@ -378,7 +378,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
     for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
     os << ";\n";
     os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
-    const int depth = bs == 1 ? 8 : (std::getenv("FF_VDEPTH") ? std::max(1, std::atoi(std::getenv("FF_VDEPTH"))) : 2);
+    // record loads in flight per batch (registers: depth x the record size)
+    const char* dk = bs == 1 ? std::getenv("FF_SDEPTH") : std::getenv("FF_VDEPTH");
+    const int depth = dk ? std::max(1, std::atoi(dk)) : (bs == 1 ? 8 : 2);
     for (int t0 = 0; t0 < k.steps; t0 += depth) {
       const int t1 = std::min(k.steps, t0 + depth);
       os << "  {\n";
