@@ -196,13 +196,14 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
     r.steps = c.steps;
     r.local = c.local;
     r.slots = c.slots;
+    r.order = c.order;  // the plan laid the records out in this order
     rc.push_back(std::move(r));
   }
   const auto t0 = std::chrono::steady_clock::now();
   // one fused kernel for every class unless FF_SPLIT_CLASSES:
   // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
   const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
-  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp);
+  std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp, p->gather.pre_steps);
   // register budget: 14 warps/SM for scalar forms (one item per warp: no
   // carried item state; NS 2.013 vs 2.038 ms at 12 warps, 2.053 with two items
   // per warp), 12 for vector forms
@@ -264,13 +265,24 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
     bbox[c] = lo;
     bbox[3 + c] = hi;
   }
+  // the code generator's step order of each class: the plan lays the class
+  // items' records out in it
+  const int n_local_scalar = m->k;
+  const ffb::kernels::ClassOrderFn order_fn = [n_local_scalar](const ffb::kernels::GatherPlan::Class& c) {
+    codegen::RowClass r;
+    r.len = c.len;
+    r.steps = c.steps;
+    r.local = c.local;
+    r.slots = c.slots;
+    return codegen::class_step_order(r, n_local_scalar);
+  };
   const cudaError_t e = ffb::kernels::build_gather_plan(m->coords, m->vconn, m->dim, bbox, m->dconn, m->ne, m->k, p->rb,
                                                         p->re - p->rb, p->row_ptr, static_cast<const uint8_t*>(p->slots),
                                                         4096, ctx->sm_count, ctx->stream, &p->gather,
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
-                                                        std::getenv("FF_SPLIT_CLASSES") != nullptr);
+                                                        std::getenv("FF_SPLIT_CLASSES") != nullptr, &order_fn);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");

@@ -195,7 +195,10 @@ int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fus
 }
 
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes, bool fused,
-                              int bs) {
+                              int bs, int pre) {
+  if (pre < 1 || pre > 8) throw CodegenError("class source: record prefix must be 1..8 steps");
+  for (const auto& c : classes)
+    if (c.steps < pre) throw CodegenError("class source: a class has fewer steps than the record prefix");
   if (plan.n_kinv <= 0) throw CodegenError("row classes need a reference-tensor plan");
   if (bs < 1 || n_local % bs) throw CodegenError("class source: bad component count");
   // classes are over (node) rows with nsc slots per incidence; vector forms
@@ -205,6 +208,7 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
   const int nkp = plan.n_kinv + (plan.n_kinv & 1);
   const int erec = (plan.n_kinv + n_local + 1) & ~1;
   if (std::getenv("FF_NO_BPAD")) os << "#define FF_NO_BPAD 1\n";  // tuning knob (both modules)
+  os << "#define FF_PRE " << pre << "\n";
   os << "// femforge-b200 class-specialised row gather (generated per (form, gather plan));\n"
         "// every class row stays in registers, indexed by compile-time slots.\n"
         "typedef long long ff_i64;\ntypedef int ff_i32;\n"
@@ -257,7 +261,7 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   b = i < FF_NBPAD ? t[FF_NKINV + (i < FF_NBPAD ? i : 0)]
                    : ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)(i - FF_NBPAD) * n_elems + ee);
 }
-#define FF_PRE 8  // records of the next item prefetched while this item computes
+// FF_PRE: record ids of an item loaded with its header (the plan's pre_steps)
 #ifndef FF_WUNROLL
 #define FF_WUNROLL 32  // write-out loop unroll (NS 2.484 vs 2.514 ms with 4, run 94)
 #endif
@@ -328,7 +332,9 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
     // one pass over the incidences in class_step_order: each element record
     // is loaded once; a slot's register opens at its first contribution and
     // goes to the staging row after its last one
-    const std::vector<int> order = class_step_order(k, n_local);
+    // the plan lays the items' records out in this order (RowClass::order);
+    // record position t holds template step order[t]
+    const std::vector<int> order = k.order.empty() ? class_step_order(k, n_local) : k.order;
     std::vector<int> first(k.len, -1), last(k.len, -1);
     for (int t = 0; t < k.steps; ++t)
       for (int j = 0; j < n_local; ++j) {
@@ -368,11 +374,11 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "    double* __restrict__ st, ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row,\n"
           "    double* __restrict__ values, double* __restrict__ rhs) {\n"
           "  int e[" << std::max(k.steps, 1) << "];\n";
-    for (int q = 0; q < k.steps; ++q) {
-      if (q < 8)
-        os << "  e[" << q << "] = ep[" << q << "];\n";
+    for (int t = 0; t < k.steps; ++t) {
+      if (t < pre)
+        os << "  e[" << order[t] << "] = ep[" << t << "];\n";
       else
-        os << "  e[" << q << "] = __ldcs(rec + " << q * 32 << ");\n";
+        os << "  e[" << order[t] << "] = __ldcs(rec + " << (t - pre) * 32 << ");\n";
     }
     if (dd == 0) os << "  double bs = 0.0;\n";
     for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
@@ -461,15 +467,15 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  const ff_i64 first = i0 + (ff_cta * FF_CWARPS + wid) * FF_IPW;\n"
           "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
           "  if (first >= last) return;\n"
-          "  // (the record array is padded by FF_PRE steps, so the loads need no bound;\n"
-          "  // they do not wait for the item's class either: a class function reads\n"
-          "  // only its own steps)\n"
+          "  // the item's first FF_PRE record ids sit at a position computable from the\n"
+          "  // item index, so they load together with the item header (every class\n"
+          "  // has >= FF_PRE steps); its other steps follow from citem_rec\n"
           "  int c = __ldg(citem_class + first);\n"
           "  int row = __ldg(citem_rows + first * 32 + lane);\n"
           "  const ff_i32* rec = crec + __ldg(citem_rec + first) * 32 + lane;\n"
           "  int ep[FF_PRE];\n"
           "#pragma unroll\n"
-          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(rec + u * 32);  // (steps past the item's: unused)\n"
+          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(crec + (first * FF_PRE + u) * 32 + lane);\n"
           "  ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
           "#if FF_IPW > 1\n"
           "  // two-stage item pipeline: while item w computes, the records and row\n"
@@ -493,7 +499,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "    ff_i64 rbegn = 0;\n"
           "    if (w + 1 < last) {\n"
           "#pragma unroll\n"
-          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = __ldcs(recn + u * 32);\n"
+          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = __ldcs(crec + ((w + 1) * FF_PRE + u) * 32 + lane);\n"
           "      rbegn = rown >= 0 ? __ldg(row_ptr + rown) : 0;\n"
           "    }\n"
           "    if (w + 2 < last) {\n"

@@ -145,7 +145,10 @@ struct RowClass {
   int steps = 0;                     // incidences
   std::vector<int> local;            // [steps] local index i of each incidence
   std::vector<std::uint8_t> slots;   // [steps][n_local] slot of column dof[j] in the row
+  std::vector<int> order;            // processing order of the steps (empty: class_step_order)
 };
+// Incidence order of a class that keeps few row slots open at once.
+std::vector<int> class_step_order(const RowClass& k, int n_local);
 
 // Whether the plan's kernels include the row gather (K2a + generic K2b).
 int record_pair_tail(int n_local);
@@ -165,8 +168,10 @@ inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, 
 // NVRTC translation unit with ff_gather_classes_s (classes of rows <= 33
 // entries) and ff_gather_classes_l (longer rows). Needs a gather-capable
 // plan (plan.n_kinv > 0). Byte-deterministic.
+// pre: the item's first `pre` record ids come from the plan's computable
+// prefix block (GatherPlan::pre_steps; every class has >= pre steps).
 std::string emit_class_source(const ElementPlan& plan, int n_local, const std::vector<RowClass>& classes,
-                              bool fused = false, int bs = 1);
+                              bool fused = false, int bs = 1, int pre = 1);
 
 // Shortest round-trip double literal valid in C/CUDA source.
 std::string double_literal(double v);

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <vector>
 
 #include <cstdint>
@@ -39,6 +40,7 @@ struct GatherPlan {
     int len = 0, steps = 0;
     std::vector<int> local;         // [steps] local index i of each step
     std::vector<uint8_t> slots;     // [steps][k]
+    std::vector<int> order;         // processing order of the steps (records are laid out in it)
     int64_t rows = 0;
   };
   std::vector<Class> classes;
@@ -46,19 +48,27 @@ struct GatherPlan {
   int32_t* citem_class = nullptr;   // [n_citems]
   int32_t* citem_rows = nullptr;    // [n_citems][32] local row or -1
   int32_t* vconn_m = nullptr;       // [E][dim+1] vertex ids in record (Morton) order, read by K2a
-  int64_t* citem_rec = nullptr;     // [n_citems] first record of the item ([steps][32] element ids)
-  int32_t* crec = nullptr;          // [n_crec] element records (-1: idle lane)
+  // element ids of the class items, in each class's processing order: item
+  // w's first pre_steps steps at crec[(w * pre_steps + t) * 32 + lane], its
+  // other steps from crec[citem_rec[w] * 32]
+  int64_t* citem_rec = nullptr;     // [n_citems + 1]
+  int32_t* crec = nullptr;          // [n_crec (+ 8 steps of padding)] element records (-1: idle lane)
+  int pre_steps = 0;
   // element order of the per-element records: record t belongs to element
   // eorder[t]; records (rec, crec) hold erank[e]
   int32_t* eorder = nullptr;
   int32_t* erank = nullptr;
 };
 // bbox: {min x, min y, min z, max x, max y, max z} of the mesh coordinates.
+// Processing order of a row class's steps (the code generator's choice; the
+// records of its items are laid out in that order).
+using ClassOrderFn = std::function<std::vector<int>(const GatherPlan::Class&)>;
 cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, int dim, const double* bbox,
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64,
-                              bool use_eorder = true, bool split_long = true);
+                              bool use_eorder = true, bool split_long = true,
+                              const ClassOrderFn* step_order = nullptr);
 void free_gather_plan(GatherPlan* p);
 
 // fem::Mesh::validate (fem.cpp:17-34) on the device: *d_bad = the lowest

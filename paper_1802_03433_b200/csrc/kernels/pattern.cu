@@ -418,20 +418,46 @@ __global__ void gather_rows_i32(const int32_t* __restrict__ in, int in_stride, i
   }
 }
 
+// records of the class items in the class's processing order: step t of
+// item w holds the element of incidence perm[class][t] of the lane's row
 __global__ void fill_class_records(const int32_t* __restrict__ erank, const int32_t* __restrict__ citem_class,
                                    const int32_t* __restrict__ citem_rows,
                                    const int64_t* __restrict__ citem_rec, int64_t n_citems,
-                                   const int32_t* __restrict__ cls_steps, const int64_t* __restrict__ inc_ptr,
-                                   const int32_t* __restrict__ inc, int k, int32_t* __restrict__ crec) {
+                                   const int32_t* __restrict__ cls_steps, const int32_t* __restrict__ perm,
+                                   const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc, int k,
+                                   int32_t* __restrict__ crec) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_citems * 32;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t w = t / 32;
     const int lane = static_cast<int>(t % 32);
     const int32_t row = citem_rows[t];
-    const int n = cls_steps[citem_class[w]];
+    const int c = citem_class[w];
+    const int n = cls_steps[c];
     const int64_t base = citem_rec[w] * 32 + lane;
     const int64_t p = row >= 0 ? inc_ptr[row] : 0;
-    for (int q = 0; q < n; ++q) crec[base + q * 32] = row >= 0 ? erank[inc[p + q] / k] : -1;
+    for (int q = 0; q < n; ++q)
+      crec[base + q * 32] = row >= 0 ? erank[inc[p + perm[c * kMaxClassSteps + q]] / k] : -1;
+  }
+}
+
+// [steps][32] records per item (prefix irec) -> the first `pre` steps of item
+// w at the computable position (w * pre + t) * 32, the rest after all of them
+// at (n_items * pre + irec2[w] + t - pre) * 32
+__global__ void relayout_records(const int32_t* __restrict__ src, const int64_t* __restrict__ irec,
+                                 const int64_t* __restrict__ irec2, int64_t n_items, int pre,
+                                 int32_t* __restrict__ dst) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n_items * 32;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = t / 32;
+    const int lane = static_cast<int>(t % 32);
+    const int64_t n = irec[w + 1] - irec[w];
+    for (int64_t q = 0; q < n; ++q) {
+      const int32_t v = src[(irec[w] + q) * 32 + lane];
+      if (q < pre)
+        dst[(w * pre + q) * 32 + lane] = v;
+      else
+        dst[(n_items * pre + irec2[w] + q - pre) * 32 + lane] = v;
+    }
   }
 }
 
@@ -577,7 +603,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes,
-                              bool use_eorder, bool split_long) {
+                              bool use_eorder, bool split_long, const ClassOrderFn* step_order) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   // FF_PLAN_TIMING=1: phase times of the plan build on stderr
@@ -811,6 +837,13 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
           cl.local.push_back(o[2 + q * (1 + k)]);
           for (int j = 0; j < k; ++j) cl.slots.push_back(static_cast<uint8_t>(o[3 + q * (1 + k) + j]));
         }
+        // processing order of the class kernel (code generator's choice):
+        // records are laid out in it
+        if (step_order && cl.steps > 0) cl.order = (*step_order)(cl);
+        if (static_cast<int>(cl.order.size()) != std::max(cl.steps, 0)) {
+          cl.order.resize(std::max(cl.steps, 0));
+          for (int q = 0; q < std::max(cl.steps, 0); ++q) cl.order[q] = q;
+        }
         out->classes.push_back(std::move(cl));
       }
     }
@@ -893,11 +926,18 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       cudaMemcpyAsync(out->citem_rows, ir.data(), nci * 32 * sizeof(int32_t), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(out->citem_rec, irec.data(), (nci + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(d_steps, cls_steps.data(), cls_steps.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+      std::vector<int32_t> perm(static_cast<size_t>(std::max(n_cls, 1)) * kMaxClassSteps, 0);
+      for (int c = 0; c < n_cls; ++c)
+        for (size_t t = 0; t < out->classes[c].order.size(); ++t) perm[c * kMaxClassSteps + t] = out->classes[c].order[t];
+      int32_t* d_perm = nullptr;
+      if ((err = cudaMalloc(&d_perm, perm.size() * sizeof(int32_t))) != cudaSuccess) return cudaFree(d_steps), done(err);
+      cudaMemcpyAsync(d_perm, perm.data(), perm.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s);
       fill_class_records<<<grid_for(nci * 32, cap), kThreads, 0, s>>>(out->erank, out->citem_class, out->citem_rows,
-                                                                      out->citem_rec, nci, d_steps, inc_ptr, inc, k,
-                                                                      out->crec);
+                                                                      out->citem_rec, nci, d_steps, d_perm, inc_ptr,
+                                                                      inc, k, out->crec);
       err = cudaStreamSynchronize(s);
       cudaFree(d_steps);
+      cudaFree(d_perm);
       if (err != cudaSuccess) return done(err);
       // element records in first-touch order of the class records (item, step,
       // lane): the elements the 32 lanes of one step read are then stored side
@@ -955,6 +995,33 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
           std::fclose(fp);
         }
       }
+      // the first `pre` steps of every item (the class kernel's prefetch) at a
+      // position computable from the item index: the warp loads them together
+      // with the item header instead of after it
+      int pre = kMaxClassSteps;
+      for (int c = 0; c < n_cls; ++c)
+        if (out->classes[c].steps > 0) pre = std::min(pre, out->classes[c].steps);
+      pre = std::min(pre, 8);
+      std::vector<int64_t> irec2(nci + 1, 0);
+      for (int64_t w = 0; w < nci; ++w) irec2[w + 1] = irec2[w] + (irec[w + 1] - irec[w]) - pre;
+      std::vector<int64_t> crec_at(nci + 1);
+      for (int64_t w = 0; w <= nci; ++w) crec_at[w] = nci * pre + irec2[w];
+      int32_t* crec2 = nullptr;
+      int64_t* d_irec2 = nullptr;
+      if ((err = cudaMalloc(&crec2, (out->n_crec + 8 * 32) * sizeof(int32_t))) != cudaSuccess) return done(err);
+      if ((err = cudaMalloc(&d_irec2, (nci + 1) * sizeof(int64_t))) != cudaSuccess)
+        return cudaFree(crec2), done(err);
+      cudaMemsetAsync(crec2 + out->n_crec, 0xff, 8 * 32 * sizeof(int32_t), s);
+      cudaMemcpyAsync(d_irec2, irec2.data(), (nci + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+      relayout_records<<<grid_for(nci * 32, cap), kThreads, 0, s>>>(out->crec, out->citem_rec, d_irec2, nci, pre,
+                                                                    crec2);
+      cudaMemcpyAsync(out->citem_rec, crec_at.data(), (nci + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+      err = cudaStreamSynchronize(s);
+      cudaFree(d_irec2);
+      if (err != cudaSuccess) return cudaFree(crec2), done(err);
+      cudaFree(out->crec);
+      out->crec = crec2;
+      out->pre_steps = pre;
     }
   }
   phase("class items");
