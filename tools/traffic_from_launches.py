@@ -5,8 +5,8 @@ source of bench.py) from an ncu launch list of `bench.py --steps K`:
       --clock-control none -k regex:ff_ --csv --log-file L.csv python bench.py ...
   python tools/traffic_from_launches.py L.csv ns 128 gather 4 > profiles/traffic_ns_n128_gather.json
 
-One assembly step = the last `per_step` ff_ launches (gather: K2a + class
-kernel + the generic row launches)."""
+One assembly step = the last `per_step` launches of the scatter's kernels
+(gather: K2a + class kernel + the generic row launches)."""
 import collections
 import csv
 import json
@@ -22,7 +22,10 @@ def main(path, config, n, scatter, per_step):
     launches = collections.OrderedDict()
     for r in rows[1:]:
         launches.setdefault((int(r[I]), r[K]), {})[r[M]] = float(r[V].replace(",", ""))
-    step = list(launches.items())[-per_step:]
+    # the last complete step of this scatter's kernels (calibration runs of the
+    # other scatter may follow in the list)
+    prefix = "ff_gather" if scatter == "gather" else "ff_assemble"
+    step = [kv for kv in launches.items() if kv[0][1].startswith(prefix)][-per_step:]
     kernels = [{"name": k, "dram_read": m["dram__bytes_read.sum"], "dram_write": m["dram__bytes_write.sum"],
                 "ms": m["gpu__time_duration.sum"] / 1e6} for (_, k), m in step]
     out = {"config": config, "scatter": scatter,
