@@ -333,6 +333,7 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N>1: strong (default, SURVEY §8e) = contiguous DOF row blocks of the one configured "
                          "mesh, halo elements duplicated; weak = the 1-GPU workload stacked N times")
+    ap.add_argument("--emulate-rank", default="", help="R/N: time rank R's row block of an N-rank run on one GPU")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.n:
@@ -372,8 +373,11 @@ def main():
     else:
         coords, vconn, dconn, n_dofs = make_mesh(ff, cfg)
         E = vconn.shape[0]
-        rb, re = rowblocks.row_block(n_dofs, world, rank)
-        if world > 1:  # strong scaling: row blocks of the one mesh
+        # --emulate-rank R/N (single GPU, diagnostics only): rank R's row block of
+        # an N-rank strong-scaling run, to predict the per-rank step time
+        emu = tuple(int(v) for v in args.emulate_rank.split("/")) if args.emulate_rank else None
+        rb, re = rowblocks.row_block(n_dofs, emu[1], emu[0]) if emu else rowblocks.row_block(n_dofs, world, rank)
+        if world > 1 or emu:  # strong scaling: row blocks of the one mesh
             ids = rowblocks.local_elements(dconn, rb, re)   # owned + halo elements
             vconn_l, dconn_l = np.ascontiguousarray(vconn[ids]), np.ascontiguousarray(dconn[ids])
         else:
