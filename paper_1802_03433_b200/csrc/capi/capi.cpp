@@ -462,13 +462,17 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
         cend[2 * c + 1] = g.fchunk_item[c + 1];
         need[c] = static_cast<unsigned>(k2a[c].size());
       }
-      // ticket order: K2a of chunk 0, then the class units of chunk c with the
-      // K2a units of chunk c+1 spread evenly among them
-      std::vector<int2> units(k2a[0]);
+      // ticket order: K2a of chunks [0, lead), then the class units of chunk c
+      // with the K2a units of chunk c + lead spread evenly among them -- the
+      // lead covers the CTAs resident at once, so a class unit rarely waits
+      int64_t lead = 4;
+      if (const char* v = std::getenv("FF_FUSED_LEAD")) lead = std::max(1, std::atoi(v));  // tuning knob
+      std::vector<int2> units;
+      for (int64_t c = 0; c < std::min(lead, nch); ++c) units.insert(units.end(), k2a[c].begin(), k2a[c].end());
       for (int64_t c = 0; c < nch; ++c) {
         const std::vector<int2>& a = cls[c];
         const std::vector<int2> none;
-        const std::vector<int2>& b = c + 1 < nch ? k2a[c + 1] : none;
+        const std::vector<int2>& b = c + lead < nch ? k2a[c + lead] : none;
         size_t ia = 0, ib = 0;
         while (ia < a.size() || ib < b.size()) {
           // keep the K2a share ahead of the class share
