@@ -554,9 +554,16 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  extern __shared__ double ff_dsm[];\n"
           "  __shared__ int2 s_unit;\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
+          "#ifdef FF_FUSED_TICKET\n"
           "  if (threadIdx.x == 0) s_unit = units[atomicAdd(ctl, 1u)];\n"
           "  __syncthreads();\n"
           "  const int2 u = s_unit;\n"
+          "#else\n"
+          "  // units in block order (CTAs are dispatched in index order: a CTA that\n"
+          "  // waits was dispatched after every K2a unit it waits for)\n"
+          "  (void)s_unit;\n"
+          "  const int2 u = __ldg(units + blockIdx.x);\n"
+          "#endif\n"
           "  if (u.x < 0) {  // K2a unit of chunk -u.x - 1\n"
           "    const int ch = -u.x - 1;\n"
           "    const ff_i64 rend = chunk_end[2 * ch];\n"
@@ -570,6 +577,18 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "    return;\n"
           "  }\n"
           "  const int ch = u.x;\n"
+          "  // the item's plan data (header, first record ids, row start) load before\n"
+          "  // the wait: only the element records come from the K2a units\n"
+          "  const ff_i64 first = (ff_i64)u.y + wid;\n"
+          "  const bool active = first < chunk_end[2 * ch + 1];\n"
+          "  const ff_i64 fi = active ? first : u.y;\n"
+          "  const int c = __ldg(citem_class + fi);\n"
+          "  const int row = active ? __ldg(citem_rows + fi * 32 + lane) : -1;\n"
+          "  const ff_i32* rec = crec + __ldg(citem_rec + fi) * 32 + lane;\n"
+          "  int ep[FF_PRE];\n"
+          "#pragma unroll\n"
+          "  for (int q = 0; q < FF_PRE; ++q) ep[q] = __ldcs(crec + (fi * FF_PRE + q) * 32 + lane);\n"
+          "  const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
           "  if (threadIdx.x == 0) {\n"
           "    for (int cc = ch; cc >= 0; --cc) {\n"
           "      if (ff_ld_acquire(ctl + 1 + n_chunks + cc)) break;\n"
@@ -580,15 +599,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  __syncthreads();\n"
           "  double* st = ff_dsm + wid * 32 * FF_SP_S;\n"
           "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * 32 * FF_SP_S) + wid * 32;\n"
-          "  const ff_i64 first = (ff_i64)u.y + wid;\n"
-          "  if (first >= chunk_end[2 * ch + 1]) return;\n"
-          "  int c = __ldg(citem_class + first);\n"
-          "  const int row = __ldg(citem_rows + first * 32 + lane);\n"
-          "  const ff_i32* rec = crec + __ldg(citem_rec + first) * 32 + lane;\n"
-          "  int ep[FF_PRE];\n"
-          "#pragma unroll\n"
-          "  for (int q = 0; q < FF_PRE; ++q) ep[q] = __ldcs(crec + (first * FF_PRE + q) * 32 + lane);\n"
-          "  const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
+          "  if (!active) return;\n"
           "  switch (c) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       os << "    case " << c << ": ff_cls_" << c << "_0(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
