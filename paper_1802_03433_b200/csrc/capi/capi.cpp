@@ -158,21 +158,9 @@ void ensure_plan(ff_pattern* p, const ff_mesh* m) {
 
 void free_class_module(ff_pattern* p) {
   if (p->class_lib) cudaLibraryUnload(p->class_lib);
-  if (p->fused_lib) cudaLibraryUnload(p->fused_lib);
   p->class_lib = nullptr;
-  p->fused_lib = nullptr;
   p->class_kernel[0] = p->class_kernel[1] = nullptr;
-  p->fused_kernel = nullptr;
   p->class_key.clear();
-}
-
-// The fused K2a + class kernel runs for scalar forms whose plan has first-touch
-// chunk boundaries (FF_FUSED=0: K2a, then the class kernel).
-bool fused_enabled(const ff_form* f, const ff_pattern* p) {
-  const char* v = std::getenv("FF_FUSED");
-  if (v && std::atoi(v) == 0) return false;
-  return f->ncomp == 1 && !f->raw && p->gather.fchunk_item.size() >= 2 && p->gather.n_citems > 0 &&
-         std::getenv("FF_SPLIT_CLASSES") == nullptr;
 }
 
 void free_gather(ff_pattern* p) {
@@ -181,9 +169,6 @@ void free_gather(ff_pattern* p) {
   p->gather_mesh = nullptr;
   free_class_module(p);
 }
-
-// records per thread of a fused K2a work unit (FF_KR in the class source)
-constexpr int kFusedKR = 4;
 
 int class_cwarps(const ff_form* f) {
   const char* v = std::getenv("FF_CWARPS");
@@ -248,18 +233,6 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
     ffb::cuda_check(cudaKernelSetAttributeForDevice(p->class_kernel[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     p->class_smem[c], p->ctx->device),
                     "class kernel shared memory attribute");
-  }
-  if (fused_enabled(f, p)) {
-    // the form's template (K2a) + the class functions + ff_gather_fused, one TU
-    const std::string fsrc = "#define FF_COHERENT_RECORDS 1\n#define FF_FUSED_MODULE 1\n" + f->source[p->slot_bytes] +
-                             "\n" + src;
-    const ffb::CompiledModule fmod = ffb::nvrtc_compile(fsrc, "femforge_fused.cu");
-    ffb::cuda_check(cudaLibraryLoadData(&p->fused_lib, fmod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
-                    "cudaLibraryLoadData (fused)");
-    ffb::cuda_check(cudaLibraryGetKernel(&p->fused_kernel, p->fused_lib, "ff_gather_fused"), "fused kernel");
-    ffb::cuda_check(cudaKernelSetAttributeForDevice(p->fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    p->class_smem[0], p->ctx->device),
-                    "fused kernel shared memory attribute");
   }
   p->class_compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   p->class_key = key;
@@ -367,12 +340,9 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
                     "K2a (element invariants) launch");
   };
   const ffb::kernels::GatherPlan& gp = p->gather;
-  // fused K2a + class rows (decided once the class module exists)
-  if (gp.n_citems > 0 && !(flags & (FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY))) ensure_class_module(f, p);
-  const bool fused_launch = p->fused_kernel && !(flags & (FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY));
   if (!(flags & FF_GATHER_ROWS_ONLY)) {
     ffb::cuda_check(cudaMemsetAsync(status, 0xff, 2 * sizeof(unsigned long long), s), "status reset");
-    if (!fused_launch) launch_k2a(0, m->ne, s);
+    launch_k2a(0, m->ne, s);
   }
   if (flags & FF_GATHER_INVARIANTS_ONLY) return;
   auto launch_generic = [&](cudaStream_t sg) {
@@ -442,84 +412,6 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   };
   if (gp.n_citems > 0) ensure_class_module(f, p);
   const int64_t ns = gp.n_citems_short;
-  if (p->fused_kernel && !(flags & (FF_GATHER_INVARIANTS_ONLY | FF_GATHER_ROWS_ONLY))) {
-    // fused K2a + class rows (one launch; records read back from L2), then
-    // the generic rows, which may read any record
-    ffb::kernels::GatherPlan& g = p->gather;
-    const int cw = class_cwarps(f);
-    const int64_t nch = static_cast<int64_t>(g.fchunk_item.size()) - 1;
-    if (!g.fused_units) {
-      const int64_t ru = int64_t(32) * cw * kFusedKR, cu = cw;
-      std::vector<std::vector<int2>> k2a(nch), cls(nch);
-      std::vector<int64_t> cend(2 * nch);
-      std::vector<unsigned> need(nch);
-      for (int64_t c = 0; c < nch; ++c) {
-        const int64_t r0 = g.fchunk_rec[c], r1 = g.fchunk_rec[c + 1];
-        for (int64_t r = r0; r < r1; r += ru) k2a[c].push_back(make_int2(static_cast<int>(-(c + 1)), static_cast<int>(r)));
-        for (int64_t i = g.fchunk_item[c]; i < g.fchunk_item[c + 1]; i += cu)
-          cls[c].push_back(make_int2(static_cast<int>(c), static_cast<int>(i)));
-        cend[2 * c] = r1;
-        cend[2 * c + 1] = g.fchunk_item[c + 1];
-        need[c] = static_cast<unsigned>(k2a[c].size());
-      }
-      // ticket order: K2a of chunks [0, lead), then the class units of chunk c
-      // with the K2a units of chunk c + lead spread evenly among them -- the
-      // lead covers the CTAs resident at once, so a class unit rarely waits
-      int64_t lead = 4;
-      if (const char* v = std::getenv("FF_FUSED_LEAD")) lead = std::max(1, std::atoi(v));  // tuning knob
-      std::vector<int2> units;
-      for (int64_t c = 0; c < std::min(lead, nch); ++c) units.insert(units.end(), k2a[c].begin(), k2a[c].end());
-      for (int64_t c = 0; c < nch; ++c) {
-        const std::vector<int2>& a = cls[c];
-        const std::vector<int2> none;
-        const std::vector<int2>& b = c + lead < nch ? k2a[c + lead] : none;
-        size_t ia = 0, ib = 0;
-        while (ia < a.size() || ib < b.size()) {
-          // keep the K2a share ahead of the class share
-          if (ib < b.size() && (ia == a.size() || ib * a.size() <= ia * b.size()))
-            units.push_back(b[ib++]);
-          else
-            units.push_back(a[ia++]);
-        }
-      }
-      g.fused_n_units = static_cast<int64_t>(units.size());
-      g.fused_units = device_alloc<int2>(units.size(), "fused work units");
-      g.fused_chunk_end = device_alloc<int64_t>(cend.size(), "fused chunk bounds");
-      g.fused_chunk_need = device_alloc<unsigned>(need.size(), "fused chunk bounds");
-      g.fused_ctl = device_alloc<unsigned>(1 + 2 * nch, "fused control words");
-      ffb::cuda_check(cudaMemcpy(g.fused_units, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice), "H2D");
-      ffb::cuda_check(cudaMemcpy(g.fused_chunk_end, cend.data(), cend.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
-                      "H2D");
-      ffb::cuda_check(cudaMemcpy(g.fused_chunk_need, need.data(), need.size() * sizeof(unsigned), cudaMemcpyHostToDevice),
-                      "H2D");
-    }
-    ffb::cuda_check(cudaMemsetAsync(g.fused_ctl, 0, (1 + 2 * nch) * sizeof(unsigned), s), "fused control reset");
-    {
-      const double* coords = m->coords;
-      const int32_t* vconn = g.vconn_m;
-      const int32_t* eorder = g.eorder;
-      double* ginv = p->ginv;
-      long long ne = m->ne;
-      const int64_t* row_ptr = p->row_ptr;
-      const int32_t* icls = g.citem_class;
-      const int32_t* irows = g.citem_rows;
-      const int64_t* irec = g.citem_rec;
-      const int32_t* crec = g.crec;
-      const int2* units = g.fused_units;
-      const int64_t* cend = g.fused_chunk_end;
-      const unsigned* need = g.fused_chunk_need;
-      int n_chunks = static_cast<int>(nch);
-      unsigned* ctl = g.fused_ctl;
-      void* args[] = {&coords, &vconn, &eorder, &ginv, &ne, &status, &row_ptr, &d_values, &d_rhs, &icls, &irows,
-                      &irec, &crec, &units, &cend, &need, &n_chunks, &ctl};
-      ffb::cuda_check(cudaLaunchKernel(reinterpret_cast<const void*>(p->fused_kernel),
-                                       dim3(static_cast<unsigned>(g.fused_n_units)), dim3(32 * cw), args,
-                                       p->class_smem[0], s),
-                      "fused K2a + class rows launch");
-    }
-    launch_generic(s);
-    return;
-  }
   // the generic rows run on the side stream, concurrently with the class
   // kernel (disjoint rows, both only read the element records): 2.861 ->
   // 2.846 ms at the north star (run 34)

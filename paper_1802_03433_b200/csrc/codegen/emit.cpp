@@ -209,16 +209,9 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
   const int erec = (plan.n_kinv + n_local + 1) & ~1;
   if (std::getenv("FF_NO_BPAD")) os << "#define FF_NO_BPAD 1\n";  // tuning knob (both modules)
   os << "#define FF_PRE " << pre << "\n";
-  os << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
-     << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
-     << class_stage_pitch(classes, 1, fused) << "\n";
   os << "// femforge-b200 class-specialised row gather (generated per (form, gather plan));\n"
         "// every class row stays in registers, indexed by compile-time slots.\n"
-        "// Compiled alone (the class module) or appended to the form's template source\n"
-        "// (FF_FUSED_MODULE: the fused K2a + class kernel), which already defines the\n"
-        "// record macros, the row code and the record loads.\n"
         "typedef long long ff_i64;\ntypedef int ff_i32;\n"
-     << "#ifndef FF_FUSED_MODULE\n"
      << "#define FF_NLOC " << n_local << "\n#define FF_BS " << bs << "\n#define FF_NB " << nb
      << "\n#define FF_NKINV " << plan.n_kinv << "\n#define FF_NKP " << nkp
      << "\n#define FF_EREC " << erec << "\n#define FF_GS " << ((plan.n_kinv + 3) / 4) * 4 << "\n"
@@ -227,6 +220,9 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "#if FF_BS == 1\n#define FF_GSTORE (4 * FF_NFULL + FF_GTAIL)\n#else\n#define FF_GSTORE FF_GS\n#endif\n"
      << "#if FF_BS == 1 && FF_GTAIL == 4 && !defined(FF_NO_BPAD)\n"
         "#define FF_NBPAD ((4 - FF_NKINV % 4) < FF_NLOC ? (4 - FF_NKINV % 4) : FF_NLOC)\n#else\n#define FF_NBPAD 0\n#endif\n"
+     << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
+     << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
+     << class_stage_pitch(classes, 1, fused) << "\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
@@ -251,9 +247,6 @@ __device__ __forceinline__ void ff_ld2(const double* p, double& a, double& b) {
 __device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
 #endif
 )" << kInvariantLoad << R"(
-#else  // FF_FUSED_MODULE: records are written by this kernel -- coherent (L2) loads
-__device__ __forceinline__ double ff_ld1(const double* p) { return __ldcg(p); }
-#endif
 // element record: invariants (ff_load_inv), load vector [FF_NLOC][E]
 // (idle lanes, e < 0, only occur in rows that are never written: they read
 // element 0 instead of branching)
@@ -530,81 +523,6 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   };
   kernel("ff_gather_classes_s", false);
   kernel("ff_gather_classes_l", true);
-  if (bs == 1 && fused) {
-    // K2a and the class rows in one launch (FF_FUSED_MODULE: this source appended
-    // to the form's template). CTAs take work units in ticket order: K2a units
-    // (FF_CWARPS * 32 * FF_KR records) of chunk c+1 interleaved with the class
-    // units (FF_CWARPS items) of chunk c; a class unit waits until every K2a
-    // unit of chunks <= c has finished (a CTA holding a smaller ticket never
-    // waits, so the waits cannot deadlock). The records a chunk's items read
-    // are written a moment before, so they are read back from L2.
-    os << "#ifdef FF_FUSED_MODULE\n#ifndef FF_KR\n#define FF_KR 4\n#endif\n"
-          "__device__ __forceinline__ unsigned ff_ld_acquire(const unsigned* p) {\n"
-          "  unsigned v;\n  asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(p) : \"memory\");\n"
-          "  return v;\n}\n"
-          "extern \"C\" __global__ void __launch_bounds__(32 * FF_CWARPS, FF_MINB_S)\n"
-          "ff_gather_fused(const double* __restrict__ coords, const ff_i32* __restrict__ vconn,\n"
-          "    const ff_i32* __restrict__ eorder, double* __restrict__ einv, ff_i64 n_elems,\n"
-          "    FfStatus* __restrict__ status, const ff_i64* __restrict__ row_ptr, double* __restrict__ values,\n"
-          "    double* __restrict__ rhs, const ff_i32* __restrict__ citem_class, const ff_i32* __restrict__ citem_rows,\n"
-          "    const ff_i64* __restrict__ citem_rec, const ff_i32* __restrict__ crec, const int2* __restrict__ units,\n"
-          "    const ff_i64* __restrict__ chunk_end, const unsigned* __restrict__ chunk_need, int n_chunks,\n"
-          "    unsigned* ctl) {\n"
-          "  // ctl: [0] ticket, [1 + c] K2a units done in chunk c, [1 + n_chunks + c] chunks <= c verified\n"
-          "  extern __shared__ double ff_dsm[];\n"
-          "  __shared__ int2 s_unit;\n"
-          "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
-          "#ifdef FF_FUSED_TICKET\n"
-          "  if (threadIdx.x == 0) s_unit = units[atomicAdd(ctl, 1u)];\n"
-          "  __syncthreads();\n"
-          "  const int2 u = s_unit;\n"
-          "#else\n"
-          "  // units in block order (CTAs are dispatched in index order: a CTA that\n"
-          "  // waits was dispatched after every K2a unit it waits for)\n"
-          "  (void)s_unit;\n"
-          "  const int2 u = __ldg(units + blockIdx.x);\n"
-          "#endif\n"
-          "  if (u.x < 0) {  // K2a unit of chunk -u.x - 1\n"
-          "    const int ch = -u.x - 1;\n"
-          "    const ff_i64 rend = chunk_end[2 * ch];\n"
-          "#pragma unroll 1\n"
-          "    for (int r = 0; r < FF_KR; ++r) {\n"
-          "      const ff_i64 t = (ff_i64)u.y + (ff_i64)r * (32 * FF_CWARPS) + threadIdx.x;\n"
-          "      ff_k2a_record(coords, vconn, eorder, n_elems, einv, status, t, t < rend);\n"
-          "    }\n"
-          "    __syncthreads();\n"
-          "    if (threadIdx.x == 0) {\n      __threadfence();\n      atomicAdd(ctl + 1 + ch, 1u);\n    }\n"
-          "    return;\n"
-          "  }\n"
-          "  const int ch = u.x;\n"
-          "  // the item's plan data (header, first record ids, row start) load before\n"
-          "  // the wait: only the element records come from the K2a units\n"
-          "  const ff_i64 first = (ff_i64)u.y + wid;\n"
-          "  const bool active = first < chunk_end[2 * ch + 1];\n"
-          "  const ff_i64 fi = active ? first : u.y;\n"
-          "  const int c = __ldg(citem_class + fi);\n"
-          "  const int row = active ? __ldg(citem_rows + fi * 32 + lane) : -1;\n"
-          "  const ff_i32* rec = crec + __ldg(citem_rec + fi) * 32 + lane;\n"
-          "  int ep[FF_PRE];\n"
-          "#pragma unroll\n"
-          "  for (int q = 0; q < FF_PRE; ++q) ep[q] = __ldcs(crec + (fi * FF_PRE + q) * 32 + lane);\n"
-          "  const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
-          "  if (threadIdx.x == 0) {\n"
-          "    for (int cc = ch; cc >= 0; --cc) {\n"
-          "      if (ff_ld_acquire(ctl + 1 + n_chunks + cc)) break;\n"
-          "      while (ff_ld_acquire(ctl + 1 + cc) < chunk_need[cc]) __nanosleep(64);\n"
-          "    }\n"
-          "    atomicExch(ctl + 1 + n_chunks + ch, 1u);\n"
-          "  }\n"
-          "  __syncthreads();\n"
-          "  double* st = ff_dsm + wid * 32 * FF_SP_S;\n"
-          "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * 32 * FF_SP_S) + wid * 32;\n"
-          "  if (!active) return;\n"
-          "  switch (c) {\n";
-    for (int c = 0; c < static_cast<int>(classes.size()); ++c)
-      os << "    case " << c << ": ff_cls_" << c << "_0(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
-    os << "    default: break;\n  }\n}\n#endif\n";
-  }
   return os.str();
 }
 

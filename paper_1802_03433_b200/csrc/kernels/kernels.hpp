@@ -54,16 +54,6 @@ struct GatherPlan {
   int64_t* citem_rec = nullptr;     // [n_citems + 1]
   int32_t* crec = nullptr;          // [n_crec (+ 8 steps of padding)] element records (-1: idle lane)
   int pre_steps = 0;
-  // fused K2a + class launch (first-touch record order): class items
-  // [fchunk_item[c], fchunk_item[c+1]) read records below fchunk_rec[c+1]
-  static constexpr int64_t kFusedChunkItems = 2048;
-  std::vector<int64_t> fchunk_item, fchunk_rec;
-  // its work-unit table and control words on the device (built at first use)
-  int2* fused_units = nullptr;
-  int64_t* fused_chunk_end = nullptr;   // [2 * n_chunks]: record end, item end
-  unsigned* fused_chunk_need = nullptr; // [n_chunks]: K2a units per chunk
-  unsigned* fused_ctl = nullptr;        // [1 + 2 * n_chunks]
-  int64_t fused_n_units = 0;
   // element order of the per-element records: record t belongs to element
   // eorder[t]; records (rec, crec) hold erank[e]
   int32_t* eorder = nullptr;

@@ -486,22 +486,6 @@ __global__ void touch_keys(const unsigned long long* __restrict__ first, const i
   }
 }
 
-// out[c] = number of sorted keys below bound[c] (lower_bound on the device)
-__global__ void count_below(const uint64_t* __restrict__ sorted, int64_t n, const uint64_t* __restrict__ bound,
-                            int nb, int64_t* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nb) return;
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) / 2;
-    if (sorted[mid] < bound[c])
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  out[c] = lo;
-}
-
 // record ranks of the old order -> ranks of the new one
 __global__ void remap_ranks(int32_t* __restrict__ crec, int64_t n, const int32_t* __restrict__ eorder_old,
                             const int32_t* __restrict__ erank_new) {
@@ -985,36 +969,6 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
         if ((err = need_temp(te)) != cudaSuccess) return tfree(), done(err);
         err = cub::DeviceRadixSort::SortPairs(temp, te, ek, ek2, eid, eorder_new, ne, 0, 64, s);
         if (err == cudaSuccess) {
-          // fused K2a + class launch: with records in first-touch order, the
-          // class items [0, P) read only records [0, R(P)), R(P) = the elements
-          // first touched before item P -- chunk boundaries every
-          // GatherPlan::kFusedChunkItems items; the last chunk also computes the
-          // records only generic rows read
-          const int64_t cw = GatherPlan::kFusedChunkItems;
-          const int64_t nch = (nci + cw - 1) / cw;
-          std::vector<uint64_t> bnd(nch + 1);
-          out->fchunk_item.resize(nch + 1);
-          out->fchunk_rec.resize(nch + 1);
-          for (int64_t c = 0; c <= nch; ++c) {
-            out->fchunk_item[c] = std::min(nci, c * cw);
-            bnd[c] = static_cast<uint64_t>(irec[out->fchunk_item[c]]) * 32;
-          }
-          uint64_t* d_bnd = nullptr;
-          if ((err = cudaMalloc(&d_bnd, (nch + 1) * (sizeof(uint64_t) + sizeof(int64_t)))) == cudaSuccess) {
-            int64_t* d_cnt = reinterpret_cast<int64_t*>(d_bnd + nch + 1);
-            cudaMemcpyAsync(d_bnd, bnd.data(), (nch + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s);
-            count_below<<<static_cast<int>((nch + 1 + 127) / 128), 128, 0, s>>>(ek2, ne, d_bnd, static_cast<int>(nch + 1),
-                                                                              d_cnt);
-            cudaMemcpyAsync(out->fchunk_rec.data(), d_cnt, (nch + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-            err = cudaStreamSynchronize(s);
-            cudaFree(d_bnd);
-          }
-          if (err != cudaSuccess) {
-            out->fchunk_item.clear();
-            out->fchunk_rec.clear();
-            return tfree(), done(err);
-          }
-          out->fchunk_rec[nch] = ne;
           invert_perm<<<grid_for(ne, cap), kThreads, 0, s>>>(eorder_new, ne, out->erank);
           remap_ranks<<<grid_for(out->n_crec, cap), kThreads, 0, s>>>(out->crec, out->n_crec, out->eorder,
                                                                        out->erank);
@@ -1174,10 +1128,6 @@ cudaError_t expand_block_pattern(const int64_t* rp_s, const int32_t* ci_s, int64
 }
 
 void free_gather_plan(GatherPlan* p) {
-  cudaFree(p->fused_units);
-  cudaFree(p->fused_chunk_end);
-  cudaFree(p->fused_chunk_need);
-  cudaFree(p->fused_ctl);
   cudaFree(p->eorder);
   cudaFree(p->erank);
   cudaFree(p->citem_class);

@@ -114,9 +114,6 @@ struct ff_pattern {
   cudaLibrary_t class_lib = nullptr;
   cudaKernel_t class_kernel[2] = {nullptr, nullptr};  // short rows, long rows
   int class_smem[2] = {0, 0};                           // their dynamic shared memory
-  // fused K2a + class rows (scalar forms; the form template + the class source)
-  cudaLibrary_t fused_lib = nullptr;
-  cudaKernel_t fused_kernel = nullptr;
   double class_compile_ms = 0.0;
   double* ginv = nullptr;   // [ne][nkp]
   double* bvec = nullptr;   // [ne][k]
