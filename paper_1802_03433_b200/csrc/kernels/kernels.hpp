@@ -68,7 +68,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64,
                               bool use_eorder = true, bool split_long = true,
-                              const ClassOrderFn* step_order = nullptr);
+                              const ClassOrderFn* step_order = nullptr, double class_frac = 0.0005);
 void free_gather_plan(GatherPlan* p);
 
 // fem::Mesh::validate (fem.cpp:17-34) on the device: *d_bad = the lowest

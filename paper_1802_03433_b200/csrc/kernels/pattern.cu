@@ -603,7 +603,8 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               const int32_t* d_dconn, int64_t ne, int k, int64_t rb, int64_t n_rows,
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes,
-                              bool use_eorder, bool split_long, const ClassOrderFn* step_order) {
+                              bool use_eorder, bool split_long, const ClassOrderFn* step_order,
+                              double class_frac) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   // FF_PLAN_TIMING=1: phase times of the plan build on stderr
@@ -774,8 +775,10 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     // warp they are as cheap as interior rows, while the generic gather costs
     // ~3x per row -- NS 2.00 -> 1.89 ms, C3 0.88 -> 0.82 against 0.5 %);
     // ordered by row count, then signature
+    // (vector forms: 0.5 % -- their nine component-pair functions per class
+    // thrash the instruction cache beyond 8 classes: config 5 62.3 vs 66.3 ms)
     const char* frac_env = std::getenv("FF_CLASS_FRAC");  // tuning knob
-    const double frac = frac_env ? std::atof(frac_env) : 0.0005;
+    const double frac = frac_env ? std::atof(frac_env) : class_frac;
     const int64_t min_rows = std::max<int64_t>(min_class_rows, static_cast<int64_t>(frac * n_rows));
     std::vector<std::pair<int64_t, uint64_t>> big;
     for (size_t u = 0; u < usig.size(); ++u)
