@@ -175,13 +175,6 @@ int class_cwarps(const ff_form* f) {
   return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
 }
 
-// Items per warp of the class kernels (FF_IPW knob; 1: measured best for
-// scalar and vector forms).
-int class_ipw(const ff_form*) {
-  const char* v = std::getenv("FF_IPW");
-  return v ? std::max(1, std::atoi(v)) : 1;
-}
-
 // NVRTC-compiles the class-specialised gather kernels of (form, plan).
 void ensure_class_module(ff_form* f, ff_pattern* p) {
   if (p->gather.classes.empty()) return;
@@ -212,14 +205,13 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   if (!std::getenv("FF_CWARPS")) src = "#define FF_CWARPS " + std::to_string(class_cwarps(f)) + "\n" + src;
   // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
   // 82.6 ms at config 5, run 43)
-  if (!std::getenv("FF_IPW")) src = "#define FF_IPW " + std::to_string(class_ipw(f)) + "\n" + src;
-  // tuning knobs (defaults in the source): FF_IPW, FF_MINB_S, FF_MINB_L
+  // tuning knobs (defaults in the source): FF_MINB_S, FF_MINB_L
   // element records through L1: with records in first-touch order the lanes of
   // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
   // FF_EINV_NA=1 streams them past L1 (the round-1 default, -6 % before the
   // first-touch order)
   if (std::getenv("FF_EINV_NA") && f->ncomp == 1) src = "#define FF_EINV_NA 1\n" + src;
-  for (const char* knob : {"FF_IPW", "FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
+  for (const char* knob : {"FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
@@ -385,11 +377,10 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   auto launch_class = [&](int c, int64_t a, int64_t b, cudaStream_t sc) {
     long long i0 = a, i1 = b;
     if (i1 <= i0) return;
-    const int64_t ipw = class_ipw(f);
-    // FF_CWARPS warps x FF_IPW items per CTA; vector forms: one CTA per component pair
+    // FF_CWARPS warps x one item per CTA; vector forms: one CTA per component pair
     const int cw = class_cwarps(f);
     const int nb = f->ncomp * f->ncomp;
-    const int64_t ctas = (i1 - i0 + cw * ipw - 1) / (cw * ipw);
+    const int64_t ctas = (i1 - i0 + cw - 1) / cw;
     const unsigned grid = static_cast<unsigned>(ctas * nb);
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;

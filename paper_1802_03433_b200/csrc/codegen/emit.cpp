@@ -307,9 +307,6 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   }
   __syncwarp();
 }
-#ifndef FF_IPW
-#define FF_IPW 2  // consecutive items per warp
-#endif
 
 #ifndef FF_CWARPS
 #define FF_CWARPS 4  // warps per CTA
@@ -440,7 +437,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
 
   auto kernel = [&](const char* name, bool longrows) {
-    os << "// items of one launch: FF_IPW consecutive items per warp, CTAs in item order;\n"
+    os << "// items of one launch: one item per warp, CTAs in item order;\n"
           "// items are sorted by (Morton window, class): a CTA runs one class (small\n"
           "// instruction footprint per SM) and the items in flight stay spatially\n"
           "// compact (element data reused in L1/L2)\n"
@@ -461,53 +458,23 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  // 16/64/256 CTAs per pair measured 62.5/63.4/71.7 vs 62.5 ms at config 5)\n"
           "  const int cd = (int)(blockIdx.x % FF_NB);\n"
           "  const ff_i64 ff_cta = blockIdx.x / FF_NB;\n"
-          "  // items [first, last) of this warp (CTAs launch in item order, so the\n"
-          "  // items in flight stay contiguous; a persistent grid measured 3.2-3.6 vs\n"
-          "  // 2.09 ms at the north star)\n"
-          "  const ff_i64 first = i0 + (ff_cta * FF_CWARPS + wid) * FF_IPW;\n"
-          "  const ff_i64 last = first + FF_IPW < i1 ? first + FF_IPW : i1;\n"
-          "  if (first >= last) return;\n"
+          "  // one class item per warp (CTAs launch in item order, so the items in\n"
+          "  // flight stay contiguous): nothing carried across items -- two items per\n"
+          "  // warp with a two-stage item pipeline measured 2.053 vs 2.013 ms, a\n"
+          "  // persistent grid 3.2-3.6 ms at the north star\n"
+          "  const ff_i64 w = i0 + ff_cta * FF_CWARPS + wid;\n"
+          "  if (w >= i1) return;\n"
           "  // the item's first FF_PRE record ids sit at a position computable from the\n"
           "  // item index, so they load together with the item header (every class\n"
           "  // has >= FF_PRE steps); its other steps follow from citem_rec\n"
-          "  int c = __ldg(citem_class + first);\n"
-          "  int row = __ldg(citem_rows + first * 32 + lane);\n"
-          "  const ff_i32* rec = crec + __ldg(citem_rec + first) * 32 + lane;\n"
+          "  const int c = __ldg(citem_class + w);\n"
+          "  const int row = __ldg(citem_rows + w * 32 + lane);\n"
+          "  const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
           "  int ep[FF_PRE];\n"
           "#pragma unroll\n"
-          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(crec + (first * FF_PRE + u) * 32 + lane);\n"
-          "  ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
-          "#if FF_IPW > 1\n"
-          "  // two-stage item pipeline: while item w computes, the records and row\n"
-          "  // start of item w+1 load (addresses known one iteration ahead) and the\n"
-          "  // header of item w+2 loads -- no load waits on another at an item start\n"
-          "  // (one item per warp, vector forms: no lookahead -- the carried state\n"
-          "  // would spill at 255 registers)\n"
-          "  int c1 = 0, row1 = -1;\n"
-          "  ff_i64 r1 = 0;\n"
-          "  if (first + 1 < last) {\n"
-          "    c1 = __ldg(citem_class + first + 1);\n"
-          "    row1 = __ldg(citem_rows + (first + 1) * 32 + lane);\n"
-          "    r1 = __ldg(citem_rec + first + 1);\n"
-          "  }\n"
-          "#endif\n"
-          "  for (ff_i64 w = first; w < last; ++w) {\n"
-          "#if FF_IPW > 1\n"
-          "    const int cn = c1, rown = row1;\n"
-          "    const ff_i32* recn = crec + r1 * 32 + lane;\n"
-          "    int epn[FF_PRE];\n"
-          "    ff_i64 rbegn = 0;\n"
-          "    if (w + 1 < last) {\n"
-          "#pragma unroll\n"
-          "      for (int u = 0; u < FF_PRE; ++u) epn[u] = __ldcs(crec + ((w + 1) * FF_PRE + u) * 32 + lane);\n"
-          "      rbegn = rown >= 0 ? __ldg(row_ptr + rown) : 0;\n"
-          "    }\n"
-          "    if (w + 2 < last) {\n"
-          "      c1 = __ldg(citem_class + w + 2);\n"
-          "      row1 = __ldg(citem_rows + (w + 2) * 32 + lane);\n"
-          "      r1 = __ldg(citem_rec + w + 2);\n"
-          "    }\n"
-          "#endif\n"
+          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(crec + (w * FF_PRE + u) * 32 + lane);\n"
+          "  const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
+          "  {\n"
           "    switch (c * FF_NB + cd) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
       if (is_long(c) == longrows)
@@ -515,10 +482,6 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           os << "      case " << c * nb + cd << ": ff_cls_" << c << "_" << cd
              << "(ep, rec, einv, n_elems, st, sr, lane, rbeg, row, values, rhs); break;\n";
     os << "      default: break;\n    }\n"
-          "#if FF_IPW > 1\n"
-          "    c = cn;\n    row = rown;\n    rec = recn;\n    rbeg = rbegn;\n"
-          "#pragma unroll\n    for (int u = 0; u < FF_PRE; ++u) ep[u] = epn[u];\n"
-          "#endif\n"
           "  }\n}\n";
   };
   kernel("ff_gather_classes_s", false);
