@@ -661,15 +661,15 @@ std::optional<ElementPlan> plan_point_bilinear(const fem::InstantiatedForm& f, c
         os << "        const double ff_P" << b << " = " << e << ";\n";
       }
       for (int i = i0; i < i1; ++i) {
-        os << "        ff_a" << i << "_" << j << " += ";
-        bool first = true;
-        for (int b = 0; b < nu; ++b)
+        // K_ij += sum_b V_b(i) P_b(j) as a chain of fused multiply-adds into
+        // the accumulator (one DFMA per term, no separate product sum)
+        std::string e = "ff_a" + std::to_string(i) + "_" + std::to_string(j);
+        for (int b = nu - 1; b >= 0; --b)
           if (use_v[b]) {
-            os << (first ? "" : " + ") << "ff_v" << i << "_" << b << " * ff_P" << b;
-            first = false;
+            e = "fma(ff_v" + std::to_string(i) + "_" + std::to_string(b) + ", ff_P" + std::to_string(b) + ", " + e + ")";
             flops += 2;
           }
-        os << ";\n";
+        os << "        ff_a" << i << "_" << j << " = " << e << ";\n";
       }
       os << "      }\n";
     }
