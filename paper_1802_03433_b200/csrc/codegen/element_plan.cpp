@@ -595,7 +595,10 @@ std::optional<ElementPlan> plan_point_bilinear(const fem::InstantiatedForm& f, c
   plan.prelude = pre.str();
   std::ostringstream os;
   std::int64_t flops = 0;
-  const int nblk = (n + 4) / 5, R = (n + nblk - 1) / nblk;
+  // rows per register block (FF_PROWS tuning knob; default <= 5)
+  int rmax = 5;
+  if (const char* v = std::getenv("FF_PROWS")) rmax = std::max(1, std::atoi(v));
+  const int nblk = (n + rmax - 1) / rmax, R = (n + nblk - 1) / nblk;
   const char* refname[3] = {"xi", "eta", "zeta"};
   auto grad = [&](const std::string& base, int r) {  // (G grad_ref phi)_r from the table row `base`
     std::string e;
