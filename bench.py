@@ -326,7 +326,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-step-s", type=float, default=2.0)
-    ap.add_argument("--block", type=int, default=256)
+    ap.add_argument("--block", type=int, default=0, help="element-kernel CTA size (0: by body, 32 pointwise / 128)")
     ap.add_argument("--strategy", default="auto")
     ap.add_argument("--scatter", default="auto", choices=["auto", "gather", "atomic"],
                     help="auto: both scatters timed on this config before the run, the faster one kept")

@@ -63,7 +63,7 @@ typedef struct ff_form_desc {
   int degree;            /* Lagrange degree 1 or 2 */
   int quad_rule;         /* 0 = default (2D: reference 3-point rule; 3D: 4-point degree 2) */
   int strategy;          /* FF_STRATEGY_* */
-  int block_size;        /* threads per CTA of the element kernel; 0 = 256 */
+  int block_size;        /* threads per CTA of the element kernels; 0 = by body (pointwise 32, reference-tensor 128) */
   const char* bilinear;  /* integrand over u, u_x, u_y[, u_z], v, v_x, v_y[, v_z], x, y[, z] */
   const char* linear;    /* integrand over v, x, y[, z] */
 } ff_form_desc;

@@ -766,7 +766,7 @@ int ff_form_create(ff_ctx* ctx, const ff_form_desc* d, ff_form** out) {
     f->ctx = ctx;
     f->dim = d->dim;
     f->degree = d->degree;
-    f->block = d->block_size > 0 ? d->block_size : 256;
+    f->block = d->block_size > 0 ? d->block_size : 128;
     fem::WeakForm wf;
     wf.bilinear = symbolic::parse(d->bilinear);
     wf.linear = symbolic::parse(d->linear);
@@ -779,6 +779,17 @@ int ff_form_create(ff_ctx* ctx, const ff_form_desc* d, ff_form** out) {
     f->params.quad_rule = d->quad_rule;
     f->params.strategy = static_cast<codegen::Strategy>(d->strategy);
     f->params.n_local = f->n_local;
+    if (d->block_size <= 0) {
+      // CTA size of the element kernels, by body: the pointwise quadrature body
+      // needs ~254 registers, so its CTAs are one warp (config 4: 4.36 ms at 32
+      // threads, 4.59 at 128, 5.73 at 256); reference-tensor bodies 128 (K2a:
+      // NS 1.888 vs 1.901 ms, C2 0.493 vs 0.518 against 256)
+      const int rule_id = d->quad_rule > 0 ? d->quad_rule : codegen::default_quad_rule(d->dim, d->degree);
+      const codegen::ElementPlan plan =
+          codegen::plan_element(f->inst, fem::quadrature_rule(d->dim, rule_id), f->params.strategy);
+      f->block = plan.strategy == codegen::Strategy::Pointwise ? 32 : 128;
+      f->params.block_size = f->block;
+    }
     f->compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     build_variant(f.get(), 1);
     *out = f.release();

@@ -230,7 +230,7 @@ class Form:
 
     ctx=None compiles without a device (source/cubin/info only)."""
 
-    def __init__(self, ctx, dim, degree, bilinear, linear, quad_rule=0, strategy="auto", block_size=256):
+    def __init__(self, ctx, dim, degree, bilinear, linear, quad_rule=0, strategy="auto", block_size=0):
         d = _FormDesc(dim, degree, quad_rule, STRATEGY.get(strategy, strategy), block_size,
                       bilinear.encode(), linear.encode())
         h = _P()
