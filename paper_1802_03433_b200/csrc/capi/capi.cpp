@@ -203,8 +203,6 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   if (fused && !std::getenv("FF_MINB_S"))
     src = "#define FF_MINB_S " + std::to_string((f->ncomp > 1 ? 12 : 14) / class_cwarps(f)) + "\n" + src;
   if (!std::getenv("FF_CWARPS")) src = "#define FF_CWARPS " + std::to_string(class_cwarps(f)) + "\n" + src;
-  // vector forms: one item per warp (9 component-pair CTAs share it; 76.8 vs
-  // 82.6 ms at config 5, run 43)
   // tuning knobs (defaults in the source): FF_MINB_S, FF_MINB_L
   // element records through L1: with records in first-touch order the lanes of
   // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
