@@ -212,6 +212,9 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   for (const char* knob : {"FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
+  // FF_ABL (analysis only, wrong results): bit 1 no write-out, 2 no invariant
+  // loads, 4 synthetic record ids, 8 no load-vector loads
+  if (const char* v = std::getenv("FF_ABL")) src = "#define FF_ABL " + std::to_string(std::atoi(v)) + "\n" + src;
   const ffb::CompiledModule mod = ffb::nvrtc_compile(src, "femforge_classes.cu");
   bind(p->ctx);
   ffb::cuda_check(cudaLibraryLoadData(&p->class_lib, mod.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0),
@@ -742,8 +745,12 @@ int ff_class_source(const ff_form* f, int n, const int32_t* len, const int32_t* 
       }
       at += steps[c];
     }
+    // FF_CLASS_PRE (analysis hook): the record prefix the plan would pick
+    int pre = 1;
+    if (const char* v = std::getenv("FF_CLASS_PRE")) pre = std::max(1, std::min(8, std::atoi(v)));
+    for (const auto& c : rc) pre = std::min(pre, std::max(c.steps, 1));
     const std::string src = codegen::emit_class_source(f->plan, f->n_local, rc,
-                                                       std::getenv("FF_SPLIT_CLASSES") == nullptr, f->ncomp);
+                                                       std::getenv("FF_SPLIT_CLASSES") == nullptr, f->ncomp, pre);
     if (out_len) *out_len = src.size();
     if (buf && cap) {
       const std::size_t k = std::min(cap - 1, src.size());

@@ -246,6 +246,17 @@ __device__ __forceinline__ void ff_ld2(const double* p, double& a, double& b) {
 }
 __device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
 #endif
+#if defined(FF_ABL) && (FF_ABL & 8)  // ablation (timing analysis only; results wrong)
+#define ff_ld1(p) (1.0)
+#endif
+// record id loads (FF_ABL & 4: synthetic ids, ablation only)
+__device__ __forceinline__ int ff_ldid(const ff_i32* p) {
+#if defined(FF_ABL) && (FF_ABL & 4)
+  return (int)(((unsigned long long)p >> 7) & 0xfffff);
+#else
+  return __ldcs(p);
+#endif
+}
 )" << kInvariantLoad << R"(
 // element record: invariants (ff_load_inv), load vector [FF_NLOC][E]
 // (idle lanes, e < 0, only occur in rows that are never written: they read
@@ -254,7 +265,13 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
                                          double (&g)[FF_NKP], double& b) {
   const ff_i64 ee = e >= 0 ? e : 0;
   double t[FF_GS];
+#if defined(FF_ABL) && (FF_ABL & 2)  // ablation (timing analysis only; results wrong)
+#pragma unroll
+  for (int q = 0; q < FF_GS; ++q) t[q] = (double)(ee + q);
+  if (ee == -7) ff_load_inv(einv, n_elems, ee, t);
+#else
   ff_load_inv(einv, n_elems, ee, t);
+#endif
 #pragma unroll
   for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
   // entries b_0 .. b_{FF_NBPAD-1} came with the invariants (chunk-tail padding)
@@ -281,6 +298,10 @@ __device__ __forceinline__ void ff_stv(double* p, double v) {
 // class (one copy, not unrolled: keeps the instruction footprint small).
 __device__ __noinline__ void ff_writeout(const double* __restrict__ st, int sp, const ff_i64* __restrict__ sr,
                                          int lane, int cnt, int q0, double* __restrict__ values) {
+#if defined(FF_ABL) && (FF_ABL & 1)  // ablation (timing analysis only; results wrong)
+  if (lane < 0) values[0] = st[0];
+  return;
+#endif
   __syncwarp();
   if (lane < cnt) {
 #pragma unroll ff_wunroll
@@ -367,7 +388,8 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
     os << "// class " << c << " (components " << cc << ", " << dd << "): " << k.len << " entries, " << k.steps
        << " incidences, at most " << peak_live(k, n_local, order) << " open\n"
        << "__device__ __forceinline__ void ff_cls_" << c << "_" << cd
-       << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv, ff_i64 n_elems,\n"
+       << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec,\n"
+          "    const double* __restrict__ einv, ff_i64 n_elems,\n"
           "    double* __restrict__ st, ff_i64* __restrict__ sr, int lane, ff_i64 rbeg, int row,\n"
           "    double* __restrict__ values, double* __restrict__ rhs) {\n"
           "  int e[" << std::max(k.steps, 1) << "];\n";
@@ -375,12 +397,21 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
       if (t < pre)
         os << "  e[" << order[t] << "] = ep[" << t << "];\n";
       else
-        os << "  e[" << order[t] << "] = __ldcs(rec + " << (t - pre) * 32 << ");\n";
+        os << "  e[" << order[t] << "] = ff_ldid(rec + " << (t - pre) * 32 << ");\n";
     }
     if (dd == 0) os << "  double bs = 0.0;\n";
     for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
     os << ";\n";
-    os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd << " : -1;\n";
+    // the lane's CSR row start goes to shared memory right before the first
+    // write-out that reads it (it depends on the row_ptr load, which should not
+    // hold up the staging stores before it)
+    bool sr_done = false;
+    auto store_sr = [&](const char* indent) {
+      if (sr_done) return;
+      sr_done = true;
+      os << indent << "sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len + dd
+         << " : -1;\n";
+    };
     // record loads in flight per batch (registers: depth x the record size)
     const char* dk = bs == 1 ? std::getenv("FF_SDEPTH") : std::getenv("FF_VDEPTH");
     const int depth = dk ? std::max(1, std::atoi(dk)) : (bs == 1 ? 8 : 2);
@@ -390,7 +421,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
       for (int t = t0; t < t1; ++t) {
         const int q = order[t];
         os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] * bs + cc
-           << ", einv, n_elems, g" << q << ", b" << q << ");\n";
+             << ", einv, n_elems, g" << q << ", b" << q << ");\n";
       }
       for (int t = t0; t < t1; ++t) {
         const int q = order[t];
@@ -414,9 +445,12 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           for (int f : closing) {
             const int sl = slot_of_fin[f];
             os << " st[lane * " << sp << " + " << pos[sl] % 32 << "] = a" << sl << ";";
-            if (f % 32 == 31 || f == k.len - 1)  // chunk f / 32 complete
-              os << "\n      ff_writeout_map(st, " << sp << ", sr, lane, " << f % 32 + 1 << ", ff_cmap_" << c << " + "
+            if (f % 32 == 31 || f == k.len - 1) {  // chunk f / 32 complete
+              os << "\n";
+              store_sr("      ");
+              os << "      ff_writeout_map(st, " << sp << ", sr, lane, " << f % 32 + 1 << ", ff_cmap_" << c << " + "
                  << f - f % 32 << ", values);";
+            }
           }
         }
         os << " }\n";
@@ -426,6 +460,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
     }
     // write-out through the staging rows (consecutive lanes = consecutive CSR
     // values of one row)
+    if (!chunked) store_sr("  ");
     if (!chunked)
       for (int q0 = 0; q0 < k.len; q0 += 32)
         os << "  ff_writeout(st + " << q0 << ", " << sp << ", sr, lane, " << std::min(32, k.len - q0) << ", " << q0
@@ -467,13 +502,16 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
           "  // the item's first FF_PRE record ids sit at a position computable from the\n"
           "  // item index, so they load together with the item header (every class\n"
           "  // has >= FF_PRE steps); its other steps follow from citem_rec\n"
+          "  // (the record ids first: their loads must not queue behind the first\n"
+          "  // use of the header; the row start loads unpredicated for the same reason)\n"
+          "  int ep[FF_PRE];\n"
+          "#pragma unroll\n"
+          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = ff_ldid(crec + (w * FF_PRE + u) * 32 + lane);\n"
           "  const int c = __ldg(citem_class + w);\n"
           "  const int row = __ldg(citem_rows + w * 32 + lane);\n"
           "  const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
-          "  int ep[FF_PRE];\n"
-          "#pragma unroll\n"
-          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = __ldcs(crec + (w * FF_PRE + u) * 32 + lane);\n"
-          "  const ff_i64 rbeg = row >= 0 ? __ldg(row_ptr + row) : 0;\n"
+          "  const ff_i64 rbeg = __ldg(row_ptr + (row >= 0 ? row : 0));\n"
+
           "  {\n"
           "    switch (c * FF_NB + cd) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
