@@ -21,6 +21,7 @@
 //    subexpressions are computed once per element).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <optional>
 #include <set>
@@ -211,6 +212,125 @@ std::string emit_call(const Entry& en, const std::string& v) {
 // ---------------------------------------------------------------------------
 // ReferenceTensor
 
+// Row-gather record of a vector form: per (test, trial) component block, a
+// basis of the block's entries. An elasticity diagonal block reads 18
+// invariants (2 M^cc + sum_p M^pp over the det G_pr G_ps) whose coefficient
+// columns span only 6 dimensions: with a basis of 6 quantities every entry is
+// <= 6 terms instead of <= 18 and a sub-row loads 2 of the record's 32-byte
+// groups instead of up to 5. Column selection keeps the reference-tensor
+// coefficients: pick independent coefficient columns S of the block
+// (sparsest first; Gram-Schmidt in long double), express every invariant's
+// column through them (col_t = sum_k X_kt col_S_k), then quantity
+// b_k = sum_t X_kt inv_t and entry (i, j) = sum_k C_ij,S_k b_k. Blocks whose
+// invariants are already independent keep them (X = identity), and equal
+// quantities are shared between blocks ((c, d) and (d, c)). Output: qsig[q] =
+// quantity q over the invariants, rep[r] = entry r over the quantities; both
+// empty (one quantity per invariant) when a block is not reproduced to 1e-13.
+void block_basis(const std::vector<std::vector<std::pair<int, double>>>& row_sig, int nt, int n_local, int bs,
+                 std::vector<std::vector<std::pair<int, double>>>& qsig,
+                 std::vector<std::vector<std::pair<int, double>>>& rep) {
+  using V = std::vector<long double>;
+  const int nn = n_local * n_local;
+  auto dot = [](const V& a, const V& b) {
+    long double s = 0.0L;
+    for (std::size_t t = 0; t < a.size(); ++t) s += a[t] * b[t];
+    return s;
+  };
+  auto norm = [&](const V& a) { return std::sqrt(dot(a, a)); };
+  auto fail = [&]() {
+    qsig.clear();
+    rep.assign(nn, {});
+  };
+  std::map<std::vector<std::pair<int, double>>, int> qid;
+  qsig.clear();
+  rep.assign(nn, {});
+  for (int blk = 0; blk < bs * bs; ++blk) {
+    std::vector<int> rows;
+    for (int r = 0; r < nn; ++r)
+      if (((r / n_local) % bs) * bs + (r % n_local) % bs == blk && !row_sig[r].empty()) rows.push_back(r);
+    if (rows.empty()) continue;
+    const int m = static_cast<int>(rows.size());
+    // coefficient columns of the block's invariants (over its entries)
+    std::map<int, V> col;
+    for (int i = 0; i < m; ++i)
+      for (const auto& [t, c] : row_sig[rows[i]]) {
+        auto& v = col[t];
+        v.resize(m, 0.0L);
+        v[i] = c;
+      }
+    std::vector<std::pair<int, int>> cand;  // (nonzeros, t)
+    for (const auto& [t, v] : col) {
+      int nz = 0;
+      for (long double x : v) nz += x != 0.0L;
+      cand.push_back({nz, t});
+    }
+    std::sort(cand.begin(), cand.end());
+    std::vector<int> S;
+    std::vector<V> U;  // orthonormalised selected columns
+    for (const auto& [nz, t] : cand) {
+      V w = col[t];
+      for (int pass = 0; pass < 2; ++pass)
+        for (const V& u : U) {
+          const long double d = dot(w, u);
+          for (int i = 0; i < m; ++i) w[i] -= d * u[i];
+        }
+      const long double nw = norm(w);
+      if (nw <= 1e-11L * norm(col[t])) continue;
+      for (auto& x : w) x /= nw;
+      U.push_back(w);
+      S.push_back(t);
+    }
+    const int k = static_cast<int>(S.size());
+    // X[:, t]: col_t over the selected columns (normal equations, k x k)
+    std::map<int, V> X;
+    for (const auto& [t, v] : col) {
+      std::vector<V> G(k, V(k + 1, 0.0L));
+      for (int a = 0; a < k; ++a) {
+        for (int b = 0; b < k; ++b) G[a][b] = dot(col[S[a]], col[S[b]]);
+        G[a][k] = dot(col[S[a]], v);
+      }
+      for (int c = 0; c < k; ++c) {  // Gauss-Jordan, partial pivoting
+        int pv = c;
+        for (int a = c + 1; a < k; ++a)
+          if (std::fabs(G[a][c]) > std::fabs(G[pv][c])) pv = a;
+        std::swap(G[c], G[pv]);
+        for (int a = 0; a < k; ++a) {
+          if (a == c || G[a][c] == 0.0L) continue;
+          const long double fct = G[a][c] / G[c][c];
+          for (int b = c; b <= k; ++b) G[a][b] -= fct * G[c][b];
+        }
+      }
+      V x(k);
+      for (int a = 0; a < k; ++a) x[a] = G[a][k] / G[a][a];
+      // exact reconstruction of the column
+      V res = v;
+      for (int a = 0; a < k; ++a)
+        for (int i = 0; i < m; ++i) res[i] -= x[a] * col[S[a]][i];
+      if (norm(res) > 1e-13L * norm(v)) return fail();
+      X[t] = x;
+    }
+    // quantities b_a = sum_t X[a][t] inv_t (shared when equal)
+    std::vector<int> q_of(k);
+    for (int a = 0; a < k; ++a) {
+      long double mx = 0.0L;
+      for (const auto& [t, x] : X) mx = std::max(mx, std::fabs(x[a]));
+      std::vector<std::pair<int, double>> sig;
+      for (const auto& [t, x] : X)
+        if (std::fabs(x[a]) > 1e-14L * mx) sig.push_back({t, static_cast<double>(x[a])});
+      auto [it, fresh] = qid.emplace(sig, static_cast<int>(qsig.size()));
+      if (fresh) qsig.push_back(sig);
+      q_of[a] = it->second;
+    }
+    // entries over the quantities: their own coefficients of the selected columns
+    for (int i = 0; i < m; ++i) {
+      const int r = rows[i];
+      for (int a = 0; a < k; ++a)
+        if (col[S[a]][i] != 0.0L) rep[r].push_back({q_of[a], static_cast<double>(col[S[a]][i])});
+      std::sort(rep[r].begin(), rep[r].end());
+    }
+  }
+}
+
 std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
   PolyBuilder pb;
   std::vector<Expr> integrands = f.geo_bilinear;
@@ -356,10 +476,66 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
   }
   // row-gather split: invariants read by the bilinear entries, in t order
   const int nn = f.n_local * f.n_local;
+  // vector forms: per-block record quantities (block_basis); empty -> one
+  // record quantity per invariant
+  std::vector<std::vector<std::pair<int, double>>> qsig, rep;
+  if (f.ncomp > 1 && !std::getenv("FF_NO_BLOCK_BASIS"))
+    block_basis(row_sig, static_cast<int>(inv.size()), f.n_local, f.ncomp, qsig, rep);
   std::map<int, int> kq;
-  for (int r = 0; r < nn; ++r)
+  for (int r = 0; r < nn && qsig.empty(); ++r)
     for (const auto& [t, c] : row_sig[r]) kq.emplace(t, 0);
-  {
+  if (!qsig.empty()) {
+    // record quantity q = sum_t c_t inv_t (a pivot entry's expression, as the
+    // element body computes that entry)
+    plan.n_kinv = static_cast<int>(qsig.size());
+    for (std::size_t q = 0; q < qsig.size(); ++q) {
+      std::string v;
+      for (std::size_t u = 0; u < qsig[q].size(); ++u) {
+        const double c = qsig[q][u].second;
+        const std::string t = "ff_t" + std::to_string(qsig[q][u].first);
+        if (u == 0)
+          v = c == 1.0 ? t : c == -1.0 ? "-" + t : double_literal(c) + " * " + t;
+        else
+          v += c == 1.0 ? " + " + t : c == -1.0 ? " - " + t : " + " + double_literal(c) + " * " + t;
+        flops += 2;
+      }
+      os << "  FF_KINV(" << q << ", " << (v.empty() ? "0.0" : v) << ");\n";
+    }
+    std::ostringstream rc;
+    std::map<double, int> coef;
+    std::vector<double> coefs;
+    auto cref = [&](double c) {
+      auto [it, fresh] = coef.emplace(c, static_cast<int>(coefs.size()));
+      if (fresh) coefs.push_back(c);
+      return "ff_kc[" + std::to_string(it->second) + "]";
+    };
+    std::ostringstream body;
+    for (int i = 0; i < f.n_local; ++i) {
+      body << "template <> __device__ __forceinline__ void ff_row<" << i
+           << ">(const double* __restrict__ g, double* __restrict__ v) {\n";
+      for (int j = 0; j < f.n_local; ++j) {
+        const auto& sig = rep[i * f.n_local + j];
+        std::string v = sig.empty() ? "0.0" : "";
+        for (std::size_t q = 0; q < sig.size(); ++q) {
+          const double c = sig[q].second;
+          const std::string t = "g[" + std::to_string(sig[q].first) + "]";
+          if (q == 0)
+            v = c == 1.0 ? t : c == -1.0 ? "-" + t : cref(c) + " * " + t;
+          else
+            v += c == 1.0 ? " + " + t : c == -1.0 ? " - " + t : " + " + cref(c) + " * " + t;
+          plan.row_flops += 2;
+        }
+        body << "  v[" << j << "] = " << v << ";\n";
+      }
+      body << "}\n";
+    }
+    rc << "__constant__ double ff_kc[" << std::max<std::size_t>(coefs.size(), 1) << "] = {";
+    for (std::size_t q = 0; q < coefs.size(); ++q) rc << (q ? ", " : "") << double_literal(coefs[q]);
+    if (coefs.empty()) rc << "0.0";
+    rc << "};\n" << body.str();
+    plan.row_code = rc.str();
+  }
+  if (qsig.empty()) {
     // vector forms: invariants ordered by the first (test, trial) component
     // block that reads them, so the row gather of one block loads a few
     // contiguous 32-byte groups of the element record
@@ -377,15 +553,15 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
     std::sort(keyed.begin(), keyed.end());
     int q = 0;
     for (const auto& [blk, t] : keyed) kq[t] = q++;
+    plan.n_kinv = static_cast<int>(kq.size());
   }
-  plan.n_kinv = static_cast<int>(kq.size());
-  {
+  if (qsig.empty()) {
     std::vector<std::pair<int, int>> by_q;
     for (const auto& [t, q] : kq) by_q.push_back({q, t});
     std::sort(by_q.begin(), by_q.end());
     for (const auto& [q, t] : by_q) os << "  FF_KINV(" << q << ", ff_t" << t << ");\n";
   }
-  {
+  if (qsig.empty()) {
     // ff_row<i>: v[j] = K_ij with the same expression (term order, literals)
     // as the element body, so both scatters compute bit-identical entries
     // coefficients live in a __constant__ table so the fp64 FMAs read them as
