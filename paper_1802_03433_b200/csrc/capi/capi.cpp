@@ -276,7 +276,7 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
                                                         std::getenv("FF_SPLIT_CLASSES") != nullptr, &order_fn,
-                                                        p->bs > 1 ? 0.005 : 0.0005);
+                                                        0.0005);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");

@@ -775,8 +775,8 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     // warp they are as cheap as interior rows, while the generic gather costs
     // ~3x per row -- NS 2.00 -> 1.89 ms, C3 0.88 -> 0.82 against 0.5 %);
     // ordered by row count, then signature
-    // (vector forms: 0.5 % -- their nine component-pair functions per class
-    // thrash the instruction cache beyond 8 classes: config 5 62.3 vs 66.3 ms)
+    // (vector forms too since their per-block record quantities: config 5
+    // 49.6 ms with 32 classes vs 51.0 with 8 at 0.5 %)
     const char* frac_env = std::getenv("FF_CLASS_FRAC");  // tuning knob
     const double frac = frac_env ? std::atof(frac_env) : class_frac;
     const int64_t min_rows = std::max<int64_t>(min_class_rows, static_cast<int64_t>(frac * n_rows));
