@@ -172,7 +172,7 @@ void free_gather(ff_pattern* p) {
 
 int class_cwarps(const ff_form* f) {
   const char* v = std::getenv("FF_CWARPS");
-  return v ? std::max(1, std::min(8, std::atoi(v))) : (f->ncomp > 1 ? 4 : 2);
+  return v ? std::max(1, std::min(8, std::atoi(v))) : 2;
 }
 
 // NVRTC-compiles the class-specialised gather kernels of (form, plan).
@@ -195,7 +195,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   const auto t0 = std::chrono::steady_clock::now();
   // one fused kernel for every class unless FF_SPLIT_CLASSES:
   // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
-  const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr;
+  const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr || f->ncomp > 1;
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp, p->gather.pre_steps);
   // register budget: 14 warps/SM for scalar forms (one item per warp: no
   // carried item state; NS 2.013 vs 2.038 ms at 12 warps, 2.053 with two items
@@ -222,7 +222,7 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[0], p->class_lib, "ff_gather_classes_s"), "class kernel");
   ffb::cuda_check(cudaLibraryGetKernel(&p->class_kernel[1], p->class_lib, "ff_gather_classes_l"), "class kernel");
   for (int c = 0; c < 2; ++c) {
-    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused, class_cwarps(f));
+    p->class_smem[c] = codegen::class_shared_bytes(rc, c, fused, class_cwarps(f), f->ncomp);
     ffb::cuda_check(cudaKernelSetAttributeForDevice(p->class_kernel[c], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     p->class_smem[c], p->ctx->device),
                     "class kernel shared memory attribute");
@@ -275,8 +275,8 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
-                                                        std::getenv("FF_SPLIT_CLASSES") != nullptr, &order_fn,
-                                                        0.0005);
+                                                        std::getenv("FF_SPLIT_CLASSES") != nullptr && p->bs == 1,
+                                                        &order_fn, 0.0005, p->bs);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
     check_alloc(e, "row-gather plan");
@@ -378,11 +378,10 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   auto launch_class = [&](int c, int64_t a, int64_t b, cudaStream_t sc) {
     long long i0 = a, i1 = b;
     if (i1 <= i0) return;
-    // FF_CWARPS warps x one item per CTA; vector forms: one CTA per component pair
+    // FF_CWARPS warps x one item per CTA; vector forms: one CTA per test component
     const int cw = class_cwarps(f);
-    const int nb = f->ncomp * f->ncomp;
     const int64_t ctas = (i1 - i0 + cw - 1) / cw;
-    const unsigned grid = static_cast<unsigned>(ctas * nb);
+    const unsigned grid = static_cast<unsigned>(ctas * f->ncomp);
     const double* ginv = p->ginv;
     long long ne_arg = m->ne;
     const int64_t* row_ptr = p->row_ptr;

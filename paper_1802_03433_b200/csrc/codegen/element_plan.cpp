@@ -21,11 +21,13 @@
 //    subexpressions are computed once per element).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <optional>
 #include <set>
 #include <sstream>
+#include <tuple>
 #include <unordered_map>
 
 #include "femforge/codegen.hpp"
@@ -212,123 +214,140 @@ std::string emit_call(const Entry& en, const std::string& v) {
 // ---------------------------------------------------------------------------
 // ReferenceTensor
 
-// Row-gather record of a vector form: per (test, trial) component block, a
-// basis of the block's entries. An elasticity diagonal block reads 18
-// invariants (2 M^cc + sum_p M^pp over the det G_pr G_ps) whose coefficient
-// columns span only 6 dimensions: with a basis of 6 quantities every entry is
-// <= 6 terms instead of <= 18 and a sub-row loads 2 of the record's 32-byte
-// groups instead of up to 5. Column selection keeps the reference-tensor
-// coefficients: pick independent coefficient columns S of the block
-// (sparsest first; Gram-Schmidt in long double), express every invariant's
-// column through them (col_t = sum_k X_kt col_S_k), then quantity
-// b_k = sum_t X_kt inv_t and entry (i, j) = sum_k C_ij,S_k b_k. Blocks whose
-// invariants are already independent keep them (X = identity), and equal
-// quantities are shared between blocks ((c, d) and (d, c)). Output: qsig[q] =
-// quantity q over the invariants, rep[r] = entry r over the quantities; both
-// empty (one quantity per invariant) when a block is not reproduced to 1e-13.
-void block_basis(const std::vector<std::vector<std::pair<int, double>>>& row_sig, int nt, int n_local, int bs,
-                 std::vector<std::vector<std::pair<int, double>>>& qsig,
-                 std::vector<std::vector<std::pair<int, double>>>& rep) {
+// Row-gather record of a vector form, block-uniform: every (test c, trial d)
+// component block's entries are ONE linear map alpha of that block's own
+// n_bq record quantities, entry ((a,c),(b,d)) = sum_k alpha[a,b][k] q[block_q[c,d] + k].
+// alpha's columns are coefficient columns C[(a,c),(b,d)], t of the blocks'
+// invariants (sparsest first, Gram-Schmidt in long double) spanning the union
+// of the blocks' column spaces (elasticity: the 6 reference tensors
+// A^rs_ab + A^sr_ab); every invariant column of block B is expressed through
+// them (col = sum_k X_k alpha_k, checked to 1e-13), so the block's quantity
+// k is sum_t X^B_kt inv_t. An elasticity diagonal block then reads 6
+// quantities instead of 18 invariants, every block's entries are <= 6 terms,
+// and one code path (ff_vrow<a>) serves all nine blocks: the row gather runs
+// the three trial components of a row in neighbouring lanes. Blocks with equal
+// quantities share them ((c, d) and (d, c) for lambda = mu); block offsets are
+// even (32-byte chunks hold whole pairs). Returns false when the union basis
+// exceeds 16 columns or a column is not reproduced.
+struct UniformBasis {
+  std::vector<std::vector<std::pair<int, double>>> qsig;   // quantity -> invariants
+  std::vector<std::vector<std::pair<int, double>>> rep;    // entry -> quantities
+  std::vector<std::vector<std::pair<int, double>>> alpha;  // node pair (a, b) -> basis column k
+  std::vector<int> block_q;                                 // [bs * bs] quantity offsets
+  int n_bq = 0;                                             // quantities per block (even)
+};
+bool uniform_block_basis(const std::vector<std::vector<std::pair<int, double>>>& row_sig, int n_local, int bs,
+                         UniformBasis& out) {
   using V = std::vector<long double>;
-  const int nn = n_local * n_local;
-  auto dot = [](const V& a, const V& b) {
+  const int nn = n_local * n_local, nsc = n_local / bs, np = nsc * nsc, nb = bs * bs;
+  auto dot = [](const V& x, const V& y) {
     long double s = 0.0L;
-    for (std::size_t t = 0; t < a.size(); ++t) s += a[t] * b[t];
+    for (std::size_t t = 0; t < x.size(); ++t) s += x[t] * y[t];
     return s;
   };
-  auto norm = [&](const V& a) { return std::sqrt(dot(a, a)); };
-  auto fail = [&]() {
-    qsig.clear();
-    rep.assign(nn, {});
-  };
-  std::map<std::vector<std::pair<int, double>>, int> qid;
-  qsig.clear();
-  rep.assign(nn, {});
-  for (int blk = 0; blk < bs * bs; ++blk) {
-    std::vector<int> rows;
-    for (int r = 0; r < nn; ++r)
-      if (((r / n_local) % bs) * bs + (r % n_local) % bs == blk && !row_sig[r].empty()) rows.push_back(r);
-    if (rows.empty()) continue;
-    const int m = static_cast<int>(rows.size());
-    // coefficient columns of the block's invariants (over its entries)
-    std::map<int, V> col;
-    for (int i = 0; i < m; ++i)
-      for (const auto& [t, c] : row_sig[rows[i]]) {
-        auto& v = col[t];
-        v.resize(m, 0.0L);
-        v[i] = c;
-      }
-    std::vector<std::pair<int, int>> cand;  // (nonzeros, t)
-    for (const auto& [t, v] : col) {
-      int nz = 0;
-      for (long double x : v) nz += x != 0.0L;
-      cand.push_back({nz, t});
-    }
-    std::sort(cand.begin(), cand.end());
-    std::vector<int> S;
-    std::vector<V> U;  // orthonormalised selected columns
-    for (const auto& [nz, t] : cand) {
-      V w = col[t];
-      for (int pass = 0; pass < 2; ++pass)
-        for (const V& u : U) {
-          const long double d = dot(w, u);
-          for (int i = 0; i < m; ++i) w[i] -= d * u[i];
-        }
-      const long double nw = norm(w);
-      if (nw <= 1e-11L * norm(col[t])) continue;
-      for (auto& x : w) x /= nw;
-      U.push_back(w);
-      S.push_back(t);
-    }
-    const int k = static_cast<int>(S.size());
-    // X[:, t]: col_t over the selected columns (normal equations, k x k)
-    std::map<int, V> X;
-    for (const auto& [t, v] : col) {
-      std::vector<V> G(k, V(k + 1, 0.0L));
-      for (int a = 0; a < k; ++a) {
-        for (int b = 0; b < k; ++b) G[a][b] = dot(col[S[a]], col[S[b]]);
-        G[a][k] = dot(col[S[a]], v);
-      }
-      for (int c = 0; c < k; ++c) {  // Gauss-Jordan, partial pivoting
-        int pv = c;
-        for (int a = c + 1; a < k; ++a)
-          if (std::fabs(G[a][c]) > std::fabs(G[pv][c])) pv = a;
-        std::swap(G[c], G[pv]);
-        for (int a = 0; a < k; ++a) {
-          if (a == c || G[a][c] == 0.0L) continue;
-          const long double fct = G[a][c] / G[c][c];
-          for (int b = c; b <= k; ++b) G[a][b] -= fct * G[c][b];
-        }
-      }
-      V x(k);
-      for (int a = 0; a < k; ++a) x[a] = G[a][k] / G[a][a];
-      // exact reconstruction of the column
-      V res = v;
-      for (int a = 0; a < k; ++a)
-        for (int i = 0; i < m; ++i) res[i] -= x[a] * col[S[a]][i];
-      if (norm(res) > 1e-13L * norm(v)) return fail();
-      X[t] = x;
-    }
-    // quantities b_a = sum_t X[a][t] inv_t (shared when equal)
-    std::vector<int> q_of(k);
-    for (int a = 0; a < k; ++a) {
-      long double mx = 0.0L;
-      for (const auto& [t, x] : X) mx = std::max(mx, std::fabs(x[a]));
-      std::vector<std::pair<int, double>> sig;
-      for (const auto& [t, x] : X)
-        if (std::fabs(x[a]) > 1e-14L * mx) sig.push_back({t, static_cast<double>(x[a])});
-      auto [it, fresh] = qid.emplace(sig, static_cast<int>(qsig.size()));
-      if (fresh) qsig.push_back(sig);
-      q_of[a] = it->second;
-    }
-    // entries over the quantities: their own coefficients of the selected columns
-    for (int i = 0; i < m; ++i) {
-      const int r = rows[i];
-      for (int a = 0; a < k; ++a)
-        if (col[S[a]][i] != 0.0L) rep[r].push_back({q_of[a], static_cast<double>(col[S[a]][i])});
-      std::sort(rep[r].begin(), rep[r].end());
+  auto norm = [&](const V& x) { return std::sqrt(dot(x, x)); };
+  // coefficient column of invariant t in block B, over the node pairs (a, b)
+  std::vector<std::map<int, V>> col(nb);
+  for (int r = 0; r < nn; ++r) {
+    const int i = r / n_local, j = r % n_local;
+    const int blk = (i % bs) * bs + j % bs, u = (i / bs) * nsc + j / bs;
+    for (const auto& [t, c] : row_sig[r]) {
+      auto& v = col[blk][t];
+      v.resize(np, 0.0L);
+      v[u] = c;
     }
   }
+  std::vector<std::tuple<int, int, int>> cand;  // (nonzeros, block, t)
+  for (int blk = 0; blk < nb; ++blk)
+    for (const auto& [t, v] : col[blk]) {
+      int nz = 0;
+      for (long double x : v) nz += x != 0.0L;
+      cand.push_back({nz, blk, t});
+    }
+  std::sort(cand.begin(), cand.end());
+  std::vector<V> A, U;  // basis columns, orthonormalised
+  for (const auto& [nz, blk, t] : cand) {
+    const V& c = col[blk][t];
+    V w = c;
+    for (int pass = 0; pass < 2; ++pass)
+      for (const V& q : U) {
+        const long double d = dot(w, q);
+        for (int u = 0; u < np; ++u) w[u] -= d * q[u];
+      }
+    const long double nw = norm(w);
+    if (nw <= 1e-11L * norm(c)) continue;
+    for (auto& x : w) x /= nw;
+    U.push_back(w);
+    A.push_back(c);
+  }
+  const int k = static_cast<int>(A.size());
+  if (std::getenv("FF_PLAN_DEBUG")) std::fprintf(stderr, "[plan] uniform block basis: %d columns\n", k);
+  if (k == 0 || k > 16) return false;
+  // normal equations of the basis (k x k), inverted once (Gauss-Jordan)
+  std::vector<V> G(k, V(2 * k, 0.0L));
+  for (int x = 0; x < k; ++x) {
+    for (int y = 0; y < k; ++y) G[x][y] = dot(A[x], A[y]);
+    G[x][k + x] = 1.0L;
+  }
+  for (int c = 0; c < k; ++c) {
+    int pv = c;
+    for (int x = c + 1; x < k; ++x)
+      if (std::fabs(G[x][c]) > std::fabs(G[pv][c])) pv = x;
+    std::swap(G[c], G[pv]);
+    const long double d = G[c][c];
+    for (auto& e : G[c]) e /= d;
+    for (int x = 0; x < k; ++x) {
+      if (x == c || G[x][c] == 0.0L) continue;
+      const long double fct = G[x][c];
+      for (int y = 0; y < 2 * k; ++y) G[x][y] -= fct * G[c][y];
+    }
+  }
+  out = UniformBasis{};
+  out.n_bq = k + (k & 1);
+  out.block_q.assign(nb, 0);
+  std::map<std::vector<std::vector<std::pair<int, double>>>, int> seen;
+  for (int blk = 0; blk < nb; ++blk) {
+    // X[t] = G^-1 A^T col_t, the block's invariant columns over the basis
+    std::vector<std::vector<std::pair<int, double>>> qs(out.n_bq);
+    std::map<int, V> X;
+    for (const auto& [t, c] : col[blk]) {
+      V rhs(k), x(k, 0.0L);
+      for (int y = 0; y < k; ++y) rhs[y] = dot(A[y], c);
+      for (int y = 0; y < k; ++y)
+        for (int z = 0; z < k; ++z) x[y] += G[y][k + z] * rhs[z];
+      V res = c;
+      for (int y = 0; y < k; ++y)
+        for (int u = 0; u < np; ++u) res[u] -= x[y] * A[y][u];
+      if (norm(res) > 1e-13L * norm(c)) {
+        if (std::getenv("FF_PLAN_DEBUG"))
+          std::fprintf(stderr, "[plan] block %d invariant %d residual %Lg\n", blk, t, norm(res) / norm(c));
+        return false;
+      }
+      X[t] = x;
+    }
+    for (int y = 0; y < k; ++y) {
+      long double mx = 0.0L;
+      for (const auto& [t, x] : X) mx = std::max(mx, std::fabs(x[y]));
+      for (const auto& [t, x] : X)
+        if (std::fabs(x[y]) > 1e-14L * mx) qs[y].push_back({t, static_cast<double>(x[y])});
+    }
+    auto [it, fresh] = seen.emplace(qs, static_cast<int>(out.qsig.size()));
+    if (fresh) out.qsig.insert(out.qsig.end(), qs.begin(), qs.end());
+    out.block_q[blk] = it->second;
+  }
+  out.alpha.assign(np, {});
+  for (int u = 0; u < np; ++u)
+    for (int y = 0; y < k; ++y)
+      if (A[y][u] != 0.0L) out.alpha[u].push_back({y, static_cast<double>(A[y][u])});
+  out.rep.assign(nn, {});
+  for (int r = 0; r < nn; ++r) {
+    const int i = r / n_local, j = r % n_local;
+    const int blk = (i % bs) * bs + j % bs, u = (i / bs) * nsc + j / bs;
+    if (row_sig[r].empty()) continue;
+    for (const auto& [y, a] : out.alpha[u])
+      if (!out.qsig[out.block_q[blk] + y].empty()) out.rep[r].push_back({out.block_q[blk] + y, a});
+  }
+  return true;
 }
 
 std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule) {
@@ -479,8 +498,13 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
   // vector forms: per-block record quantities (block_basis); empty -> one
   // record quantity per invariant
   std::vector<std::vector<std::pair<int, double>>> qsig, rep;
-  if (f.ncomp > 1 && !std::getenv("FF_NO_BLOCK_BASIS"))
-    block_basis(row_sig, static_cast<int>(inv.size()), f.n_local, f.ncomp, qsig, rep);
+  UniformBasis ub;
+  if (f.ncomp > 1 && uniform_block_basis(row_sig, f.n_local, f.ncomp, ub)) {
+    qsig = ub.qsig;
+    rep = ub.rep;
+    plan.n_bq = ub.n_bq;
+    plan.block_q = ub.block_q;
+  }
   std::map<int, int> kq;
   for (int r = 0; r < nn && qsig.empty(); ++r)
     for (const auto& [t, c] : row_sig[r]) kq.emplace(t, 0);
@@ -529,10 +553,36 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
       }
       body << "}\n";
     }
+    // ff_vrow<a>: v[b] = entry ((a, c), (b, d)) of any block from that
+    // block's quantities g[0 .. n_bq)
+    const int nsc = f.n_local / f.ncomp;
+    for (int a = 0; a < nsc; ++a) {
+      body << "template <> __device__ __forceinline__ void ff_vrow<" << a
+           << ">(const double* __restrict__ g, double* __restrict__ v) {\n";
+      for (int b = 0; b < nsc; ++b) {
+        const auto& sig = ub.alpha[a * nsc + b];
+        std::string v = sig.empty() ? "0.0" : "";
+        for (std::size_t q = 0; q < sig.size(); ++q) {
+          const double c = sig[q].second;
+          const std::string t = "g[" + std::to_string(sig[q].first) + "]";
+          if (q == 0)
+            v = c == 1.0 ? t : c == -1.0 ? "-" + t : cref(c) + " * " + t;
+          else
+            v += c == 1.0 ? " + " + t : c == -1.0 ? " - " + t : " + " + cref(c) + " * " + t;
+        }
+        body << "  v[" << b << "] = " << v << ";\n";
+      }
+      body << "}\n";
+    }
     rc << "__constant__ double ff_kc[" << std::max<std::size_t>(coefs.size(), 1) << "] = {";
     for (std::size_t q = 0; q < coefs.size(); ++q) rc << (q ? ", " : "") << double_literal(coefs[q]);
     if (coefs.empty()) rc << "0.0";
-    rc << "};\n" << body.str();
+    rc << "};\n";
+    rc << "template <int A>\n__device__ __forceinline__ void ff_vrow(const double* __restrict__ g, double* __restrict__ v);\n";
+    rc << "// quantity offset of component block (c, d) in the element record\n__constant__ int ff_block_q["
+       << plan.block_q.size() << "] = {";
+    for (std::size_t q = 0; q < plan.block_q.size(); ++q) rc << (q ? ", " : "") << plan.block_q[q];
+    rc << "};\n#define FF_NBQ " << plan.n_bq << "\n" << body.str();
     plan.row_code = rc.str();
   }
   if (qsig.empty()) {

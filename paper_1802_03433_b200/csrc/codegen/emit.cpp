@@ -113,7 +113,7 @@ bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_s
   // vector forms)
   (void)block_size;
   return plan.n_kinv > 0 && ncomp >= 1 && n_local / ncomp <= 12 &&
-         (ncomp == 1 ? plan.n_kinv + n_local <= 24 : plan.n_kinv <= 64);
+         (ncomp == 1 ? plan.n_kinv + n_local <= 24 : plan.n_bq > 0 && plan.n_kinv <= 96);
 }
 
 namespace {
@@ -186,8 +186,19 @@ std::vector<int> class_step_order(const RowClass& k, int n_local) {
   return best;
 }
 
-int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused) {
+int vector_stage_pitch(const std::vector<RowClass>& classes, int bs) {
   int m = 1;
+  for (const auto& c : classes) m = std::max(m, bs * c.len);
+  while (m % 16 != bs % 16) ++m;  // FF_SP3 = bs (mod 16): conflict-free staging stores
+  return m;
+}
+
+int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused, int bs) {
+  int m = 1;
+  if (bs > 1) {  // vector forms: whole rows staged (no chunks), one kernel
+    for (const auto& c : classes) m = std::max(m, c.len);
+    return m | 1;
+  }
   for (const auto& c : classes)
     if (fused || (c.len > 33) == (kernel == 1)) m = std::max(m, c.len);
   // rows longer than 33 are staged in chunks of 32 in finalisation order
@@ -201,6 +212,7 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
     if (c.steps < pre) throw CodegenError("class source: a class has fewer steps than the record prefix");
   if (plan.n_kinv <= 0) throw CodegenError("row classes need a reference-tensor plan");
   if (bs < 1 || n_local % bs) throw CodegenError("class source: bad component count");
+  if (bs > 1 && plan.n_bq <= 0) throw CodegenError("class source: vector forms need a block-uniform record");
   // classes are over (node) rows with nsc slots per incidence; vector forms
   // gather each (test c, trial d) component pair as its own sub-row
   const int nsc = n_local / bs, nb = bs * bs;
@@ -221,8 +233,8 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "#if FF_BS == 1 && FF_GTAIL == 4 && !defined(FF_NO_BPAD)\n"
         "#define FF_NBPAD ((4 - FF_NKINV % 4) < FF_NLOC ? (4 - FF_NKINV % 4) : FF_NLOC)\n#else\n#define FF_NBPAD 0\n#endif\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
-     << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused) << "\n#define FF_SP_L "
-     << class_stage_pitch(classes, 1, fused) << "\n"
+     << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused, bs) << "\n#define FF_SP_L "
+     << class_stage_pitch(classes, 1, fused, bs) << "\n#define FF_SP3 " << vector_stage_pitch(classes, bs) << "\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
@@ -328,6 +340,52 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
   }
   __syncwarp();
 }
+
+#if FF_BS > 1
+// vector forms: lane = (row lane / FF_BS, trial component d = lane % FF_BS);
+// quantities of component block (c, d) at the even record offset dq:
+// FF_NBQ / 2 16-byte loads (no lane-dependent shuffling of a chunk)
+__device__ __forceinline__ void ff_vload(int e, int dq, int i, const double* __restrict__ einv, ff_i64 n_elems,
+                                         double (&g)[FF_NBQ], double& b) {
+  const ff_i64 ee = e >= 0 ? e : 0;
+  const double* p = einv + ee * FF_GS + dq;
+#if defined(FF_ABL) && (FF_ABL & 2)  // ablation (timing analysis only; results wrong)
+#pragma unroll
+  for (int k = 0; k < FF_NBQ; ++k) g[k] = (double)(ee + k);
+  if (ee == -7) ff_ld2(p, g[0], g[1]);
+#else
+#pragma unroll
+  for (int k = 0; k < FF_NBQ; k += 2) ff_ld2(p + k, g[k], g[k + 1]);
+#endif
+  b = ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)i * n_elems + ee);
+}
+// the warp's staging tile holds its rows in CSR order: row r (lanes
+// FF_BS r .. FF_BS r + FF_BS - 1) at r * FF_SP3, value FF_BS * slot + d
+// (FF_SP3 = FF_BS mod 16: the lane stores of one slot hit distinct banks);
+// write-out = whole CSR rows, coalesced, every sector written once
+// (one instantiation per row length: the per-row loop fully unrolled)
+template <int LEN>
+__device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
+                                          double* __restrict__ values) {
+#if defined(FF_ABL) && (FF_ABL & 1)  // ablation (timing analysis only; results wrong)
+  if (lane < 0) values[0] = st[0];
+  return;
+#endif
+  __syncwarp();
+  constexpr int n = FF_BS * LEN;
+#pragma unroll 1
+  for (int r = 0; r < 32 / FF_BS; ++r) {
+    const ff_i64 rb = sr[FF_BS * r];
+    if (rb < 0) continue;
+    double* __restrict__ out = values + rb;
+    const double* __restrict__ in = st + r * FF_SP3;
+#pragma unroll
+    for (int p0 = 0; p0 < n; p0 += 32)
+      if (p0 + 32 <= n || p0 + lane < n) out[p0 + lane] = in[p0 + lane];
+  }
+  __syncwarp();
+}
+#endif
 
 #ifndef FF_CWARPS
 #define FF_CWARPS 4  // warps per CTA
@@ -469,7 +527,72 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
     os << "}\n";
     }  // component pairs
   };
-  for (int c = 0; c < static_cast<int>(classes.size()); ++c) class_fn(c);
+  // vector forms: one function per (class, test component cc); the lanes of
+  // a row carry its FF_BS trial components (data: the block's quantity offset)
+  auto vclass_fn = [&](int c) {
+    const RowClass& k = classes[c];
+    const std::vector<int> order = k.order.empty() ? class_step_order(k, nsc) : k.order;
+    std::vector<int> last(k.len, -1), first(k.len, -1);
+    for (int t = 0; t < k.steps; ++t)
+      for (int j = 0; j < nsc; ++j) {
+        const int sl = k.slots[order[t] * nsc + j];
+        if (first[sl] < 0) first[sl] = t;
+        last[sl] = t;
+      }
+    for (int cc = 0; cc < bs; ++cc) {
+      os << "// class " << c << " (test component " << cc << "): " << k.len << " entries, " << k.steps
+         << " incidences\n"
+         << "__device__ __forceinline__ void ff_cls_" << c << "_" << cc
+         << "(const int (&ep)[FF_PRE], const ff_i32* __restrict__ rec, const double* __restrict__ einv, ff_i64 n_elems,\n"
+            "    double* __restrict__ st, double* __restrict__ stl, ff_i64* __restrict__ sr, int lane, int dq, ff_i64 rbeg,\n"
+            "    int row,\n"
+            "    double* __restrict__ values, double* __restrict__ rhs) {\n"
+            "  int e[" << std::max(k.steps, 1) << "];\n";
+      for (int t = 0; t < k.steps; ++t) {
+        if (t < pre)
+          os << "  e[" << order[t] << "] = ep[" << t << "];\n";
+        else
+          os << "  e[" << order[t] << "] = ff_ldid(rec + " << (t - pre) * 32 << ");\n";
+      }
+      os << "  double bs = 0.0;\n";
+      for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
+      os << ";\n";
+      const char* dk = std::getenv("FF_VDEPTH");
+      const int depth = dk ? std::max(1, std::atoi(dk)) : 4;
+      for (int t0 = 0; t0 < k.steps; t0 += depth) {
+        const int t1 = std::min(k.steps, t0 + depth);
+        os << "  {\n";
+        for (int t = t0; t < t1; ++t) {
+          const int q = order[t];
+          os << "    double g" << q << "[FF_NBQ], b" << q << "; ff_vload(e[" << q << "], dq, "
+             << k.local[q] * bs + cc << ", einv, n_elems, g" << q << ", b" << q << ");\n";
+        }
+        for (int t = t0; t < t1; ++t) {
+          const int q = order[t];
+          os << "    { double v[" << nsc << "]; ff_vrow<" << k.local[q] << ">(g" << q << ", v);";
+          for (int j = 0; j < nsc; ++j) {
+            const int sl = k.slots[q * nsc + j];
+            os << " a" << sl << (first[sl] == t ? " = v[" : " += v[") << j << "];";
+          }
+          for (int j = 0; j < nsc; ++j) {
+            const int sl = k.slots[q * nsc + j];
+            if (last[sl] == t) os << " stl[" << bs * sl << "] = a" << sl << ";";
+          }
+          os << " }\n    bs += b" << q << ";\n";
+        }
+        os << "  }\n";
+      }
+      os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len << " : -1;\n"
+         << "  ff_vwriteout<" << k.len << ">(st, sr, lane, values);\n"
+         << "  if (row >= 0 && lane % FF_BS == 0) __stcs(rhs + FF_BS * row + " << cc << ", bs);\n}\n";
+    }
+  };
+  for (int c = 0; c < static_cast<int>(classes.size()); ++c) {
+    if (bs > 1)
+      vclass_fn(c);
+    else
+      class_fn(c);
+  }
 
   auto kernel = [&](const char* name, bool longrows) {
     os << "// items of one launch: one item per warp, CTAs in item order;\n"
@@ -522,6 +645,43 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
     os << "      default: break;\n    }\n"
           "  }\n}\n";
   };
+  auto vkernel = [&](const char* name) {
+    os << "// vector forms: FF_BS consecutive CTAs run the same items, one test\n"
+          "// component each; lane = (row lane / FF_BS, trial component lane % FF_BS)\n"
+          "extern \"C\" __global__ void __launch_bounds__(32 * FF_CWARPS, FF_MINB_S)\n" << name
+       << "(const double* __restrict__ einv, ff_i64 n_elems, const ff_i64* __restrict__ row_ptr,\n"
+          "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
+          "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
+          "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
+          "  extern __shared__ double ff_dsm[];\n"
+          "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
+          "  double* st = ff_dsm + wid * (32 / FF_BS + 1) * FF_SP3;\n"
+          "  double* stl = st + (lane / FF_BS) * FF_SP3 + lane % FF_BS;  // idle lanes: a spare row\n"
+          "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * (32 / FF_BS + 1) * FF_SP3) + wid * 32;\n"
+          "  const int cc = (int)(blockIdx.x % FF_BS);\n"
+          "  const ff_i64 w = i0 + (ff_i64)(blockIdx.x / FF_BS) * FF_CWARPS + wid;\n"
+          "  if (w >= i1) return;\n"
+          "  int ep[FF_PRE];\n"
+          "#pragma unroll\n"
+          "  for (int u = 0; u < FF_PRE; ++u) ep[u] = ff_ldid(crec + (w * FF_PRE + u) * 32 + lane);\n"
+          "  const int c = __ldg(citem_class + w);\n"
+          "  const int row = __ldg(citem_rows + w * 32 + lane);\n"
+          "  const ff_i32* rec = crec + __ldg(citem_rec + w) * 32 + lane;\n"
+          "  const ff_i64 rbeg = __ldg(row_ptr + (row >= 0 ? row : 0));\n"
+          "  const int dq = ff_block_q[cc * FF_BS + lane % FF_BS];\n"
+          "  switch (c * FF_BS + cc) {\n";
+    for (int c = 0; c < static_cast<int>(classes.size()); ++c)
+      for (int cc = 0; cc < bs; ++cc)
+        os << "    case " << c * bs + cc << ": ff_cls_" << c << "_" << cc
+           << "(ep, rec, einv, n_elems, st, stl, sr, lane, dq, rbeg, row, values, rhs); break;\n";
+    os << "    default: break;\n  }\n}\n";
+  };
+  if (bs > 1) {
+    vkernel("ff_gather_classes_s");
+    // (one kernel: whole rows are staged, no long-row split)
+    os << "extern \"C\" __global__ void ff_gather_classes_l() {}\n";
+    return os.str();
+  }
   kernel("ff_gather_classes_s", false);
   kernel("ff_gather_classes_l", true);
   return os.str();

@@ -106,6 +106,11 @@ struct ElementPlan {
   int n_kinv = 0;
   std::string row_code;
   std::int64_t row_flops = 0;  // fp64 operations of all n_local rows
+  // Vector forms (block-uniform record): component block (c, d)'s entries
+  // are one linear map of its n_bq quantities at record offset
+  // block_q[c * ncomp + d] (ff_vrow<a> in row_code, ff_block_q, FF_NBQ).
+  int n_bq = 0;
+  std::vector<int> block_q;
 };
 
 ElementPlan plan_element(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule,
@@ -159,10 +164,16 @@ bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_s
 std::vector<int> class_step_order(const RowClass& k, int n_local);
 // Staging-row pitch of class kernel `kernel` (0: _s, 1: _l; odd, >= its
 // longest class row).
-int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused);
+// Vector forms (bs > 1) stage whole rows in one kernel: the longest row, odd.
+int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused, int bs = 1);
+// Vector forms: row pitch of the CSR-order staging tile (32 / bs rows + a
+// spare row per warp): >= bs * longest row, = bs (mod 16).
+int vector_stage_pitch(const std::vector<RowClass>& classes, int bs);
 // Dynamic shared memory of class kernel `kernel` (4 warps).
-inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused, int warps = 4) {
-  return warps * 32 * class_stage_pitch(classes, kernel, fused) * 8 + warps * 32 * 8;
+inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused, int warps = 4,
+                              int bs = 1) {
+  if (bs > 1) return warps * (32 / bs + 1) * vector_stage_pitch(classes, bs) * 8 + warps * 32 * 8;
+  return warps * 32 * class_stage_pitch(classes, kernel, fused, bs) * 8 + warps * 32 * 8;
 }
 
 // NVRTC translation unit with ff_gather_classes_s (classes of rows <= 33

@@ -46,7 +46,7 @@ struct GatherPlan {
   std::vector<Class> classes;
   int64_t n_citems = 0, n_citems_short = 0, n_crec = 0, n_class_rows = 0;
   int32_t* citem_class = nullptr;   // [n_citems]
-  int32_t* citem_rows = nullptr;    // [n_citems][32] local row or -1
+  int32_t* citem_rows = nullptr;    // [n_citems][32] local row of each lane or -1 (row_lanes lanes per row)
   int32_t* vconn_m = nullptr;       // [E][dim+1] vertex ids in record (Morton) order, read by K2a
   // element ids of the class items, in each class's processing order: item
   // w's first pre_steps steps at crec[(w * pre_steps + t) * 32 + lane], its
@@ -68,7 +68,8 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows = 128, int max_classes = 64,
                               bool use_eorder = true, bool split_long = true,
-                              const ClassOrderFn* step_order = nullptr, double class_frac = 0.0005);
+                              const ClassOrderFn* step_order = nullptr, double class_frac = 0.0005,
+                              int row_lanes = 1);
 void free_gather_plan(GatherPlan* p);
 
 // fem::Mesh::validate (fem.cpp:17-34) on the device: *d_bad = the lowest

@@ -604,7 +604,7 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
                               const int64_t* d_row_ptr, const uint8_t* d_slots, int window, int sm_count,
                               cudaStream_t s, GatherPlan* out, int min_class_rows, int max_classes,
                               bool use_eorder, bool split_long, const ClassOrderFn* step_order,
-                              double class_frac) {
+                              double class_frac, int row_lanes) {
   if (k > 12) return cudaErrorInvalidValue;
   if (ne * k >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   // FF_PLAN_TIMING=1: phase times of the plan build on stderr
@@ -860,13 +860,16 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     // are neighbours along that line (FF_ROW_ITEMS=0: Morton order of the DOF
     // points; NS 2.49 -> 2.09 ms together with the first-touch records below)
     const bool row_items = !std::getenv("FF_ROW_ITEMS") || std::atoi(std::getenv("FF_ROW_ITEMS")) != 0;
+    // rows per class item: 32, or 32 / row_lanes rows of row_lanes lanes each
+    // (vector forms: the trial components of a row in neighbouring lanes)
+    const int rpi = 32 / std::max(1, row_lanes);
     std::vector<std::vector<int32_t>> members(n_cls);
     std::vector<std::vector<int64_t>> first_pos(n_cls);
     for (int64_t pos = 0; pos < n_rows; ++pos) {
       const int32_t r = row_items ? static_cast<int32_t>(pos) : morton[pos];
       const int c = cls_h[r];
       if (c < 0) continue;
-      if (members[c].size() % 32 == 0) first_pos[c].push_back(pos);
+      if (members[c].size() % rpi == 0) first_pos[c].push_back(pos);
       members[c].push_back(r);
     }
     struct Item {
@@ -904,11 +907,11 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       const Item& it = items[w];
       ic[w] = it.c;
       const auto& m = members[it.c];
-      for (int l = 0; l < 32; ++l) {
-        const size_t q = static_cast<size_t>(it.idx) * 32 + l;
+      for (int l = 0; l < rpi * std::max(1, row_lanes); ++l) {
+        const size_t q = static_cast<size_t>(it.idx) * rpi + l / std::max(1, row_lanes);
         if (q < m.size()) {
           ir[w * 32 + l] = m[q];
-          ++ncr;
+          ncr += l % std::max(1, row_lanes) == 0;
         }
       }
       irec[w] = nrec;
