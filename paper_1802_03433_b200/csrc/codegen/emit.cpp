@@ -186,9 +186,16 @@ std::vector<int> class_step_order(const RowClass& k, int n_local) {
   return best;
 }
 
+// vector write-out by TMA bulk copies (rows staged at the parity of their CSR
+// start, one spare value per row); FF_VTMA=0: coalesced store loop
+bool vector_tma() {
+  const char* v = std::getenv("FF_VTMA");
+  return !v || std::atoi(v) != 0;
+}
+
 int vector_stage_pitch(const std::vector<RowClass>& classes, int bs) {
   int m = 1;
-  for (const auto& c : classes) m = std::max(m, bs * c.len);
+  for (const auto& c : classes) m = std::max(m, bs * c.len + (vector_tma() ? 1 : 0));
   while (m % 16 != bs % 16) ++m;  // FF_SP3 = bs (mod 16): conflict-free staging stores
   return m;
 }
@@ -234,7 +241,10 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
         "#define FF_NBPAD ((4 - FF_NKINV % 4) < FF_NLOC ? (4 - FF_NKINV % 4) : FF_NLOC)\n#else\n#define FF_NBPAD 0\n#endif\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused, bs) << "\n#define FF_SP_L "
-     << class_stage_pitch(classes, 1, fused, bs) << "\n#define FF_SP3 " << vector_stage_pitch(classes, bs) << "\n"
+     << class_stage_pitch(classes, 1, fused, bs) << "\n#define FF_SP3 " << vector_stage_pitch(classes, bs)
+     << "\n#define FF_VTMA " << (bs > 1 && vector_tma() ? 1 : 0) << "\n"
+     << "// per-warp staging tile (doubles; even: every tile starts 16-byte aligned)\n"
+     << "#define FF_TILE3 (((32 / FF_BS + 1) * FF_SP3 + 1) & ~1)\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
@@ -382,6 +392,36 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
 #pragma unroll
     for (int p0 = 0; p0 < n; p0 += 32)
       if (p0 + 32 <= n || p0 + lane < n) out[p0 + lane] = in[p0 + lane];
+  }
+  __syncwarp();
+}
+// TMA variant: row r (lane r) staged at r * FF_SP3 + parity so that staging
+// and CSR start share their 16-byte phase; the odd head / tail value by a
+// plain store, the rest by one cp.async.bulk (the LSU carries no write-out)
+template <int LEN>
+__device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
+                                              double* __restrict__ values) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane < 32 / FF_BS) {
+    const ff_i64 rb = sr[FF_BS * lane];
+    if (rb >= 0) {
+      constexpr int n = FF_BS * LEN;
+      const int o = lane * FF_SP3 + (int)((rb ^ (ff_i64)(lane * FF_SP3)) & 1);
+      const double* in = st + o;
+      double* out = values + rb;
+      const int a = (int)(rb & 1);
+      if (a) out[0] = in[0];
+      const int m = (n - a) & ~1;
+      if (m > 0) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(in + a);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + a), "r"(sa),
+                     "r"(m * 8) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      if ((n - a) & 1) out[n - 1] = in[n - 1];
+      if (m > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
   }
   __syncwarp();
 }
@@ -554,7 +594,10 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
         else
           os << "  e[" << order[t] << "] = ff_ldid(rec + " << (t - pre) * 32 << ");\n";
       }
-      os << "  double bs = 0.0;\n";
+      os << "  double bs = 0.0;\n"
+         << "#if FF_VTMA  // the row's staging at the parity of its CSR start\n"
+         << "  stl += (int)(((FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len
+         << ") ^ (ff_i64)((lane / FF_BS) * FF_SP3)) & 1);\n#endif\n";
       for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
       os << ";\n";
       const char* dk = std::getenv("FF_VDEPTH");
@@ -583,7 +626,8 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
         os << "  }\n";
       }
       os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len << " : -1;\n"
-         << "  ff_vwriteout<" << k.len << ">(st, sr, lane, values);\n"
+         << "#if FF_VTMA\n  ff_vwriteout_tma<" << k.len << ">(st, sr, lane, values);\n#else\n"
+         << "  ff_vwriteout<" << k.len << ">(st, sr, lane, values);\n#endif\n"
          << "  if (row >= 0 && lane % FF_BS == 0) __stcs(rhs + FF_BS * row + " << cc << ", bs);\n}\n";
     }
   };
@@ -653,11 +697,11 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
           "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
           "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
           "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
-          "  extern __shared__ double ff_dsm[];\n"
+          "  extern __shared__ __align__(16) double ff_dsm[];\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
-          "  double* st = ff_dsm + wid * (32 / FF_BS + 1) * FF_SP3;\n"
+          "  double* st = ff_dsm + wid * FF_TILE3;\n"
           "  double* stl = st + (lane / FF_BS) * FF_SP3 + lane % FF_BS;  // idle lanes: a spare row\n"
-          "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * (32 / FF_BS + 1) * FF_SP3) + wid * 32;\n"
+          "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * FF_TILE3) + wid * 32;\n"
           "  const int cc = (int)(blockIdx.x % FF_BS);\n"
           "  const ff_i64 w = i0 + (ff_i64)(blockIdx.x / FF_BS) * FF_CWARPS + wid;\n"
           "  if (w >= i1) return;\n"

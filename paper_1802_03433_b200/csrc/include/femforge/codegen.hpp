@@ -172,7 +172,7 @@ int vector_stage_pitch(const std::vector<RowClass>& classes, int bs);
 // Dynamic shared memory of class kernel `kernel` (4 warps).
 inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused, int warps = 4,
                               int bs = 1) {
-  if (bs > 1) return warps * (32 / bs + 1) * vector_stage_pitch(classes, bs) * 8 + warps * 32 * 8;
+  if (bs > 1) return warps * (((32 / bs + 1) * vector_stage_pitch(classes, bs) + 1) & ~1) * 8 + warps * 32 * 8;
   return warps * 32 * class_stage_pitch(classes, kernel, fused, bs) * 8 + warps * 32 * 8;
 }
 
