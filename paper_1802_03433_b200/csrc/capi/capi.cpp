@@ -170,6 +170,11 @@ void free_gather(ff_pattern* p) {
   free_class_module(p);
 }
 
+bool vector_fused() {
+  const char* v = std::getenv("FF_VSPLIT");
+  return v && std::atoi(v) == 0;
+}
+
 int class_cwarps(const ff_form* f) {
   const char* v = std::getenv("FF_CWARPS");
   return v ? std::max(1, std::min(8, std::atoi(v))) : 2;
@@ -195,13 +200,23 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   const auto t0 = std::chrono::steady_clock::now();
   // one fused kernel for every class unless FF_SPLIT_CLASSES:
   // measured 3.18 vs 3.29 ms at the north star (profiles/, run 25)
-  const bool fused = std::getenv("FF_SPLIT_CLASSES") == nullptr || f->ncomp > 1;
+  // vector forms: long rows (> 33 node entries) in their own kernel, so the
+  // short rows' staging tiles allow 16 warps/SM (config 5: 37.3 vs 42.4 ms
+  // fused); FF_VSPLIT=0 fuses them
+  const bool fused = f->ncomp > 1 ? vector_fused() : std::getenv("FF_SPLIT_CLASSES") == nullptr;
   std::string src = codegen::emit_class_source(f->plan, f->n_local, rc, fused, f->ncomp, p->gather.pre_steps);
   // register budget: 14 warps/SM for scalar forms (one item per warp: no
   // carried item state; NS 2.013 vs 2.038 ms at 12 warps, 2.053 with two items
   // per warp), 12 for vector forms
   if (fused && !std::getenv("FF_MINB_S"))
     src = "#define FF_MINB_S " + std::to_string((f->ncomp > 1 ? 12 : 14) / class_cwarps(f)) + "\n" + src;
+  if (!fused && f->ncomp > 1) {
+    // split vector kernels: 16 warps/SM for short rows (128 registers), 8 for
+    // long rows (234 registers, no spills): config 5 29.96 ms against 37.35
+    // with 10 warps (168 registers + spills) and 37.33 with 12
+    if (!std::getenv("FF_MINB_S")) src = "#define FF_MINB_S " + std::to_string(16 / class_cwarps(f)) + "\n" + src;
+    if (!std::getenv("FF_MINB_L")) src = "#define FF_MINB_L " + std::to_string(8 / class_cwarps(f)) + "\n" + src;
+  }
   if (!std::getenv("FF_CWARPS")) src = "#define FF_CWARPS " + std::to_string(class_cwarps(f)) + "\n" + src;
   // tuning knobs (defaults in the source): FF_MINB_S, FF_MINB_L
   // element records through L1: with records in first-touch order the lanes of
@@ -275,7 +290,8 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
                                                         cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
-                                                        std::getenv("FF_SPLIT_CLASSES") != nullptr && p->bs == 1,
+                                                        p->bs == 1 ? std::getenv("FF_SPLIT_CLASSES") != nullptr
+                                                                   : !vector_fused(),
                                                         &order_fn, 0.0005, p->bs);
   if (e != cudaSuccess) {
     ffb::kernels::free_gather_plan(&p->gather);
@@ -417,9 +433,12 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   // one (disjoint rows): the two register budgets share the SMs and the
   // element records they both read stay in L2
   if (gp.n_citems > 0) {
+    // (with generic rows on the side stream too, the long-row kernel joins
+    // them there: FF_CLASS_SIDE=1)
+    const bool side_long = generic_side && std::getenv("FF_CLASS_SIDE") && ns > 0 && gp.n_citems > ns;
     const bool both = !generic_side && ns > 0 && gp.n_citems > ns && !std::getenv("FF_SERIAL_CLASSES");
     if (both) fork(ctx->side);
-    launch_class(1, ns, gp.n_citems, both ? ctx->side : s);
+    launch_class(1, ns, gp.n_citems, both || side_long ? ctx->side : s);
     launch_class(0, 0, ns, s);
     if (both) join(ctx->side);
   }

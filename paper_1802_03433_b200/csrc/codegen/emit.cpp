@@ -193,9 +193,10 @@ bool vector_tma() {
   return !v || std::atoi(v) != 0;
 }
 
-int vector_stage_pitch(const std::vector<RowClass>& classes, int bs) {
+int vector_stage_pitch(const std::vector<RowClass>& classes, int bs, int kernel, bool fused) {
   int m = 1;
-  for (const auto& c : classes) m = std::max(m, bs * c.len + (vector_tma() ? 1 : 0));
+  for (const auto& c : classes)
+    if (fused || (c.len > 33) == (kernel == 1)) m = std::max(m, bs * c.len + (vector_tma() ? 1 : 0));
   while (m % 16 != bs % 16) ++m;  // FF_SP3 = bs (mod 16): conflict-free staging stores
   return m;
 }
@@ -241,10 +242,12 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
         "#define FF_NBPAD ((4 - FF_NKINV % 4) < FF_NLOC ? (4 - FF_NKINV % 4) : FF_NLOC)\n#else\n#define FF_NBPAD 0\n#endif\n"
      << "// staging pitches of the two kernels (odd: conflict-free lane-row stores)\n"
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused, bs) << "\n#define FF_SP_L "
-     << class_stage_pitch(classes, 1, fused, bs) << "\n#define FF_SP3 " << vector_stage_pitch(classes, bs)
+     << class_stage_pitch(classes, 1, fused, bs) << "\n#define FF_SP3_S " << vector_stage_pitch(classes, bs, 0, fused)
+     << "\n#define FF_SP3_L " << vector_stage_pitch(classes, bs, 1, fused)
      << "\n#define FF_VTMA " << (bs > 1 && vector_tma() ? 1 : 0) << "\n"
-     << "// per-warp staging tile (doubles; even: every tile starts 16-byte aligned)\n"
-     << "#define FF_TILE3 (((32 / FF_BS + 1) * FF_SP3 + 1) & ~1)\n"
+     << "// per-warp staging tiles (doubles; even: every tile starts 16-byte aligned)\n"
+     << "#define FF_TILE3_S (((32 / FF_BS + 1) * FF_SP3_S + 1) & ~1)\n"
+     << "#define FF_TILE3_L (((32 / FF_BS + 1) * FF_SP3_L + 1) & ~1)\n"
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
@@ -370,11 +373,11 @@ __device__ __forceinline__ void ff_vload(int e, int dq, int i, const double* __r
   b = ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)i * n_elems + ee);
 }
 // the warp's staging tile holds its rows in CSR order: row r (lanes
-// FF_BS r .. FF_BS r + FF_BS - 1) at r * FF_SP3, value FF_BS * slot + d
-// (FF_SP3 = FF_BS mod 16: the lane stores of one slot hit distinct banks);
+// FF_BS r .. FF_BS r + FF_BS - 1) at r * SP3, value FF_BS * slot + d
+// (SP3 = FF_BS mod 16: the lane stores of one slot hit distinct banks);
 // write-out = whole CSR rows, coalesced, every sector written once
 // (one instantiation per row length: the per-row loop fully unrolled)
-template <int LEN>
+template <int LEN, int SP3>
 __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
                                           double* __restrict__ values) {
 #if defined(FF_ABL) && (FF_ABL & 1)  // ablation (timing analysis only; results wrong)
@@ -388,17 +391,17 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
     const ff_i64 rb = sr[FF_BS * r];
     if (rb < 0) continue;
     double* __restrict__ out = values + rb;
-    const double* __restrict__ in = st + r * FF_SP3;
+    const double* __restrict__ in = st + r * SP3;
 #pragma unroll
     for (int p0 = 0; p0 < n; p0 += 32)
       if (p0 + 32 <= n || p0 + lane < n) out[p0 + lane] = in[p0 + lane];
   }
   __syncwarp();
 }
-// TMA variant: row r (lane r) staged at r * FF_SP3 + parity so that staging
+// TMA variant: row r (lane r) staged at r * SP3 + parity so that staging
 // and CSR start share their 16-byte phase; the odd head / tail value by a
 // plain store, the rest by one cp.async.bulk (the LSU carries no write-out)
-template <int LEN>
+template <int LEN, int SP3>
 __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
                                               double* __restrict__ values) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -407,7 +410,7 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
     const ff_i64 rb = sr[FF_BS * lane];
     if (rb >= 0) {
       constexpr int n = FF_BS * LEN;
-      const int o = lane * FF_SP3 + (int)((rb ^ (ff_i64)(lane * FF_SP3)) & 1);
+      const int o = lane * SP3 + (int)((rb ^ (ff_i64)(lane * SP3)) & 1);
       const double* in = st + o;
       double* out = values + rb;
       const int a = (int)(rb & 1);
@@ -571,6 +574,7 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
   // a row carry its FF_BS trial components (data: the block's quantity offset)
   auto vclass_fn = [&](int c) {
     const RowClass& k = classes[c];
+    const char* sp3 = is_long(c) ? "FF_SP3_L" : "FF_SP3_S";
     const std::vector<int> order = k.order.empty() ? class_step_order(k, nsc) : k.order;
     std::vector<int> last(k.len, -1), first(k.len, -1);
     for (int t = 0; t < k.steps; ++t)
@@ -597,7 +601,7 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
       os << "  double bs = 0.0;\n"
          << "#if FF_VTMA  // the row's staging at the parity of its CSR start\n"
          << "  stl += (int)(((FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len
-         << ") ^ (ff_i64)((lane / FF_BS) * FF_SP3)) & 1);\n#endif\n";
+         << ") ^ (ff_i64)((lane / FF_BS) * " << sp3 << ")) & 1);\n#endif\n";
       for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
       os << ";\n";
       const char* dk = std::getenv("FF_VDEPTH");
@@ -626,8 +630,8 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
         os << "  }\n";
       }
       os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len << " : -1;\n"
-         << "#if FF_VTMA\n  ff_vwriteout_tma<" << k.len << ">(st, sr, lane, values);\n#else\n"
-         << "  ff_vwriteout<" << k.len << ">(st, sr, lane, values);\n#endif\n"
+         << "#if FF_VTMA\n  ff_vwriteout_tma<" << k.len << ", " << sp3 << ">(st, sr, lane, values);\n#else\n"
+         << "  ff_vwriteout<" << k.len << ", " << sp3 << ">(st, sr, lane, values);\n#endif\n"
          << "  if (row >= 0 && lane % FF_BS == 0) __stcs(rhs + FF_BS * row + " << cc << ", bs);\n}\n";
     }
   };
@@ -689,19 +693,21 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
     os << "      default: break;\n    }\n"
           "  }\n}\n";
   };
-  auto vkernel = [&](const char* name) {
+  auto vkernel = [&](const char* name, bool longrows) {
+    const std::string sp3 = longrows ? "FF_SP3_L" : "FF_SP3_S", tile = longrows ? "FF_TILE3_L" : "FF_TILE3_S";
     os << "// vector forms: FF_BS consecutive CTAs run the same items, one test\n"
           "// component each; lane = (row lane / FF_BS, trial component lane % FF_BS)\n"
-          "extern \"C\" __global__ void __launch_bounds__(32 * FF_CWARPS, FF_MINB_S)\n" << name
+          "extern \"C\" __global__ void __launch_bounds__(32 * FF_CWARPS, " << (longrows ? "FF_MINB_L" : "FF_MINB_S")
+       << ")\n" << name
        << "(const double* __restrict__ einv, ff_i64 n_elems, const ff_i64* __restrict__ row_ptr,\n"
           "    double* __restrict__ values, double* __restrict__ rhs, const ff_i32* __restrict__ citem_class,\n"
           "    const ff_i32* __restrict__ citem_rows, const ff_i64* __restrict__ citem_rec,\n"
           "    const ff_i32* __restrict__ crec, ff_i64 i0, ff_i64 i1) {\n"
           "  extern __shared__ __align__(16) double ff_dsm[];\n"
           "  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;\n"
-          "  double* st = ff_dsm + wid * FF_TILE3;\n"
-          "  double* stl = st + (lane / FF_BS) * FF_SP3 + lane % FF_BS;  // idle lanes: a spare row\n"
-          "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * FF_TILE3) + wid * 32;\n"
+          "  double* st = ff_dsm + wid * " << tile << ";\n"
+          "  double* stl = st + (lane / FF_BS) * " << sp3 << " + lane % FF_BS;  // idle lanes: a spare row\n"
+          "  ff_i64* sr = (ff_i64*)(ff_dsm + FF_CWARPS * " << tile << ") + wid * 32;\n"
           "  const int cc = (int)(blockIdx.x % FF_BS);\n"
           "  const ff_i64 w = i0 + (ff_i64)(blockIdx.x / FF_BS) * FF_CWARPS + wid;\n"
           "  if (w >= i1) return;\n"
@@ -715,15 +721,15 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
           "  const int dq = ff_block_q[cc * FF_BS + lane % FF_BS];\n"
           "  switch (c * FF_BS + cc) {\n";
     for (int c = 0; c < static_cast<int>(classes.size()); ++c)
+      if (is_long(c) == longrows)
       for (int cc = 0; cc < bs; ++cc)
         os << "    case " << c * bs + cc << ": ff_cls_" << c << "_" << cc
            << "(ep, rec, einv, n_elems, st, stl, sr, lane, dq, rbeg, row, values, rhs); break;\n";
     os << "    default: break;\n  }\n}\n";
   };
   if (bs > 1) {
-    vkernel("ff_gather_classes_s");
-    // (one kernel: whole rows are staged, no long-row split)
-    os << "extern \"C\" __global__ void ff_gather_classes_l() {}\n";
+    vkernel("ff_gather_classes_s", false);
+    vkernel("ff_gather_classes_l", true);
     return os.str();
   }
   kernel("ff_gather_classes_s", false);

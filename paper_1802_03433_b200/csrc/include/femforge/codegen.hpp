@@ -168,11 +168,12 @@ std::vector<int> class_step_order(const RowClass& k, int n_local);
 int class_stage_pitch(const std::vector<RowClass>& classes, int kernel, bool fused, int bs = 1);
 // Vector forms: row pitch of the CSR-order staging tile (32 / bs rows + a
 // spare row per warp): >= bs * longest row, = bs (mod 16).
-int vector_stage_pitch(const std::vector<RowClass>& classes, int bs);
+int vector_stage_pitch(const std::vector<RowClass>& classes, int bs, int kernel = 0, bool fused = true);
 // Dynamic shared memory of class kernel `kernel` (4 warps).
 inline int class_shared_bytes(const std::vector<RowClass>& classes, int kernel, bool fused, int warps = 4,
                               int bs = 1) {
-  if (bs > 1) return warps * (((32 / bs + 1) * vector_stage_pitch(classes, bs) + 1) & ~1) * 8 + warps * 32 * 8;
+  if (bs > 1)
+    return warps * (((32 / bs + 1) * vector_stage_pitch(classes, bs, kernel, fused) + 1) & ~1) * 8 + warps * 32 * 8;
   return warps * 32 * class_stage_pitch(classes, kernel, fused, bs) * 8 + warps * 32 * 8;
 }
 
