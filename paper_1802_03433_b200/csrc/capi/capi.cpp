@@ -433,12 +433,9 @@ void launch_gather(ff_form* f, const ff_mesh* m, ff_pattern* p, double* d_values
   // one (disjoint rows): the two register budgets share the SMs and the
   // element records they both read stay in L2
   if (gp.n_citems > 0) {
-    // (with generic rows on the side stream too, the long-row kernel joins
-    // them there: FF_CLASS_SIDE=1)
-    const bool side_long = generic_side && std::getenv("FF_CLASS_SIDE") && ns > 0 && gp.n_citems > ns;
     const bool both = !generic_side && ns > 0 && gp.n_citems > ns && !std::getenv("FF_SERIAL_CLASSES");
     if (both) fork(ctx->side);
-    launch_class(1, ns, gp.n_citems, both || side_long ? ctx->side : s);
+    launch_class(1, ns, gp.n_citems, both ? ctx->side : s);
     launch_class(0, 0, ns, s);
     if (both) join(ctx->side);
   }

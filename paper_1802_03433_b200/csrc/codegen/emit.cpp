@@ -186,17 +186,10 @@ std::vector<int> class_step_order(const RowClass& k, int n_local) {
   return best;
 }
 
-// vector write-out by TMA bulk copies (rows staged at the parity of their CSR
-// start, one spare value per row); FF_VTMA=0: coalesced store loop
-bool vector_tma() {
-  const char* v = std::getenv("FF_VTMA");
-  return !v || std::atoi(v) != 0;
-}
-
 int vector_stage_pitch(const std::vector<RowClass>& classes, int bs, int kernel, bool fused) {
   int m = 1;
   for (const auto& c : classes)
-    if (fused || (c.len > 33) == (kernel == 1)) m = std::max(m, bs * c.len + (vector_tma() ? 1 : 0));
+    if (fused || (c.len > 33) == (kernel == 1)) m = std::max(m, bs * c.len + 1);  // + 1: TMA parity shift
   while (m % 16 != bs % 16) ++m;  // FF_SP3 = bs (mod 16): conflict-free staging stores
   return m;
 }
@@ -244,7 +237,7 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "#define FF_SP_S " << class_stage_pitch(classes, 0, fused, bs) << "\n#define FF_SP_L "
      << class_stage_pitch(classes, 1, fused, bs) << "\n#define FF_SP3_S " << vector_stage_pitch(classes, bs, 0, fused)
      << "\n#define FF_SP3_L " << vector_stage_pitch(classes, bs, 1, fused)
-     << "\n#define FF_VTMA " << (bs > 1 && vector_tma() ? 1 : 0) << "\n"
+     << "\n"
      << "// per-warp staging tiles (doubles; even: every tile starts 16-byte aligned)\n"
      << "#define FF_TILE3_S (((32 / FF_BS + 1) * FF_SP3_S + 1) & ~1)\n"
      << "#define FF_TILE3_L (((32 / FF_BS + 1) * FF_SP3_L + 1) & ~1)\n"
@@ -373,37 +366,15 @@ __device__ __forceinline__ void ff_vload(int e, int dq, int i, const double* __r
   b = ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)i * n_elems + ee);
 }
 // the warp's staging tile holds its rows in CSR order: row r (lanes
-// FF_BS r .. FF_BS r + FF_BS - 1) at r * SP3, value FF_BS * slot + d
-// (SP3 = FF_BS mod 16: the lane stores of one slot hit distinct banks);
-// write-out = whole CSR rows, coalesced, every sector written once
-// (one instantiation per row length: the per-row loop fully unrolled)
+// FF_BS r .. FF_BS r + FF_BS - 1) at r * SP3 + parity, value FF_BS * slot + d
+// (SP3 = FF_BS mod 16: the lane stores of one slot hit distinct banks; the
+// parity gives staging and CSR start the same 16-byte phase). Write-out: lane
+// r sends row r, the odd head / tail value by a plain store, the rest by one
+// cp.async.bulk (TMA): whole rows, every sector written once (config 5: 30.0
+// vs 30.45 ms with a coalesced store loop)
 template <int LEN, int SP3>
 __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
                                           double* __restrict__ values) {
-#if defined(FF_ABL) && (FF_ABL & 1)  // ablation (timing analysis only; results wrong)
-  if (lane < 0) values[0] = st[0];
-  return;
-#endif
-  __syncwarp();
-  constexpr int n = FF_BS * LEN;
-#pragma unroll 1
-  for (int r = 0; r < 32 / FF_BS; ++r) {
-    const ff_i64 rb = sr[FF_BS * r];
-    if (rb < 0) continue;
-    double* __restrict__ out = values + rb;
-    const double* __restrict__ in = st + r * SP3;
-#pragma unroll
-    for (int p0 = 0; p0 < n; p0 += 32)
-      if (p0 + 32 <= n || p0 + lane < n) out[p0 + lane] = in[p0 + lane];
-  }
-  __syncwarp();
-}
-// TMA variant: row r (lane r) staged at r * SP3 + parity so that staging
-// and CSR start share their 16-byte phase; the odd head / tail value by a
-// plain store, the rest by one cp.async.bulk (the LSU carries no write-out)
-template <int LEN, int SP3>
-__device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, const ff_i64* __restrict__ sr, int lane,
-                                              double* __restrict__ values) {
 #if defined(FF_ABL) && (FF_ABL & 1)  // ablation (timing analysis only; results wrong)
   if (lane < 0) values[0] = st[0];
   return;
@@ -603,9 +574,9 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
           os << "  e[" << order[t] << "] = ff_ldid(rec + " << (t - pre) * 32 << ");\n";
       }
       os << "  double bs = 0.0;\n"
-         << "#if FF_VTMA  // the row's staging at the parity of its CSR start\n"
+         << "  // the row's staging at the parity of its CSR start (TMA write-out)\n"
          << "  stl += (int)(((FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len
-         << ") ^ (ff_i64)((lane / FF_BS) * " << sp3 << ")) & 1);\n#endif\n";
+         << ") ^ (ff_i64)((lane / FF_BS) * " << sp3 << ")) & 1);\n";
       for (int sl = 0; sl < k.len; ++sl) os << (sl % 16 ? ", a" : (sl ? ";\n  double a" : "  double a")) << sl;
       os << ";\n";
       const char* dk = std::getenv("FF_VDEPTH");
@@ -634,8 +605,7 @@ __device__ __noinline__ void ff_vwriteout_tma(const double* __restrict__ st, con
         os << "  }\n";
       }
       os << "  sr[lane] = row >= 0 ? FF_NB * rbeg + " << static_cast<long long>(bs) * cc * k.len << " : -1;\n"
-         << "#if FF_VTMA\n  ff_vwriteout_tma<" << k.len << ", " << sp3 << ">(st, sr, lane, values);\n#else\n"
-         << "  ff_vwriteout<" << k.len << ", " << sp3 << ">(st, sr, lane, values);\n#endif\n"
+         << "  ff_vwriteout<" << k.len << ", " << sp3 << ">(st, sr, lane, values);\n"
          << "  if (row >= 0 && lane % FF_BS == 0) __stcs(rhs + FF_BS * row + " << cc << ", bs);\n}\n";
     }
   };
