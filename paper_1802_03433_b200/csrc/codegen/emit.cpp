@@ -325,7 +325,11 @@ __device__ __noinline__ void ff_writeout(const double* __restrict__ st, int sp, 
 #pragma unroll ff_wunroll
     for (int m = 0; m < 32; ++m) {
       const ff_i64 rb = sr[m];
+#if defined(FF_ABL) && (FF_ABL & 16)  // ablation: the same stores into a 2 MB window (no DRAM writes)
+      if (rb >= 0) ff_stv(values + ((rb + FF_BS * (q0 + lane)) & 0x3FFFF), st[m * sp + lane]);
+#else
       if (rb >= 0) ff_stv(values + rb + FF_BS * (q0 + lane), st[m * sp + lane]);
+#endif
     }
   }
   __syncwarp();
@@ -341,7 +345,11 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
 #pragma unroll ff_wunroll
     for (int m = 0; m < 32; ++m) {
       const ff_i64 rb = sr[m];
+#if defined(FF_ABL) && (FF_ABL & 16)
+      if (rb >= 0) ff_stv(values + ((rb + FF_BS * off) & 0x3FFFF), st[m * sp + lane]);
+#else
       if (rb >= 0) ff_stv(values + rb + FF_BS * off, st[m * sp + lane]);
+#endif
     }
   }
   __syncwarp();

@@ -191,3 +191,35 @@ def test_blocked_elasticity_form_compiles(ff):
     assert info["n_local"] == 30 and info["n_kinv"] == 36
     assert f.cubin[:4] == b"\x7fELF" and "#define FF_BS 3" in f.source
     assert "ff_gather_invariants" in f.source and "ff_gather_apply<29>(r, g, d, arow)" in f.source
+
+
+def _vrow_terms(src, nsc):
+    import re
+    terms = []
+    for a in range(nsc):
+        body = src[src.index(f"void ff_vrow<{a}>("):]
+        body = body[:body.index("}")]
+        terms += [0 if e == "0.0" else e.count("g[") for e in re.findall(r"v\[\d+\] = (.*?);", body)]
+    return terms
+
+
+@pytest.mark.parametrize("lam,mu,nbq,nkinv", [("1", "1", 6, 36), ("2", "0.5", 10, 90)])
+def test_vector_record_is_block_uniform(ff, lam, mu, nbq, nkinv):
+    """Vector forms: every (test, trial) component block's entries are one
+    linear map (ff_vrow) of that block's own record quantities
+    (element_plan.cpp: uniform_block_basis). Elasticity: 6 quantities per
+    block for lambda = mu ((c,d) and (d,c) share them: 36 in the record), 9
+    (padded to 10) otherwise; every entry of the P2 node-pair map reads <= 6
+    resp. 9 quantities -- the diagonal blocks' 18-invariant entries are gone."""
+    import re
+    b, l = ff.elasticity_text(3, lam=lam, mu=mu)
+    f = ff.Form.blocked(None, 3, 2, 3, b, l, quad_rule=4)
+    src = f.source
+    assert f.info["n_kinv"] == nkinv
+    assert re.search(r"#define FF_NBQ (\d+)", src).group(1) == str(nbq)
+    q = [int(x) for x in re.search(r"ff_block_q\[9\] = \{(.*?)\}", src).group(1).split(",")]
+    assert all(o % 2 == 0 and o + nbq <= nkinv for o in q)
+    if lam == mu:
+        assert q[1] == q[3] and q[2] == q[6] and q[5] == q[7]  # (c,d) and (d,c) share
+    t = _vrow_terms(src, 10)
+    assert len(t) == 100 and max(t) <= (6 if lam == mu else 9)

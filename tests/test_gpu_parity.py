@@ -415,7 +415,8 @@ def _elasticity_system(ff, ctx, n, row_begin=0, row_end=None, ids=None, lam="1",
 def test_elasticity_matches_oracle(ff, ctx, n, scatter):
     """Config 5 (vector P2 elasticity): block-expanded pattern bit-exact, values
     and RHS <= 1e-12 normwise against the C restatement, through the row
-    gather (per component-pair sub-rows) and the atomic scatter."""
+    gather (block-uniform records, the three trial components of a row in
+    neighbouring lanes) and the atomic scatter."""
     c, v, d, nd, rp, ci, val, rhs, f, m, p = _elasticity_system(ff, ctx, n, lam="2", mu="0.5", force=("0", "1", "-1"),
                                                                 scatter=scatter)
     assert p.scatter_for(f) == scatter and p.n_rows == 3 * nd
@@ -428,8 +429,9 @@ def test_elasticity_matches_oracle(ff, ctx, n, scatter):
 
 def test_elasticity_class_gather_matches_atomic(ff, ctx):
     """Vector forms through the class-specialised gather (node-row classes,
-    one register-resident sub-row per (test, trial) component pair): equal to
-    the atomic scatter to rounding, bitwise reproducible run to run."""
+    lanes = (row, trial component), rows staged in CSR order and written by
+    TMA; short- and long-row kernels): equal to the atomic scatter to
+    rounding, bitwise reproducible run to run."""
     n = 8
     ctx.set_gather_classes(200)
     try:
