@@ -175,7 +175,7 @@ bool vector_fused() {
   return v && std::atoi(v) == 0;
 }
 
-int class_cwarps(const ff_form* f) {
+int class_cwarps(const ff_form*) {
   const char* v = std::getenv("FF_CWARPS");
   return v ? std::max(1, std::min(8, std::atoi(v))) : 2;
 }
@@ -615,18 +615,20 @@ void free_mesh(ff_mesh* m) {
   if (m->dconn != m->vconn) cudaFree(m->dconn);
   cudaFree(m->vconn);
   cudaFree(m->stage);
+  cudaFree(m->stage_d);
   delete m;
 }
 
 // Upload n ids into dst through the staging buffer; true when any id changed.
 bool upload_conn(ff_mesh* m, int32_t* dst, const int32_t* src, int64_t n) {
   ff_ctx* ctx = m->ctx;
-  const int64_t need = std::max<int64_t>(m->ne * m->k, m->ne * (m->dim + 1));
-  if (!m->stage) m->stage = device_alloc<int32_t>(need, "connectivity staging");
-  ffb::cuda_check(cudaMemcpyAsync(m->stage, src, n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  // staging per array (vconn: m->stage, dconn: m->stage_d), sized for it
+  int32_t*& stage = dst == m->vconn ? m->stage : m->stage_d;
+  if (!stage) stage = device_alloc<int32_t>(std::max<int64_t>(n, 1), "connectivity staging");
+  ffb::cuda_check(cudaMemcpyAsync(stage, src, n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
   unsigned long long* d_diff = ctx->d_status + 2;
   ffb::cuda_check(cudaMemsetAsync(d_diff, 0, sizeof(unsigned long long), ctx->stream), "memset");
-  ffb::cuda_check(ffb::kernels::copy_compare(m->stage, dst, n, d_diff, ctx->sm_count, ctx->stream), "compare");
+  ffb::cuda_check(ffb::kernels::copy_compare(stage, dst, n, d_diff, ctx->sm_count, ctx->stream), "compare");
   unsigned long long diff = 0;
   ffb::cuda_check(cudaMemcpyAsync(&diff, d_diff, sizeof diff, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
   ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "connectivity upload");
@@ -657,11 +659,12 @@ int ff_init(int device, ff_ctx** out) {
     ffb::cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attribute");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     ffb::cuda_check(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    ffb::cuda_check(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking), "cudaStreamCreate");
 
     ffb::cuda_check(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming), "cudaEventCreate");
     ffb::cuda_check(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming), "cudaEventCreate");
-    c->d_status = device_alloc<unsigned long long>(3, "status");  // [bad_elem, bad_row, scratch]
-    ffb::cuda_check(cudaMallocHost(&c->h_status, 2 * sizeof(unsigned long long)), "cudaMallocHost");
+    c->d_status = device_alloc<unsigned long long>(5, "status");  // [bad_elem, bad_row, scratch, 2 diffs]
+    ffb::cuda_check(cudaMallocHost(&c->h_status, 4 * sizeof(unsigned long long)), "cudaMallocHost");
     ffb::cuda_check(cudaMemset(c->d_status, 0xff, 2 * sizeof(unsigned long long)), "memset");
     *out = c.release();
   });
@@ -675,6 +678,8 @@ int ff_ctx_destroy(ff_ctx* ctx) {
     cudaFree(ctx->d_status);
     cudaFreeHost(ctx->h_status);
     cudaStreamSynchronize(ctx->side);
+    cudaStreamSynchronize(ctx->upload);
+    cudaStreamDestroy(ctx->upload);
     cudaEventDestroy(ctx->fork);
     cudaEventDestroy(ctx->join);
     cudaStreamDestroy(ctx->side);
@@ -1259,28 +1264,66 @@ int ff_assemble(ff_form* f, ff_mesh* m, ff_pattern* p, const double* coords, con
     // inputs: the flattened mesh (device.cpp:48-64 analogue), host -> device
     if (coords)
       ffb::cuda_check(cudaMemcpyAsync(m->coords, coords, m->nv * m->dim * sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    // The reference re-searches every column on every call (device.cpp:274-288);
-    // here the connectivity goes through a staging buffer and is compared
-    // exactly with the resident copy: any change gives the mesh a new
-    // generation, so the slot and gather plans are re-derived (and the missing
-    // column check re-run), and the new connectivity is validated like a new
-    // mesh (device.cpp:49)
-    bool changed = false;
-    if (vconn) changed |= upload_conn(m, m->vconn, vconn, m->ne * (m->dim + 1));
-    if (dconn && m->dconn != m->vconn) changed |= upload_conn(m, m->dconn, dconn, m->ne * m->k);
-    if (changed) {
-      m->generation = next_generation();
-      validate_mesh(m, true);
-    }
     const int64_t n_rows = p->bs * (p->re - p->rb);
     const int64_t nnz = int64_t(p->bs) * p->bs * p->nnz;
     if (!p->e2e_values) p->e2e_values = device_alloc<double>(nnz, "values");
     if (!p->e2e_rhs) p->e2e_rhs = device_alloc<double>(n_rows, "rhs");
-    launch_assembly(f, m, p, p->e2e_values, p->e2e_rhs, ctx->stream);
-    report_status(ctx, stats);
-    ffb::cuda_check(cudaMemcpyAsync(values_out, p->e2e_values, nnz * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-    ffb::cuda_check(cudaMemcpyAsync(rhs_out, p->e2e_rhs, n_rows * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-    ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "D2H");
+    const bool has_d = dconn && m->dconn != m->vconn;
+    auto assemble_and_copy = [&]() {
+      launch_assembly(f, m, p, p->e2e_values, p->e2e_rhs, ctx->stream);
+      ffb::cuda_check(cudaMemcpyAsync(values_out, p->e2e_values, nnz * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+      ffb::cuda_check(cudaMemcpyAsync(rhs_out, p->e2e_rhs, n_rows * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    };
+    // The reference re-searches every column on every call (device.cpp:274-288);
+    // here the connectivity goes through staging buffers and is compared
+    // exactly with the resident copy: any change gives the mesh a new
+    // generation, so the slot and gather plans are re-derived (and the missing
+    // column check re-run), and the new connectivity is validated like a new
+    // mesh (device.cpp:49). Once the (pattern, mesh) plans exist, the upload and
+    // compare run on their own stream while the assembly runs with the resident
+    // connectivity and its values go back to the host (H2D and D2H overlap on
+    // the full-duplex link); a changed connectivity re-runs the assembly.
+    const bool planned = p->plan_mesh == m && p->plan_generation == m->generation && p->slots;
+    if ((vconn || has_d) && planned) {
+      const int64_t nvc = m->ne * (m->dim + 1), ndc = m->ne * m->k;
+      if (vconn && !m->stage) m->stage = device_alloc<int32_t>(std::max<int64_t>(nvc, 1), "connectivity staging");
+      if (has_d && !m->stage_d) m->stage_d = device_alloc<int32_t>(std::max<int64_t>(ndc, 1), "connectivity staging");
+      unsigned long long* d_diff = ctx->d_status + 3;
+      cudaStream_t u = ctx->upload;
+      ffb::cuda_check(cudaMemsetAsync(d_diff, 0, 2 * sizeof(unsigned long long), u), "memset");
+      if (vconn) {
+        ffb::cuda_check(cudaMemcpyAsync(m->stage, vconn, nvc * sizeof(int32_t), cudaMemcpyHostToDevice, u), "H2D");
+        ffb::cuda_check(ffb::kernels::compare(m->stage, m->vconn, nvc, d_diff, ctx->sm_count, u), "compare");
+      }
+      if (has_d) {
+        ffb::cuda_check(cudaMemcpyAsync(m->stage_d, dconn, ndc * sizeof(int32_t), cudaMemcpyHostToDevice, u), "H2D");
+        ffb::cuda_check(ffb::kernels::compare(m->stage_d, m->dconn, ndc, d_diff + 1, ctx->sm_count, u), "compare");
+      }
+      ffb::cuda_check(cudaMemcpyAsync(ctx->h_status + 2, d_diff, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, u),
+                      "D2H");
+      assemble_and_copy();
+      ffb::cuda_check(cudaStreamSynchronize(u), "connectivity upload");
+      ffb::cuda_check(cudaStreamSynchronize(ctx->stream), "D2H");
+      if (ctx->h_status[2] || ctx->h_status[3]) {  // changed: adopt it and assemble again
+        if (vconn && ctx->h_status[2])
+          ffb::cuda_check(cudaMemcpyAsync(m->vconn, m->stage, nvc * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+        if (has_d && ctx->h_status[3])
+          ffb::cuda_check(cudaMemcpyAsync(m->dconn, m->stage_d, ndc * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+        m->generation = next_generation();
+        validate_mesh(m, true);
+        assemble_and_copy();
+      }
+    } else {
+      bool changed = false;
+      if (vconn) changed |= upload_conn(m, m->vconn, vconn, m->ne * (m->dim + 1));
+      if (has_d) changed |= upload_conn(m, m->dconn, dconn, m->ne * m->k);
+      if (changed) {
+        m->generation = next_generation();
+        validate_mesh(m, true);
+      }
+      assemble_and_copy();
+    }
+    report_status(ctx, stats);  // (also waits for the D2H copies)
     if (stats) stats->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   });
 }

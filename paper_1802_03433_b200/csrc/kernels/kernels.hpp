@@ -79,6 +79,9 @@ void free_gather_plan(GatherPlan* p);
 cudaError_t validate_mesh(const double* d_coords, int dim, int64_t nv, const int32_t* d_vconn, const int32_t* d_dconn,
                           int k, int64_t n_dofs, int64_t ne, bool orient, unsigned long long* d_bad, int sm_count,
                           cudaStream_t s);
+// *d_diff |= 1 when d_src and d_dst differ anywhere (exact; nothing written).
+cudaError_t compare(const int32_t* d_src, const int32_t* d_dst, int64_t n, unsigned long long* d_diff, int sm_count,
+                    cudaStream_t s);
 // d_dst := d_src (n int32); *d_diff |= 1 when any value changed (exact).
 cudaError_t copy_compare(const int32_t* d_src, int32_t* d_dst, int64_t n, unsigned long long* d_diff, int sm_count,
                          cudaStream_t s);

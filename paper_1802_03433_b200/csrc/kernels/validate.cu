@@ -84,7 +84,23 @@ __global__ void copy_compare_kernel(const int32_t* __restrict__ src, int32_t* __
   if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) atomicOr(diff, 1ull);
 }
 
+// *diff |= 1 when src and dst differ anywhere (exact; dst is not written)
+__global__ void compare_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t n,
+                               unsigned long long* __restrict__ diff) {
+  bool d = false;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d |= src[t] != dst[t];
+  if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) atomicOr(diff, 1ull);
+}
+
 }  // namespace
+
+cudaError_t compare(const int32_t* d_src, const int32_t* d_dst, int64_t n, unsigned long long* d_diff, int sm_count,
+                    cudaStream_t s) {
+  if (n > 0) compare_kernel<<<grid_for(n, sm_count * 8), kThreads, 0, s>>>(d_src, d_dst, n, d_diff);
+  return cudaGetLastError();
+}
 
 cudaError_t validate_mesh(const double* d_coords, int dim, int64_t nv, const int32_t* d_vconn, const int32_t* d_dconn,
                           int k, int64_t n_dofs, int64_t ne, bool orient, unsigned long long* d_bad, int sm_count,

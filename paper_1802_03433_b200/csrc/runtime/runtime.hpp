@@ -41,9 +41,10 @@ struct ff_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;             // second stream: concurrent gather launches
+  cudaStream_t upload = nullptr;           // ff_assemble: connectivity upload + compare
   cudaEvent_t fork = nullptr, join = nullptr;
-  unsigned long long* d_status = nullptr;  // [bad_elem, bad_row]
-  unsigned long long* h_status = nullptr;  // pinned mirror
+  unsigned long long* d_status = nullptr;  // [bad_elem, bad_row, scratch, vconn diff, dconn diff]
+  unsigned long long* h_status = nullptr;  // pinned mirror (4: [bad_elem, bad_row, vconn diff, dconn diff])
   int scatter = 2;                          // FF_SCATTER_*_MODE (default: row gather)
   int64_t class_min_rows = 128;             // gather row classes (0: off)
 };
@@ -78,7 +79,8 @@ struct ff_mesh {
   int32_t* vconn = nullptr;
   int32_t* dconn = nullptr;  // == vconn for P1
   std::uint64_t generation = 0;      // process-wide unique per connectivity (plan keys)
-  int32_t* stage = nullptr;          // ff_assemble upload staging (exact re-upload compare)
+  int32_t* stage = nullptr;          // ff_assemble upload staging of vconn (exact re-upload compare)
+  int32_t* stage_d = nullptr;        // ... of dconn (P2: uploaded concurrently with vconn's compare)
 };
 
 struct ff_pattern {
