@@ -427,7 +427,8 @@ def test_elasticity_matches_oracle(ff, ctx, n, scatter):
     assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
 
 
-def test_elasticity_class_gather_matches_atomic(ff, ctx):
+@pytest.mark.parametrize("lam,mu", [("1", "1"), ("2", "0.5")])
+def test_elasticity_class_gather_matches_atomic(ff, ctx, lam, mu):
     """Vector forms through the class-specialised gather (node-row classes,
     lanes = (row, trial component), rows staged in CSR order and written by
     TMA; short- and long-row kernels): equal to the atomic scatter to
@@ -435,7 +436,7 @@ def test_elasticity_class_gather_matches_atomic(ff, ctx):
     n = 8
     ctx.set_gather_classes(200)
     try:
-        *_, val_a, rhs_a, f, m, p = _elasticity_system(ff, ctx, n, scatter="atomic")
+        *_, val_a, rhs_a, f, m, p = _elasticity_system(ff, ctx, n, lam=lam, mu=mu, scatter="atomic")
         ctx.set_scatter("gather")
         val_g, rhs_g = ff.assemble(f, m, p)
         val_g2, rhs_g2 = ff.assemble(f, m, p)
