@@ -678,6 +678,8 @@ std::optional<ElementPlan> plan_tensor(const fem::InstantiatedForm& f, const fem
     for (int r : members) os << " " << emit_call(entries[r], name);
     os << " }\n";
   }
+  plan.b_zero.assign(f.n_local, 0);
+  for (int i = 0; i < f.n_local; ++i) plan.b_zero[i] = row_sig[nn + i].empty() ? 1 : 0;
   plan.n_unique_entries = static_cast<int>(ordered.size());
   plan.flops = flops;
   plan.body = os.str();

@@ -82,6 +82,20 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
   fill(text, "PAIR_TAIL", std::to_string(record_pair_tail(f.n_local)));
   fill(text, "ROW_CODE", gather ? plan.row_code : std::string());
   {
+    // load-vector entries of the element record: identically zero entries are
+    // not stored (config 5, f = (0, 0, -1): 20 of 30)
+    const std::vector<int> sl = record_bslots(plan, f.n_local, f.ncomp);
+    std::string t = "__constant__ int ff_bslot[FF_NLOC] = {";
+    std::string st;
+    for (int i = 0; i < f.n_local; ++i) {
+      t += (i ? ", " : "") + std::to_string(sl[i]);
+      if (sl[i] >= 0)
+        st += "    __stcg(bs + (ff_i64)" + std::to_string(sl[i]) + " * n_elems + t, out[FF_NKINV + " + std::to_string(i) + "]);\n";
+    }
+    fill(text, "BSLOT", gather ? t + "};" : std::string());
+    fill(text, "BSTORE", gather ? st : std::string());
+  }
+  {
     std::string d =
         "__device__ __forceinline__ void ff_gather_dispatch(int i, const FfRec& r, const double (&g)[FF_NKP], int d,\n"
         "                                                   double* __restrict__ arow) {\n  switch (i) {\n";
@@ -106,6 +120,20 @@ std::string emit_source(const fem::InstantiatedForm& f, const LaunchParams& cfg,
 int record_pair_tail(int n_local) {
   if (const char* v = std::getenv("FF_PAIR_TAIL")) return std::atoi(v) != 0 ? 1 : 0;
   return n_local <= 4 ? 1 : 0;
+}
+
+std::vector<int> record_bslots(const ElementPlan& plan, int n_local, int ncomp, int* n_soa) {
+  // FF_NBPAD of the templates: scalar records whose invariants leave a
+  // 4-chunk tail carry the first load-vector entries in its padding
+  const int nk = plan.n_kinv;
+  const int gtail = nk % 4 == 0 ? 0 : ((nk % 4 <= 2 && record_pair_tail(n_local)) ? 2 : 4);
+  const int nbpad = (ncomp == 1 && gtail == 4 && !std::getenv("FF_NO_BPAD")) ? std::min(4 - nk % 4, n_local) : 0;
+  std::vector<int> slot(n_local, -1);
+  int k = 0;
+  for (int i = nbpad; i < n_local; ++i)
+    if (static_cast<int>(plan.b_zero.size()) != n_local || !plan.b_zero[i]) slot[i] = k++;
+  if (n_soa) *n_soa = k;
+  return slot;
 }
 
 bool gather_capable(const ElementPlan& plan, int n_local, int ncomp, int block_size) {
@@ -217,6 +245,7 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
   // classes are over (node) rows with nsc slots per incidence; vector forms
   // gather each (test c, trial d) component pair as its own sub-row
   const int nsc = n_local / bs, nb = bs * bs;
+  const std::vector<int> bslot = record_bslots(plan, n_local, bs);  // load-vector record slots
   std::ostringstream os;
   const int nkp = plan.n_kinv + (plan.n_kinv & 1);
   const int erec = (plan.n_kinv + n_local + 1) & ~1;
@@ -279,7 +308,8 @@ __device__ __forceinline__ int ff_ldid(const ff_i32* p) {
 // element record: invariants (ff_load_inv), load vector [FF_NLOC][E]
 // (idle lanes, e < 0, only occur in rows that are never written: they read
 // element 0 instead of branching)
-__device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict__ einv, ff_i64 n_elems,
+// (sl: the entry's slot in the record's load-vector array, -1: zero entry)
+__device__ __forceinline__ void ff_cload(int e, int i, int sl, const double* __restrict__ einv, ff_i64 n_elems,
                                          double (&g)[FF_NKP], double& b) {
   const ff_i64 ee = e >= 0 ? e : 0;
   double t[FF_GS];
@@ -294,7 +324,7 @@ __device__ __forceinline__ void ff_cload(int e, int i, const double* __restrict_
   for (int q = 0; q < FF_NKP; ++q) g[q] = q < FF_GS ? t[q < FF_GS ? q : 0] : 0.0;
   // entries b_0 .. b_{FF_NBPAD-1} came with the invariants (chunk-tail padding)
   b = i < FF_NBPAD ? t[FF_NKINV + (i < FF_NBPAD ? i : 0)]
-                   : ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)(i - FF_NBPAD) * n_elems + ee);
+                   : (sl < 0 ? 0.0 : ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)sl * n_elems + ee));
 }
 // FF_PRE: record ids of an item loaded with its header (the plan's pre_steps)
 #ifndef FF_WUNROLL
@@ -359,7 +389,7 @@ __device__ __noinline__ void ff_writeout_map(const double* __restrict__ st, int 
 // vector forms: lane = (row lane / FF_BS, trial component d = lane % FF_BS);
 // quantities of component block (c, d) at the even record offset dq:
 // FF_NBQ / 2 16-byte loads (no lane-dependent shuffling of a chunk)
-__device__ __forceinline__ void ff_vload(int e, int dq, int i, const double* __restrict__ einv, ff_i64 n_elems,
+__device__ __forceinline__ void ff_vload(int e, int dq, int sl, const double* __restrict__ einv, ff_i64 n_elems,
                                          double (&g)[FF_NBQ], double& b) {
   const ff_i64 ee = e >= 0 ? e : 0;
   const double* p = einv + ee * FF_GS + dq;
@@ -371,7 +401,7 @@ __device__ __forceinline__ void ff_vload(int e, int dq, int i, const double* __r
 #pragma unroll
   for (int k = 0; k < FF_NBQ; k += 2) ff_ld2(p + k, g[k], g[k + 1]);
 #endif
-  b = ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)i * n_elems + ee);
+  b = sl < 0 ? 0.0 : ff_ld1(einv + n_elems * FF_GSTORE + (ff_i64)sl * n_elems + ee);
 }
 // the warp's staging tile holds its rows in CSR order: row r (lanes
 // FF_BS r .. FF_BS r + FF_BS - 1) at r * SP3 + parity, value FF_BS * slot + d
@@ -505,7 +535,7 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
       for (int t = t0; t < t1; ++t) {
         const int q = order[t];
         os << "    double g" << q << "[FF_NKP], b" << q << "; ff_cload(e[" << q << "], " << k.local[q] * bs + cc
-             << ", einv, n_elems, g" << q << ", b" << q << ");\n";
+             << ", " << bslot[k.local[q] * bs + cc] << ", einv, n_elems, g" << q << ", b" << q << ");\n";
       }
       for (int t = t0; t < t1; ++t) {
         const int q = order[t];
@@ -595,7 +625,7 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
         for (int t = t0; t < t1; ++t) {
           const int q = order[t];
           os << "    double g" << q << "[FF_NBQ], b" << q << "; ff_vload(e[" << q << "], dq, "
-             << k.local[q] * bs + cc << ", einv, n_elems, g" << q << ", b" << q << ");\n";
+             << bslot[k.local[q] * bs + cc] << ", einv, n_elems, g" << q << ", b" << q << ");\n";
         }
         for (int t = t0; t < t1; ++t) {
           const int q = order[t];

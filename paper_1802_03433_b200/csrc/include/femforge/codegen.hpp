@@ -111,7 +111,13 @@ struct ElementPlan {
   // block_q[c * ncomp + d] (ff_vrow<a> in row_code, ff_block_q, FF_NBQ).
   int n_bq = 0;
   std::vector<int> block_q;
+  // load-vector entries that are identically zero (the record skips them)
+  std::vector<char> b_zero;
 };
+// Element-record slot of load-vector entry i in the SoA part (entries
+// below n_bpad ride in the invariants' chunk padding; -1: zero, not stored)
+// and the number of stored SoA entries.
+std::vector<int> record_bslots(const ElementPlan& plan, int n_local, int ncomp, int* n_soa = nullptr);
 
 ElementPlan plan_element(const fem::InstantiatedForm& f, const fem::QuadratureRule& rule,
                          Strategy strategy = Strategy::Auto);
