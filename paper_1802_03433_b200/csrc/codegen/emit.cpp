@@ -528,7 +528,9 @@ __device__ __noinline__ void ff_vwriteout(const double* __restrict__ st, const f
     };
     // record loads in flight per batch (registers: depth x the record size)
     const char* dk = bs == 1 ? std::getenv("FF_SDEPTH") : std::getenv("FF_VDEPTH");
-    const int depth = dk ? std::max(1, std::atoi(dk)) : (bs == 1 ? 8 : 2);
+    // (scalar forms: 9 -- NS 1.857 ms against 1.905 / 1.861 / 1.868 for 8 / 7 / 10,
+    // C3 0.807 vs 0.828 for 8)
+    const int depth = dk ? std::max(1, std::atoi(dk)) : (bs == 1 ? 9 : 2);
     for (int t0 = 0; t0 < k.steps; t0 += depth) {
       const int t1 = std::min(k.steps, t0 + depth);
       os << "  {\n";
