@@ -211,10 +211,10 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   if (fused && !std::getenv("FF_MINB_S"))
     src = "#define FF_MINB_S " + std::to_string((f->ncomp > 1 ? 12 : 14) / class_cwarps(f)) + "\n" + src;
   if (!fused && f->ncomp > 1) {
-    // split vector kernels: 16 warps/SM for short rows (128 registers), 8 for
-    // long rows (234 registers, no spills): config 5 29.96 ms against 37.35
-    // with 10 warps (168 registers + spills) and 37.33 with 12
-    if (!std::getenv("FF_MINB_S")) src = "#define FF_MINB_S " + std::to_string(16 / class_cwarps(f)) + "\n" + src;
+    // split vector kernels: 20 warps/SM for short rows (config 5 27.29 ms
+    // against 28.31 / 27.80 with 16 / 24), 8 for long rows (234 registers, no
+    // spills: 29.96 ms against 37.35 with 10 warps at 168 registers + spills)
+    if (!std::getenv("FF_MINB_S")) src = "#define FF_MINB_S " + std::to_string(20 / class_cwarps(f)) + "\n" + src;
     if (!std::getenv("FF_MINB_L")) src = "#define FF_MINB_L " + std::to_string(8 / class_cwarps(f)) + "\n" + src;
   }
   if (!std::getenv("FF_CWARPS")) src = "#define FF_CWARPS " + std::to_string(class_cwarps(f)) + "\n" + src;
