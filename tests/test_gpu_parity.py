@@ -492,6 +492,35 @@ def _elasticity_rbm(ff, ctx, sp, n):
     assert normwise(np.concatenate([x[3] for x in pieces]), rhs) <= TOL
 
 
+def test_elasticity_class_gather_row_blocks(ff, ctx):
+    """The vector class gather (lane-triple items of 10 node rows, CSR-order
+    staging, TMA row write-out, short/long-row kernels) over 3 node-aligned row
+    blocks with their halo elements: the concatenated blocks equal the 1-GPU
+    system (SURVEY §8e for config 5), every block compared with the oracle."""
+    n = 8
+    ctx.set_gather_classes(32)
+    try:
+        c, v, d, nd, rp, ci, val, rhs, *_ = _elasticity_system(ff, ctx, n, lam="2", mu="0.5")
+        parts, off, pieces = 3, 0, []
+        for part in range(parts):
+            sb, se = ff.partition_rows(nd, parts, part)
+            ids = ff.select_elements(d, sb, se)
+            sub = _elasticity_system(ff, ctx, n, 3 * sb, 3 * se, ids, lam="2", mu="0.5")
+            assert sub[-1].gather_info(sub[-2])["n_class_rows"] > 0
+            pieces.append((sub[4][:-1] + off, sub[5], sub[6], sub[7]))
+            off += sub[4][-1]
+    finally:
+        ctx.set_gather_classes(128)
+    rp_cat = np.concatenate([x[0] for x in pieces] + [np.array([off])])
+    assert np.array_equal(rp_cat, rp) and np.array_equal(np.concatenate([x[1] for x in pieces]), ci)
+    assert normwise(np.concatenate([x[2] for x in pieces]), val) <= TOL
+    assert normwise(np.concatenate([x[3] for x in pieces]), rhs) <= TOL
+    orp, oci = po.build_pattern(d, nd)
+    vrp, vci = po.block_pattern(orp, oci, 3)
+    ov, ob = po.assemble_elasticity(3, 2, 4, c, v, d, vrp, vci, lam=2.0, mu=0.5, force=(0.0, 0.0, -1.0))
+    assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
+
+
 def test_bench_two_ranks_on_one_gpu(ff):
     """The multi-rank bench path (row blocks, halo elements, global nnz, max
     over ranks) with 2 ranks sharing the one GPU over gloo: one JSON line, the
