@@ -521,6 +521,41 @@ def test_elasticity_class_gather_row_blocks(ff, ctx):
     assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
 
 
+@pytest.mark.parametrize("deg", [1, 2])
+@pytest.mark.parametrize("scatter", ["gather", "atomic"])
+def test_elasticity_2d_matches_oracle(ff, ctx, deg, scatter):
+    """2D vector elasticity (2 components: lane pairs in the class gather, the
+    CSR-order staging at pitch = 2 mod 16) on a 48^2 unit square, P1 and P2,
+    lambda != mu: block pattern bit-exact and values / RHS <= 1e-12 against
+    the C restatement, through the class + generic row gather and the atomic
+    scatter."""
+    n = 48
+    ctx.set_scatter(scatter)
+    ctx.set_gather_classes(64)
+    try:
+        xy, v = ff.unit_square_mesh(n)
+        if deg == 2:
+            d, nd = ff.p2_dofs(2, v, xy.shape[0])
+        else:
+            d, nd = v, xy.shape[0]
+        b, l = ff.elasticity_text(2, lam="2", mu="0.5", f=("1", "-1"))
+        f = ff.Form.blocked(ctx, 2, deg, 2, b, l)
+        m = ff.Mesh(ctx, 2, xy, v, d if deg == 2 else None, nd if deg == 2 else None, ncomp=2)
+        p = ff.Pattern(ctx, m)
+        rp, ci = p.export()
+        val, rhs = ff.assemble(f, m, p)
+        if scatter == "gather":
+            assert p.gather_info(m)["n_class_rows"] > 0
+    finally:
+        ctx.set_gather_classes(128)
+    orp, oci = po.build_pattern(d, nd)
+    vrp, vci = po.block_pattern(orp, oci, 2)
+    assert np.array_equal(rp, vrp) and np.array_equal(ci, vci)
+    # the default 2D rule is the reference's 3-point rule (fem.cpp:43-48), quad id 3
+    ov, ob = po.assemble_elasticity(2, deg, 3, xy, v, d, vrp, vci, lam=2.0, mu=0.5, force=(1.0, -1.0))
+    assert normwise(val, ov) <= TOL and normwise(rhs, ob) <= TOL
+
+
 def test_bench_two_ranks_on_one_gpu(ff):
     """The multi-rank bench path (row blocks, halo elements, global nnz, max
     over ranks) with 2 ranks sharing the one GPU over gloo: one JSON line, the
