@@ -243,7 +243,7 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
   if (bs < 1 || n_local % bs) throw CodegenError("class source: bad component count");
   if (bs > 1 && plan.n_bq <= 0) throw CodegenError("class source: vector forms need a block-uniform record");
   // classes are over (node) rows with nsc slots per incidence; vector forms
-  // gather each (test c, trial d) component pair as its own sub-row
+  // run the three trial components of a row in neighbouring lanes (vclass_fn)
   const int nsc = n_local / bs, nb = bs * bs;
   const std::vector<int> bslot = record_bslots(plan, n_local, bs);  // load-vector record slots
   std::ostringstream os;
@@ -331,9 +331,8 @@ __device__ __forceinline__ void ff_cload(int e, int i, int sl, const double* __r
 #define FF_WUNROLL 32  // write-out loop unroll (NS 2.484 vs 2.514 ms with 4, run 94)
 #endif
 constexpr int ff_wunroll = FF_WUNROLL;  // (#pragma unroll takes a constant expression, not a macro)
-// CSR value stores: streaming (evict-first) for scalar rows, which are written
-// whole; vector sub-rows fill every FF_BS-th value, so their lines must stay
-// in L2 until the other component pairs' CTAs complete them
+// CSR value stores of the scalar write-out: streaming (evict-first), rows are
+// written whole (vector forms write their rows by TMA, ff_vwriteout)
 __device__ __forceinline__ void ff_stv(double* p, double v) {
 #if FF_BS == 1
   __stcs(p, v);
