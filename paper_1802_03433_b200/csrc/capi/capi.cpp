@@ -219,11 +219,6 @@ void ensure_class_module(ff_form* f, ff_pattern* p) {
   }
   if (!std::getenv("FF_CWARPS")) src = "#define FF_CWARPS " + std::to_string(class_cwarps(f)) + "\n" + src;
   // tuning knobs (defaults in the source): FF_MINB_S, FF_MINB_L
-  // element records through L1: with records in first-touch order the lanes of
-  // a step read neighbouring records (2.095 -> 2.082 ms at the north star);
-  // FF_EINV_NA=1 streams them past L1 (the round-1 default, -6 % before the
-  // first-touch order)
-  if (std::getenv("FF_EINV_NA") && f->ncomp == 1) src = "#define FF_EINV_NA 1\n" + src;
   for (const char* knob : {"FF_MINB_S", "FF_MINB_L", "FF_WUNROLL", "FF_CWARPS"})
     if (const char* v = std::getenv(knob))
       src = "#define " + std::string(knob) + " " + std::to_string(std::max(1, std::atoi(v))) + "\n" + src;
@@ -289,7 +284,7 @@ void ensure_gather_plan(ff_pattern* p, const ff_mesh* m) {
                                                         4096, ctx->sm_count, ctx->stream, &p->gather,
                                                         cmin > 0 ? static_cast<int>(std::min<int64_t>(cmin, 1 << 30))
                                                                  : (1 << 30),
-                                                        cmin > 0 ? 64 : 0, !std::getenv("FF_NO_EORDER"),
+                                                        cmin > 0 ? 64 : 0, true,
                                                         p->bs == 1 ? std::getenv("FF_SPLIT_CLASSES") != nullptr
                                                                    : !vector_fused(),
                                                         &order_fn, 0.0005, p->bs);

@@ -273,18 +273,9 @@ std::string emit_class_source(const ElementPlan& plan, int n_local, const std::v
      << "template <int I>\n__device__ __forceinline__ void ff_row(const double* __restrict__ g, double* __restrict__ v);\n"
      << plan.row_code
      << R"(
-#ifdef FF_EINV_NA  // element records streamed past L1 (no allocation)
-__device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, double& c, double& d) {
-  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
-}
-__device__ __forceinline__ void ff_ld2(const double* p, double& a, double& b) {
-  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
-}
-// load-vector entries stay L1-allocating: the lanes of a class item and the
-// items of a CTA read neighbouring elements' entry i, which share lines
-// (2.81 -> 2.61 ms at the north star against no-allocate, run 72)
-__device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
-#else
+// element records through L1: in first-touch order the lanes of a step read
+// neighbouring records (2.095 -> 2.082 ms at the north star against the
+// round-1 L1::no_allocate stream)
 __device__ __forceinline__ void ff_ld4(const double* p, double& a, double& b, double& c, double& d) {
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
@@ -292,7 +283,6 @@ __device__ __forceinline__ void ff_ld2(const double* p, double& a, double& b) {
   asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
 }
 __device__ __forceinline__ double ff_ld1(const double* p) { return __ldg(p); }
-#endif
 #if defined(FF_ABL) && (FF_ABL & 8)  // ablation (timing analysis only; results wrong)
 #define ff_ld1(p) (1.0)
 #endif

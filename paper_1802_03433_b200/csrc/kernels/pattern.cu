@@ -729,11 +729,10 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     return done(err);
   phase("row sort");
   // ---- row classes (signature counts on the host, verified on the device)
-  std::vector<int32_t> morton(n_rows), cls_h(n_rows, -1);
+  std::vector<int32_t> cls_h(n_rows, -1);
   {
     // signature counts on the device: sort + run-length encode; the host sees
     // only the distinct signatures
-    if (n_rows > 0) cudaMemcpyAsync(morton.data(), order, n_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     std::vector<uint64_t> usig;
     std::vector<int32_t> ucnt;
     if (n_rows > 0) {
@@ -857,16 +856,15 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
     // interleaved by the Morton position of their first row
     // class rows in row (DOF) order: on a lattice numbering the 32 rows of an
     // item are a line of same-class DOFs, so at every step the lanes' elements
-    // are neighbours along that line (FF_ROW_ITEMS=0: Morton order of the DOF
+    // are neighbours along that line (measured against the Morton order of the DOF
     // points; NS 2.49 -> 2.09 ms together with the first-touch records below)
-    const bool row_items = !std::getenv("FF_ROW_ITEMS") || std::atoi(std::getenv("FF_ROW_ITEMS")) != 0;
     // rows per class item: 32, or 32 / row_lanes rows of row_lanes lanes each
     // (vector forms: the trial components of a row in neighbouring lanes)
     const int rpi = 32 / std::max(1, row_lanes);
     std::vector<std::vector<int32_t>> members(n_cls);
     std::vector<std::vector<int64_t>> first_pos(n_cls);
     for (int64_t pos = 0; pos < n_rows; ++pos) {
-      const int32_t r = row_items ? static_cast<int32_t>(pos) : morton[pos];
+      const int32_t r = static_cast<int32_t>(pos);
       const int c = cls_h[r];
       if (c < 0) continue;
       if (members[c].size() % rpi == 0) first_pos[c].push_back(pos);
@@ -951,9 +949,8 @@ cudaError_t build_gather_plan(const double* d_coords, const int32_t* d_vconn, in
       // lane): the elements the 32 lanes of one step read are then stored side
       // by side, and a warp's 32-byte record loads cover 8 consecutive lines
       // instead of 32 scattered ones (the class kernel was bound by L1 tag
-      // wavefronts of those scattered loads). FF_FIRST_TOUCH=0: Morton order.
-      const bool ftouch = !std::getenv("FF_FIRST_TOUCH") || std::atoi(std::getenv("FF_FIRST_TOUCH")) != 0;
-      if (ftouch && ne > 0) {
+      // wavefronts of those scattered loads).
+      if (ne > 0) {
         unsigned long long* first = nullptr;
         uint64_t *ek = nullptr, *ek2 = nullptr;
         int32_t *eid = nullptr, *eorder_new = nullptr;
