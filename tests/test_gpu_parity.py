@@ -492,6 +492,24 @@ def _elasticity_rbm(ff, ctx, sp, n):
     assert normwise(np.concatenate([x[3] for x in pieces]), rhs) <= TOL
 
 
+def test_elasticity_zero_load_vector(ff, ctx):
+    """A load vector that is identically zero in every component (f = 0): the
+    element record stores no load-vector entry at all, the row kernels never
+    load one, and the RHS comes out exactly zero; the matrix equals the atomic
+    scatter's."""
+    n = 8
+    ctx.set_gather_classes(64)
+    try:
+        *_, val_a, rhs_a, f, m, p = _elasticity_system(ff, ctx, n, force=("0", "0", "0"), scatter="atomic")
+        ctx.set_scatter("gather")
+        val_g, rhs_g = ff.assemble(f, m, p)
+        assert p.gather_info(m)["n_class_rows"] > 0
+    finally:
+        ctx.set_gather_classes(128)
+    assert not rhs_g.any() and not rhs_a.any()
+    assert normwise(val_g, val_a) <= 1e-15
+
+
 def test_elasticity_class_gather_row_blocks(ff, ctx):
     """The vector class gather (lane-triple items of 10 node rows, CSR-order
     staging, TMA row write-out, short/long-row kernels) over 3 node-aligned row
